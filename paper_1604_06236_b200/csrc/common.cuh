@@ -1,0 +1,134 @@
+// common.cuh — shared device/host helpers for libnfft45 (sm_100a, fp64).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/nfft45.h"
+
+namespace nfft45 {
+
+// ----------------------------------------------------------------- errors
+
+void set_error(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define NFFT_CUDA(call)                                 \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+#define NFFT_CHECK(call)             \
+  do {                               \
+    int _s = (call);                 \
+    if (_s != NFFT45_OK) return _s;  \
+  } while (0)
+
+// Every kernel launch of this library goes through LAUNCH so that
+// nfft45_launch_count() can report how many of OUR kernels ran.
+extern std::atomic<int64_t> g_launches;
+#define LAUNCH(kernel, grid, block, smem, stream, ...)                     \
+  do {                                                                     \
+    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);            \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                    \
+    cudaError_t _le = cudaGetLastError();                                  \
+    if (_le != cudaSuccess) return cuda_fail(_le, #kernel);                \
+  } while (0)
+
+// ------------------------------------------------------- complex (double2)
+
+__host__ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__host__ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__host__ __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__host__ __device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+__host__ __device__ __forceinline__ double2 cscale(double2 a, double s) {
+  return make_double2(a.x * s, a.y * s);
+}
+// acc += w * y (w real)
+__host__ __device__ __forceinline__ void caxpy(double2& acc, double w, double2 y) {
+  acc.x = fma(w, y.x, acc.x);
+  acc.y = fma(w, y.y, acc.y);
+}
+// complex division a / b (straightforward; b is never tiny on our paths)
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  double d = fma(b.x, b.x, b.y * b.y);
+  double inv = 1.0 / d;
+  return make_double2(fma(a.x, b.x, a.y * b.y) * inv, fma(a.y, b.x, -a.x * b.y) * inv);
+}
+
+// ------------------------------------------------------------ phases
+
+// frac(K * t) in [-1/2, 1/2], exact up to one rounding: the product is split
+// with an FMA (TwoProduct) so non-dyadic K (e.g. 3*2^k) keeps full accuracy;
+// for dyadic K the error term is exactly zero.  Replaces the 80-bit mod-1
+// reduction of gridding.py:26-29.
+__device__ __forceinline__ double turns_of_product(double K, double t) {
+  double p = K * t;
+  double e = fma(K, t, -p);
+  double r = p - rint(p);
+  return r + e;
+}
+
+// e^{2 pi i x} for x in turns (|x| <= 1/2 keeps sincospi's argument exact).
+__device__ __forceinline__ double2 cis_turns(double x) {
+  double s, c;
+  sincospi(2.0 * x, &s, &c);
+  return make_double2(c, s);
+}
+
+// Fine-grid geometry of one node: u = n t = i0 + f, i0 = rint(u), |f| <= 1/2
+// (gridding.py:57-69).  n t is split with an FMA so f is exact to one rounding
+// even when n is not a power of two.
+struct NodeGeo {
+  int i0;
+  double f;
+};
+__device__ __forceinline__ NodeGeo node_geo(double t, double n) {
+  double p = n * t;
+  double e = fma(n, t, -p);
+  double r = rint(p);
+  NodeGeo g;
+  g.i0 = (int)r;
+  g.f = (p - r) + e;
+  return g;
+}
+
+// ------------------------------------------------------------ misc
+
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+
+// Gaussian window parameters (gridding.py:32-34): b = m / (2 sqrt2 pi);
+// weights exp(-d^2 / 4b), deconvolution exp(b (2 pi nu / n)^2) / sqrt(4 pi b).
+struct Window {
+  int m;          // half-width
+  double b;       // shape
+  double alpha;   // 1 / (4 b)
+  static Window make(int m) {
+    Window w;
+    w.m = m;
+    w.b = (double)m / (2.0 * 1.4142135623730951 * 3.141592653589793);
+    w.alpha = 1.0 / (4.0 * w.b);
+    return w;
+  }
+};
+
+// Maximum half-width handled by the unrolled fast paths; wider windows use
+// the generic (per-tap exp) kernels.
+constexpr int kFastM = 14;
+
+}  // namespace nfft45

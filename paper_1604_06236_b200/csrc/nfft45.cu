@@ -1,0 +1,719 @@
+// nfft45.cu — C ABI (include/nfft45.h): node sets, forward NFFTs, Lagrange
+// quantities, inverse plans and the type-4/5 solves with refinement.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "fft.cuh"
+#include "ops.cuh"
+
+namespace nfft45 {
+
+std::atomic<int64_t> g_launches{0};
+static thread_local std::string tl_err;
+
+void set_error(int code, const std::string& msg) {
+  (void)code;
+  tl_err = msg;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  tl_err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  return NFFT45_ERR_CUDA;
+}
+
+static int fail(int code, const std::string& msg) {
+  tl_err = msg;
+  return code;
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  int status = NFFT45_OK;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    cudaError_t e = cudaSetDevice(dev);
+    if (e != cudaSuccess) status = cuda_fail(e, "cudaSetDevice");
+    static std::once_flag once[64];
+    if (status == NFFT45_OK && dev < 64) {
+      std::call_once(once[dev], [dev]() {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          uint64_t thr = UINT64_MAX;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+      });
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Stream-ordered scratch buffer.
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t st;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  int alloc(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    return NFFT45_OK;
+  }
+  double2* c() { return reinterpret_cast<double2*>(p); }
+  double* d() { return reinterpret_cast<double*>(p); }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+// Lagrange guards (lagrange.py:25-29).
+static const double kReVLimit = std::log(1.79769313486231570815e308) - 16.0;
+static const double kDerivativeFloor = 1e-300;
+
+}  // namespace nfft45
+
+using namespace nfft45;
+
+struct nfft45_grid {
+  GridDev d;
+};
+
+struct nfft45_plan {
+  const nfft45_grid* g;
+  int64_t P;
+  double a;
+  int eta;
+  int m;
+  double2* tables;  // one allocation holding everything below
+  double2 *v, *ks, *L, *dL, *nw, *decay, *coef;
+  double2 *c5, *c4;  // ascending-node fused factors nw * cis(-/+ K t)
+};
+
+// ------------------------------------------------------------- kernels
+
+namespace nfft45 {
+
+__global__ void k_log_series(double2* lam, int64_t R, double a) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= R) return;
+  // lagrange.py:52  lam[1:] = -exp(-2 pi p a) / p
+  double v = p == 0 ? 0.0 : -exp(-2.0 * 3.141592653589793 * (double)p * a) / (double)p;
+  lam[p] = make_double2(v, 0.0);
+}
+
+// ks = exp(i pi P + 2 pi i sum t + v) (lagrange.py:92-97).  The constant
+// phase arrives in turns (from a double-double instant sum) and Im v is
+// split into whole turns plus an exactly computed remainder, so the
+// argument handed to sincospi is O(1) however large |Im v| grows.
+__global__ void k_kernel_samples(const double2* __restrict__ v, double2* __restrict__ ks, int64_t P,
+                                 double c_turns, double* __restrict__ max_re) {
+  __shared__ double red[256];
+  const double kTwoPiHi = 6.283185307179586232, kTwoPiLo = 2.4492935982947064e-16;
+  const double kInvTwoPi = 0.15915494309189533577;
+  double mx = 0.0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < P; q += (int64_t)gridDim.x * blockDim.x) {
+    double2 x = v[q];
+    mx = fmax(mx, fabs(x.x));
+    double tv = x.y * kInvTwoPi;
+    double resid = fma(-tv, kTwoPiHi, x.y) - tv * kTwoPiLo;  // Im v - 2 pi tv
+    double f = (tv - rint(tv)) + c_turns;
+    f -= rint(f);
+    double s, c;
+    sincospi(2.0 * f + resid * 0.31830988618379067154, &s, &c);
+    double mag = exp(x.x);
+    ks[q] = make_double2(mag * c, mag * s);
+  }
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) max_re[blockIdx.x] = red[0];
+}
+
+// Eq. 43: L = (FFT(ks) - P e^{-2 pi P a} delta_0) * e^{2 pi p a} / P, in place.
+__global__ void k_coeff_fix(double2* L, int64_t P, double a) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  double2 x = L[p];
+  if (p == 0) x.x -= (double)P * exp(-2.0 * 3.141592653589793 * (double)P * a);
+  double boost = exp(2.0 * 3.141592653589793 * (double)p * a);
+  double s = boost / (double)P;
+  L[p] = make_double2(x.x * s, x.y * s);
+}
+
+// dcoef_k = (k+1) L_{k+1} (k < P-1), dcoef_{P-1} = P (lagrange.py:150-152)
+__global__ void k_dcoef(const double2* __restrict__ L, double2* __restrict__ d, int64_t P) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= P) return;
+  if (k < P - 1) {
+    double2 x = L[k + 1];
+    double f = (double)(k + 1);
+    d[k] = make_double2(f * x.x, f * x.y);
+  } else {
+    d[k] = make_double2((double)P, 0.0);
+  }
+}
+
+__global__ void k_min_abs(const double2* __restrict__ x, int64_t n, double* __restrict__ out) {
+  __shared__ double red[256];
+  double mn = INFINITY;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    mn = fmin(mn, hypot(x[i].x, x[i].y));
+  red[threadIdx.x] = mn;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = red[0];
+}
+
+// Plan scalars per node (inverse.py:70-78) and the fused solve factors.
+__global__ void k_plan_tables(const double* __restrict__ t, const double* __restrict__ ts,
+                              const int* __restrict__ perm, const double2* __restrict__ dL, int64_t P, double a,
+                              double2* __restrict__ nw, double2* __restrict__ decay, double2* __restrict__ coef) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= P) return;
+  const double twopi = 2.0 * 3.141592653589793;
+  // decay = e^{-2 pi p a}; coef_scale = (1/decay)/P
+  double dec = exp(-twopi * (double)q * a);
+  decay[q] = make_double2(dec, 0.0);
+  coef[q] = make_double2((1.0 / dec) / (double)P, 0.0);
+  // h = 1 / (cis(-P t) e^{-2 pi P a} - 1);  nw = h / (L' cis(t))
+  double tq = t[q];
+  double2 cpt = cis_turns(-turns_of_product((double)P, tq));
+  double damp = exp(-twopi * (double)P * a);
+  double2 den = make_double2(cpt.x * damp - 1.0, cpt.y * damp);
+  double2 h = cdiv(make_double2(1.0, 0.0), den);
+  double2 ct = cis_turns(tq >= 0.5 ? tq - 1.0 : tq);
+  double2 w = cdiv(h, cmul(dL[q], ct));
+  nw[q] = w;
+}
+
+__global__ void k_fused_factors(const double* __restrict__ ts, const int* __restrict__ perm,
+                                const double2* __restrict__ nw, int64_t P, double K, double2* __restrict__ c5,
+                                double2* __restrict__ c4) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  double x = turns_of_product(K, ts[i]);
+  double2 w = nw[perm[i]];
+  c5[i] = cmul(w, cis_turns(-x));
+  c4[i] = cmul(w, cis_turns(x));
+}
+
+__global__ void k_max_reduce(const double* in, int n, double* out, int is_min) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double r = is_min ? INFINITY : 0.0;
+    for (int i = 0; i < n; i++) r = is_min ? fmin(r, in[i]) : fmax(r, in[i]);
+    *out = r;
+  }
+}
+
+}  // namespace nfft45
+
+// ------------------------------------------------------- internal steps
+
+namespace nfft45 {
+
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// A = type1(grid, a, R) (forward.py:26-64) with optional fold onto P,
+// optional spectral table and optional subtraction: the shared backbone of
+// nfft_type1, nonuniform_conv, compute_v_samples and the type-4 refinement.
+static int type1_core(const GridDev& g, const double2* a, int64_t batch, int64_t R, int m, int64_t P,
+                      const double2* tab, const double2* sub, double2* out, cudaStream_t st) {
+  const int64_t n = 2 * R;
+  const int64_t K = R / 2;
+  Window win = Window::make(m);
+  Scratch H(st);
+  NFFT_CHECK(H.alloc(sizeof(double2) * batch * n));
+  NodeFactor f{nullptr, (double)K, -1};
+  NFFT_CHECK(spread(g, n, win, a, batch, f, H.c(), st));
+  NFFT_CHECK(fft_run(H.c(), H.c(), batch, n, -1, nullptr, nullptr, st));
+  NFFT_CHECK(band_fold(H.c(), n, R, K, P, win, true, tab, sub, out, batch, st));
+  return NFFT45_OK;
+}
+
+// s = type2(S, grid) (forward.py:67-102), optional subtraction.
+static int type2_core(const GridDev& g, const double2* Sc, int64_t batch, int64_t P, int m, const double2* sub,
+                      double2* out, cudaStream_t st) {
+  const int64_t n = 2 * P;
+  const int64_t K = P / 2;
+  Window win = Window::make(m);
+  Scratch F(st);
+  NFFT_CHECK(F.alloc(sizeof(double2) * batch * n));
+  NFFT_CHECK(band_pad(Sc, P, n, K, win, true, nullptr, F.c(), batch, st));
+  NFFT_CHECK(fft_run(F.c(), F.c(), batch, n, +1, nullptr, nullptr, st));
+  NodeFactor f{nullptr, (double)K, +1};
+  NFFT_CHECK(gather(g, n, win, F.c(), batch, f, sub, out, st));
+  return NFFT45_OK;
+}
+
+static int v_core(const GridDev& g, double a, int eta, int m, double2* v, cudaStream_t st) {
+  const int64_t P = g.Q;
+  const int64_t R = (int64_t)eta * P;
+  Scratch lam(st), V(st);
+  NFFT_CHECK(lam.alloc(sizeof(double2) * R));
+  NFFT_CHECK(V.alloc(sizeof(double2) * P));
+  LAUNCH(k_log_series, (unsigned)ceil_div(R, 256), 256, 0, st, lam.c(), R, a);
+  NFFT_CHECK(type1_core(g, nullptr, 1, R, m, P, lam.c(), nullptr, V.c(), st));
+  NFFT_CHECK(fft_run(V.c(), v, 1, P, +1, nullptr, nullptr, st));
+  return NFFT45_OK;
+}
+
+static double const_turns(const GridDev& g) {
+  // i pi P + 2 pi i sum(t)  ->  turns P/2 + sum t  (mod 1)
+  double half = (g.Q % 2) ? 0.5 : 0.0;
+  double hi = g.sum_hi - std::rint(g.sum_hi);
+  double c = (hi + half) + g.sum_lo;
+  return c - std::rint(c);
+}
+
+static int ks_core(const GridDev& g, const double2* v, double2* ks, double* d_maxre, cudaStream_t st) {
+  const int64_t P = g.Q;
+  int blocks = (int)std::min<int64_t>(ceil_div(P, 256), 1024);
+  Scratch part(st);
+  NFFT_CHECK(part.alloc(sizeof(double) * blocks));
+  LAUNCH(k_kernel_samples, blocks, 256, 0, st, v, ks, P, const_turns(g), part.d());
+  LAUNCH(k_max_reduce, 1, 32, 0, st, part.d(), blocks, d_maxre, 0);
+  return NFFT45_OK;
+}
+
+static int coeff_core(const double2* ks, int64_t P, double a, double2* L, cudaStream_t st) {
+  NFFT_CHECK(fft_run(ks, L, 1, P, -1, nullptr, nullptr, st));
+  LAUNCH(k_coeff_fix, (unsigned)ceil_div(P, 256), 256, 0, st, L, P, a);
+  return NFFT45_OK;
+}
+
+static int deriv_core(const GridDev& g, const double2* L, int m, double2* dL, double* d_minabs, cudaStream_t st) {
+  const int64_t P = g.Q;
+  Scratch d(st), part(st);
+  NFFT_CHECK(d.alloc(sizeof(double2) * P));
+  LAUNCH(k_dcoef, (unsigned)ceil_div(P, 256), 256, 0, st, L, d.c(), P);
+  NFFT_CHECK(type2_core(g, d.c(), 1, P, m, nullptr, dL, st));
+  int blocks = (int)std::min<int64_t>(ceil_div(P, 256), 1024);
+  NFFT_CHECK(part.alloc(sizeof(double) * blocks));
+  LAUNCH(k_min_abs, blocks, 256, 0, st, dL, P, part.d());
+  LAUNCH(k_max_reduce, 1, 32, 0, st, part.d(), blocks, d_minabs, 1);
+  return NFFT45_OK;
+}
+
+static int check_guards(const double* d_guard, int have_re, int have_dl, cudaStream_t st) {
+  double h[2] = {0.0, INFINITY};
+  NFFT_CUDA(cudaMemcpyAsync(h, d_guard, sizeof(h), cudaMemcpyDeviceToHost, st));
+  NFFT_CUDA(cudaStreamSynchronize(st));
+  char buf[256];
+  if (have_re && !(h[0] <= kReVLimit)) {
+    snprintf(buf, sizeof buf,
+             "|Re v| reaches %.1f, beyond the exp() overflow margin (%.1f); the grid is too strongly clustered "
+             "for this damping",
+             h[0], kReVLimit);
+    return fail(NFFT45_ERR_KERNEL_OVERFLOW, buf);
+  }
+  if (have_dl && !(h[1] >= kDerivativeFloor)) {
+    snprintf(buf, sizeof buf, "derivative sample magnitude %.3e below 1e-300; interpolation weights would overflow",
+             h[1]);
+    return fail(NFFT45_ERR_SINGULAR_DERIVATIVE, buf);
+  }
+  return NFFT45_OK;
+}
+
+// ------------------------------------------------------------- solves
+
+static int type5_core(const nfft45_plan* p, const double2* s, int64_t batch, double2* out, cudaStream_t st) {
+  const GridDev& g = p->g->d;
+  const int64_t P = p->P, n = 2 * P, K = P / 2;
+  Window win = Window::make(p->m);
+  Scratch H(st), V(st);
+  NFFT_CHECK(H.alloc(sizeof(double2) * batch * n));
+  NFFT_CHECK(V.alloc(sizeof(double2) * batch * P));
+  NodeFactor f{p->c5, 0.0, 0};
+  NFFT_CHECK(spread(g, n, win, s, batch, f, H.c(), st));                                  // forward.py:47-54
+  NFFT_CHECK(fft_run(H.c(), H.c(), batch, n, -1, nullptr, nullptr, st));                  // forward.py:55
+  NFFT_CHECK(band_fold(H.c(), n, P, K, P, win, true, p->decay, nullptr, V.c(), batch, st));  // :64, :153
+  NFFT_CHECK(fft_run(V.c(), V.c(), batch, P, +1, nullptr, p->ks, st));                    // :162, inverse.py:114
+  NFFT_CHECK(fft_run(V.c(), out, batch, P, -1, nullptr, p->coef, st));                    // inverse.py:115
+  return NFFT45_OK;
+}
+
+static int type4_core(const nfft45_plan* p, const double2* A, int64_t batch, double2* out, cudaStream_t st) {
+  const GridDev& g = p->g->d;
+  const int64_t P = p->P, n = 2 * P, K = P / 2;
+  Window win = Window::make(p->m);
+  Scratch V(st), F(st);
+  NFFT_CHECK(V.alloc(sizeof(double2) * batch * P));
+  NFFT_CHECK(F.alloc(sizeof(double2) * batch * n));
+  NFFT_CHECK(fft_run(A, V.c(), batch, P, +1, p->decay, p->ks, st));       // inverse.py:132-133
+  NFFT_CHECK(fft_run(V.c(), V.c(), batch, P, -1, nullptr, p->coef, st));   // inverse.py:134
+  NFFT_CHECK(band_pad(V.c(), P, n, K, win, true, nullptr, F.c(), batch, st));  // forward.py:88-89
+  NFFT_CHECK(fft_run(F.c(), F.c(), batch, n, +1, nullptr, nullptr, st));  // forward.py:90
+  NodeFactor f{p->c4, 0.0, 0};
+  NFFT_CHECK(gather(g, n, win, F.c(), batch, f, nullptr, out, st));        // forward.py:91-102, inverse.py:143
+  return NFFT45_OK;
+}
+
+typedef int (*SolveFn)(const nfft45_plan*, const double2*, int64_t, double2*, cudaStream_t);
+
+// Section V refinement (inverse.py:146-162).  fwd5: residual via type-2
+// (sample domain) else via type-1 of length P (spectrum domain).
+static int refine_core(const nfft45_plan* p, const double2* data, int64_t batch, int passes, double2* out,
+                       bool type5, cudaStream_t st) {
+  SolveFn solve = type5 ? type5_core : type4_core;
+  NFFT_CHECK(solve(p, data, batch, out, st));
+  if (passes <= 0) return NFFT45_OK;
+  const GridDev& g = p->g->d;
+  const int64_t P = p->P;
+  Scratch r(st), y(st), norms(st);
+  NFFT_CHECK(r.alloc(sizeof(double2) * batch * P));
+  NFFT_CHECK(y.alloc(sizeof(double2) * batch * P));
+  NFFT_CHECK(norms.alloc(sizeof(double) * batch * passes));
+  for (int pass = 0; pass < passes; pass++) {
+    if (type5) NFFT_CHECK(type2_core(g, out, batch, P, p->m, data, r.c(), st));
+    else NFFT_CHECK(type1_core(g, out, batch, P, p->m, P, nullptr, data, r.c(), st));
+    if (passes >= 2) NFFT_CHECK(row_norms(r.c(), P, batch, norms.d() + (int64_t)pass * batch, st));
+    NFFT_CHECK(solve(p, r.c(), batch, y.c(), st));
+    NFFT_CHECK(csub_batch(out, y.c(), out, batch * P, st));
+  }
+  if (passes >= 2) {
+    std::vector<double> h((size_t)batch * passes);
+    NFFT_CUDA(cudaMemcpyAsync(h.data(), norms.d(), sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+    NFFT_CUDA(cudaStreamSynchronize(st));
+    for (int pass = 1; pass < passes; pass++)
+      for (int64_t b = 0; b < batch; b++) {
+        double prev = h[(size_t)(pass - 1) * batch + b], cur = h[(size_t)pass * batch + b];
+        if (cur > prev) {
+          char buf[200];
+          snprintf(buf, sizeof buf,
+                   "residual norm grew between passes (%.3e -> %.3e); method error >= 1 at these parameters", prev,
+                   cur);
+          return fail(NFFT45_ERR_NON_CONVERGENCE, buf);
+        }
+      }
+  }
+  return NFFT45_OK;
+}
+
+}  // namespace nfft45
+
+// ================================================================== C ABI
+
+extern "C" {
+
+const char* nfft45_last_error(void) { return tl_err.c_str(); }
+int nfft45_version(void) { return 100; }
+int64_t nfft45_launch_count(void) { return g_launches.load(); }
+
+int nfft45_validate_grid(const double* t, int64_t Q, double min_gap, int64_t* order) {
+  char buf[256];
+  if (Q < 1 || !t) return fail(NFFT45_ERR_OUT_OF_RANGE, "grid must be a nonempty 1-D sequence of instants");
+  for (int64_t i = 0; i < Q; i++)
+    if (!std::isfinite(t[i])) return fail(NFFT45_ERR_OUT_OF_RANGE, "grid contains non-finite instants");
+  for (int64_t i = 0; i < Q; i++)
+    if (t[i] < 0.0 || t[i] >= 1.0) {
+      snprintf(buf, sizeof buf, "instant %.17g outside the fundamental period [0, 1)", t[i]);
+      return fail(NFFT45_ERR_OUT_OF_RANGE, buf);
+    }
+  std::vector<int64_t> ord((size_t)Q);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return t[a] < t[b]; });
+  if (Q > 1) {
+    double gmin = INFINITY;
+    int64_t at = 0;
+    for (int64_t i = 0; i < Q; i++) {
+      double gap = i + 1 < Q ? t[ord[i + 1]] - t[ord[i]] : 1.0 - t[ord[Q - 1]] + t[ord[0]];
+      if (gap < gmin) { gmin = gap; at = i; }
+    }
+    if (gmin < min_gap) {
+      snprintf(buf, sizeof buf, "circular gap %.3e below floor %.3e near t=%.17g", gmin, min_gap, t[ord[at]]);
+      return fail(NFFT45_ERR_DUPLICATE_NODE, buf);
+    }
+  }
+  if (order) std::copy(ord.begin(), ord.end(), order);
+  return NFFT45_OK;
+}
+
+int nfft45_grid_create(const double* t, const int64_t* order, int64_t Q, int device, nfft45_grid** out) {
+  if (!out || !t || !order || Q < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid grid arguments");
+  if (Q > (int64_t)1 << 30) return fail(NFFT45_ERR_INVALID_ARGUMENT, "grid too large (max 2^30 nodes)");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(NFFT45_ERR_NO_DEVICE, "no CUDA device available (the product path has no CPU fallback)");
+  DeviceGuard dg(device);
+  if (dg.status) return dg.status;
+  std::vector<double> ts((size_t)Q);
+  std::vector<int> perm((size_t)Q);
+  for (int64_t i = 0; i < Q; i++) {
+    perm[i] = (int)order[i];
+    ts[i] = t[order[i]];
+  }
+  // double-double running sum of the instants (caller order; lagrange.py:92)
+  double hi = 0.0, lo = 0.0;
+  for (int64_t i = 0; i < Q; i++) {
+    double s = hi + t[i];
+    double bb = s - hi;
+    double err = (hi - (s - bb)) + (t[i] - bb);
+    hi = s;
+    lo += err;
+  }
+  nfft45_grid* g = new nfft45_grid();
+  g->d.device = device;
+  g->d.Q = Q;
+  g->d.sum_hi = hi;
+  g->d.sum_lo = lo;
+  size_t bytes = sizeof(double) * 2 * Q + sizeof(int) * Q;
+  char* base = nullptr;
+  cudaError_t e = cudaMalloc(&base, bytes);
+  if (e != cudaSuccess) {
+    delete g;
+    return cuda_fail(e, "cudaMalloc(grid)");
+  }
+  g->d.t = reinterpret_cast<double*>(base);
+  g->d.ts = g->d.t + Q;
+  g->d.perm = reinterpret_cast<int*>(g->d.ts + Q);
+  e = cudaMemcpy(g->d.t, t, sizeof(double) * Q, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(g->d.ts, ts.data(), sizeof(double) * Q, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(g->d.perm, perm.data(), sizeof(int) * Q, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(base);
+    delete g;
+    return cuda_fail(e, "cudaMemcpy(grid)");
+  }
+  *out = g;
+  return NFFT45_OK;
+}
+
+void nfft45_grid_destroy(nfft45_grid* g) {
+  if (!g) return;
+  DeviceGuard dg(g->d.device);
+  cudaFree(g->d.t);
+  delete g;
+}
+
+int64_t nfft45_grid_size(const nfft45_grid* g) { return g ? g->d.Q : 0; }
+
+#define C2(p) reinterpret_cast<const double2*>(p)
+#define D2(p) reinterpret_cast<double2*>(p)
+
+int nfft45_type1(const nfft45_grid* g, const double* a, int64_t batch, int64_t R, int m, double* out, void* st) {
+  if (!g || R < 1 || m < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid type-1 arguments");
+  DeviceGuard dg(g->d.device);
+  if (dg.status) return dg.status;
+  return type1_core(g->d, C2(a), batch, R, m, R, nullptr, nullptr, D2(out), S(st));
+}
+
+int nfft45_type2(const nfft45_grid* g, const double* Sc, int64_t batch, int64_t P, int m, double* out, void* st) {
+  if (!g || P < 1 || m < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid type-2 arguments");
+  DeviceGuard dg(g->d.device);
+  if (dg.status) return dg.status;
+  return type2_core(g->d, C2(Sc), batch, P, m, nullptr, D2(out), S(st));
+}
+
+int nfft45_nonuniform_conv(const nfft45_grid* g, const double* a, int64_t batch, const double* lam, int64_t R,
+                           int64_t P, int m, double* out, void* st) {
+  if (!g || P < 1 || R < 1 || m < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid convolution arguments");
+  if (R % P) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "kernel length %lld is not a multiple of output length %lld", (long long)R,
+             (long long)P);
+    return fail(NFFT45_ERR_SIZE_MISMATCH, buf);
+  }
+  DeviceGuard dg(g->d.device);
+  if (dg.status) return dg.status;
+  cudaStream_t s = S(st);
+  Scratch V(s);
+  NFFT_CHECK(V.alloc(sizeof(double2) * batch * P));
+  NFFT_CHECK(type1_core(g->d, C2(a), batch, R, m, P, C2(lam), nullptr, V.c(), s));
+  return fft_run(V.c(), D2(out), batch, P, +1, nullptr, nullptr, s);
+}
+
+int nfft45_type1_direct(const nfft45_grid* g, const double* a, int64_t batch, int64_t R, double* out, void* st) {
+  if (!g || R < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid direct type-1 arguments");
+  DeviceGuard dg(g->d.device);
+  if (dg.status) return dg.status;
+  return direct_type1(g->d, C2(a), batch, R, D2(out), S(st));
+}
+
+int nfft45_type2_direct(const nfft45_grid* g, const double* Sc, int64_t batch, int64_t P, double* out, void* st) {
+  if (!g || P < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid direct type-2 arguments");
+  DeviceGuard dg(g->d.device);
+  if (dg.status) return dg.status;
+  return direct_type2(g->d, C2(Sc), batch, P, D2(out), S(st));
+}
+
+int nfft45_dft(const double* in, double* out, int64_t batch, int64_t N, int sign, void* st) {
+  if (N < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "DFT length must be >= 1");
+  return fft_run(C2(in), D2(out), batch, N, sign, nullptr, nullptr, S(st));
+}
+
+int nfft45_v_samples(const nfft45_grid* g, double a, int eta, int m, double* v, void* st) {
+  if (!g || eta < 1 || m < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid v-samples arguments");
+  if ((int64_t)eta * g->d.Q < 2)
+    return fail(NFFT45_ERR_INVALID_ARGUMENT, "need eta * P >= 2 so the truncated series has at least one term");
+  DeviceGuard dg(g->d.device);
+  if (dg.status) return dg.status;
+  return v_core(g->d, a, eta, m, D2(v), S(st));
+}
+
+int nfft45_kernel_samples(const nfft45_grid* g, const double* v, double* ks, void* st) {
+  if (!g) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid grid");
+  DeviceGuard dg(g->d.device);
+  if (dg.status) return dg.status;
+  cudaStream_t s = S(st);
+  Scratch guard(s);
+  NFFT_CHECK(guard.alloc(sizeof(double) * 2));
+  NFFT_CHECK(ks_core(g->d, C2(v), D2(ks), guard.d(), s));
+  return check_guards(guard.d(), 1, 0, s);
+}
+
+int nfft45_kernel_coefficients(const double* ks, int64_t P, double a, double* L, void* st) {
+  if (P < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid coefficient arguments");
+  return coeff_core(C2(ks), P, a, D2(L), S(st));
+}
+
+int nfft45_derivative_coefficients(const double* L, int64_t P, double* d, void* st) {
+  if (P < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid coefficient length");
+  LAUNCH(k_dcoef, (unsigned)ceil_div(P, 256), 256, 0, S(st), C2(L), D2(d), P);
+  return NFFT45_OK;
+}
+
+int nfft45_min_abs(const double* x, int64_t n, double* out, void* st) {
+  if (n < 1 || !out) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid min-abs arguments");
+  cudaStream_t s = S(st);
+  int blocks = (int)std::min<int64_t>(ceil_div(n, 256), 1024);
+  Scratch part(s), res(s);
+  NFFT_CHECK(part.alloc(sizeof(double) * blocks));
+  NFFT_CHECK(res.alloc(sizeof(double)));
+  LAUNCH(k_min_abs, blocks, 256, 0, s, C2(x), n, part.d());
+  LAUNCH(k_max_reduce, 1, 32, 0, s, part.d(), blocks, res.d(), 1);
+  NFFT_CUDA(cudaMemcpyAsync(out, res.d(), sizeof(double), cudaMemcpyDeviceToHost, s));
+  NFFT_CUDA(cudaStreamSynchronize(s));
+  return NFFT45_OK;
+}
+
+int nfft45_derivative_samples(const nfft45_grid* g, const double* L, int m, double* dL, void* st) {
+  if (!g || m < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid derivative arguments");
+  DeviceGuard dg(g->d.device);
+  if (dg.status) return dg.status;
+  cudaStream_t s = S(st);
+  Scratch guard(s);
+  NFFT_CHECK(guard.alloc(sizeof(double) * 2));
+  NFFT_CHECK(deriv_core(g->d, C2(L), m, D2(dL), guard.d() + 1, s));
+  return check_guards(guard.d(), 0, 1, s);
+}
+
+int nfft45_plan_create(const nfft45_grid* g, double a, int eta, int m, void* st, nfft45_plan** out) {
+  if (!g || !out) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid plan arguments");
+  if (!(a > 0.0)) return fail(NFFT45_ERR_NON_POSITIVE_DAMPING, "damping must be positive");
+  if (eta < 1 || m < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "eta and m must be >= 1");
+  const int64_t P = g->d.Q;
+  if ((int64_t)eta * P < 2)
+    return fail(NFFT45_ERR_INVALID_ARGUMENT, "need eta * P >= 2 so the truncated series has at least one term");
+  DeviceGuard dg(g->d.device);
+  if (dg.status) return dg.status;
+  cudaStream_t s = S(st);
+  nfft45_plan* p = new nfft45_plan();
+  p->g = g;
+  p->P = P;
+  p->a = a;
+  p->eta = eta;
+  p->m = m;
+  cudaError_t e = cudaMalloc(&p->tables, sizeof(double2) * 9 * P);
+  if (e != cudaSuccess) {
+    delete p;
+    return cuda_fail(e, "cudaMalloc(plan)");
+  }
+  double2* t = p->tables;
+  p->v = t;
+  p->ks = t + P;
+  p->L = t + 2 * P;
+  p->dL = t + 3 * P;
+  p->nw = t + 4 * P;
+  p->decay = t + 5 * P;
+  p->coef = t + 6 * P;
+  p->c5 = t + 7 * P;
+  p->c4 = t + 8 * P;
+  int status = NFFT45_OK;
+  {
+    Scratch guard(s);
+    status = guard.alloc(sizeof(double) * 2);
+    if (!status) status = v_core(g->d, a, eta, m, p->v, s);
+    if (!status) status = ks_core(g->d, p->v, p->ks, guard.d(), s);
+    if (!status) status = coeff_core(p->ks, P, a, p->L, s);
+    if (!status) status = deriv_core(g->d, p->L, m, p->dL, guard.d() + 1, s);
+    if (!status) {
+      k_plan_tables<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(g->d.t, g->d.ts, g->d.perm, p->dL, P, a, p->nw,
+                                                              p->decay, p->coef);
+      g_launches++;
+      k_fused_factors<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(g->d.ts, g->d.perm, p->nw, P, (double)(P / 2),
+                                                                p->c5, p->c4);
+      g_launches++;
+      cudaError_t le = cudaGetLastError();
+      if (le != cudaSuccess) status = cuda_fail(le, "plan tables");
+    }
+    if (!status) status = check_guards(guard.d(), 1, 1, s);
+  }
+  if (status) {
+    cudaStreamSynchronize(s);
+    cudaFree(p->tables);
+    delete p;
+    return status;
+  }
+  *out = p;
+  return NFFT45_OK;
+}
+
+void nfft45_plan_destroy(nfft45_plan* p) {
+  if (!p) return;
+  DeviceGuard dg(p->g->d.device);
+  cudaFree(p->tables);
+  delete p;
+}
+
+int nfft45_plan_table(const nfft45_plan* p, int which, double* dst, void* st) {
+  if (!p || which < 0 || which > 6) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid plan table");
+  DeviceGuard dg(p->g->d.device);
+  if (dg.status) return dg.status;
+  const double2* src = p->tables + (int64_t)which * p->P;
+  NFFT_CUDA(cudaMemcpyAsync(dst, src, sizeof(double2) * p->P, cudaMemcpyDeviceToDevice, S(st)));
+  return NFFT45_OK;
+}
+
+int nfft45_type5(const nfft45_plan* p, const double* s, int64_t batch, double* out, void* st) {
+  if (!p) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid plan");
+  DeviceGuard dg(p->g->d.device);
+  if (dg.status) return dg.status;
+  return type5_core(p, C2(s), batch, D2(out), S(st));
+}
+
+int nfft45_type4(const nfft45_plan* p, const double* A, int64_t batch, double* out, void* st) {
+  if (!p) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid plan");
+  DeviceGuard dg(p->g->d.device);
+  if (dg.status) return dg.status;
+  return type4_core(p, C2(A), batch, D2(out), S(st));
+}
+
+int nfft45_refine_type5(const nfft45_plan* p, const double* s, int64_t batch, int passes, double* out, void* st) {
+  if (!p || passes < 0) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid refine arguments");
+  DeviceGuard dg(p->g->d.device);
+  if (dg.status) return dg.status;
+  return refine_core(p, C2(s), batch, passes, D2(out), true, S(st));
+}
+
+int nfft45_refine_type4(const nfft45_plan* p, const double* A, int64_t batch, int passes, double* out, void* st) {
+  if (!p || passes < 0) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid refine arguments");
+  DeviceGuard dg(p->g->d.device);
+  if (dg.status) return dg.status;
+  return refine_core(p, C2(A), batch, passes, D2(out), false, S(st));
+}
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+// ops.cuh — internal launchers shared by the C-ABI layer.
+#pragma once
+
+#include "common.cuh"
+
+namespace nfft45 {
+
+// Device-resident node set (NonuniformGrid, grid.py:35-61).
+struct GridDev {
+  int device;
+  int64_t Q;
+  double* t;       // caller order [Q]
+  double* ts;      // ascending [Q]
+  int* perm;       // ts[i] = t[perm[i]]
+  double sum_hi;   // sum of instants as a double-double (lagrange.py:92)
+  double sum_lo;
+};
+
+// Gaussian taps exp(-alpha k^2), k = 0..kFastM (for the factorised weights).
+struct GaussTab {
+  double g[kFastM + 1];
+};
+GaussTab gauss_tab(const Window& w);
+
+// Node factor applied before spreading / after gathering:
+//   fac != nullptr : multiply by fac[i] (ascending-node order)
+//   else if phaseK != 0 : multiply by e^{phase_sign * 2 pi i phaseK t}
+struct NodeFactor {
+  const double2* fac;
+  double phaseK;
+  int phase_sign;
+};
+
+// H[b][j] = sum_q w(j - n t_q) * amp[b][q] * factor_q  (gridding.py:57-72,
+// forward.py:47-54).  amp == nullptr means unit amplitudes.  Deterministic:
+// every cell sums its contributions in ascending-node order.
+int spread(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch,
+           NodeFactor f, double2* H, cudaStream_t st);
+
+// out[b][q] = factor_q * sum_k w_k H[b][i0_q + k]  (- sub[b][q] if sub)
+// (forward.py:91-102).  Node-indexed vectors are in caller order.
+int gather(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch,
+           NodeFactor f, const double2* sub, double2* out, cudaStream_t st);
+
+// out[b][q] = sum_{e<eta} X(eP + q),  X(p) = H[b][(p - K) mod n] * deconv(p) * tab[p]
+// (forward.py:64 band select + deconvolution, forward.py:153-154 fold).
+// deconv uses window `win` when with_deconv; tab may be nullptr.  If sub,
+// out -= sub[b][q].
+int band_fold(const double2* H, int64_t n, int64_t R, int64_t K, int64_t P, const Window& win,
+              bool with_deconv, const double2* tab, const double2* sub, double2* out, int64_t batch,
+              cudaStream_t st);
+
+// F[b][k] = S[b][p] * deconv(p) * tab[p] when k = (p - K) mod n, else 0
+// (forward.py:88-89).
+int band_pad(const double2* S, int64_t P, int64_t n, int64_t K, const Window& win, bool with_deconv,
+             const double2* tab, double2* F, int64_t batch, cudaStream_t st);
+
+// Exact direct sums (forward.py:105-130).
+int direct_type1(const GridDev& g, const double2* a, int64_t batch, int64_t R, double2* out, cudaStream_t st);
+int direct_type2(const GridDev& g, const double2* S, int64_t batch, int64_t P, double2* out, cudaStream_t st);
+
+// y[b][i] = x[b][i] - d[b][i]   (refinement correction, inverse.py:161)
+int csub_batch(const double2* x, const double2* d, double2* y, int64_t total, cudaStream_t st);
+
+// Per-signal l2 norms of r[b][0..len) into norms[b] (fixed-order reduction).
+int row_norms(const double2* r, int64_t len, int64_t batch, double* norms, cudaStream_t st);
+
+// Device deconvolution weight 1/(n Psi(nu)) of gridding.py:90.
+__device__ __forceinline__ double deconv_weight(int64_t p, int64_t K, int64_t n, double b) {
+  double nu = (double)(p - K);
+  double x = 2.0 * 3.141592653589793 * nu / (double)n;
+  return exp(b * (x * x)) / sqrt(4.0 * 3.141592653589793 * b);
+}
+
+}  // namespace nfft45

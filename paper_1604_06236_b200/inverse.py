@@ -1,0 +1,224 @@
+"""Non-iterative type-4 / type-5 inversion on the B200 (reference inverse.py:1-202).
+
+build_plan uploads the node set and builds every grid-only table on the
+device in one C call (three NFFT-sized stages + node factors); type5/type4
+are one C call each (spread/gather + Stockham FFTs with fused elementwise
+stages); refine_type5/4 run the Section V residual passes inside the C call.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _device, _lib
+from . import flops as _fl
+from .flops import FlopCounter
+from .grid import MethodParams, NonuniformGrid
+from .gridding import GriddingKernel, kernel_for_size
+from .lagrange import KernelData, _amplification_check
+
+_TABLE = {"v": 0, "ks": 1, "L": 2, "dL": 3, "nw": 4, "decay": 5, "coef": 6}
+
+
+class _PlanHandle:
+    def __init__(self, ptr, grid_handle_owner):
+        self.ptr = ptr
+        self._owner = grid_handle_owner  # keeps the device grid alive
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                _lib.load().nfft45_plan_destroy(self.ptr)
+        except Exception:
+            pass
+
+
+class InversePlan:
+    """Grid-only precomputation, reusable across right-hand sides (inverse.py:33-55).
+
+    Device tables live in the C plan; the numpy views the reference exposes
+    (kernel_data, node_weights, h1_coefficients, coef_scale) are copied back
+    lazily on first access and are read-only.
+    """
+
+    def __init__(self, grid: NonuniformGrid, params: MethodParams, handle: _PlanHandle, device: int,
+                 kernel_fine: GriddingKernel, kernel_base: GriddingKernel):
+        self.grid = grid
+        self.params = params
+        self.kernel_fine = kernel_fine
+        self.kernel_base = kernel_base
+        self.device = device
+        self._h = handle
+        self._cache = {}
+        self._mu = threading.Lock()
+
+    @property
+    def size(self) -> int:
+        return self.grid.size
+
+    @property
+    def handle(self):
+        return self._h.ptr
+
+    def table(self, name: str, as_tensor: bool = False):
+        """One plan table (caller order for node-indexed ones)."""
+        torch = _device.torch
+        t = torch.empty(self.size, dtype=torch.complex128, device=f"cuda:{self.device}")
+        _lib.call("nfft45_plan_table", self.handle, _TABLE[name], t.data_ptr(), _device.stream_handle(self.device))
+        return t if as_tensor else t.cpu().numpy()
+
+    def _host(self, name: str, real: bool = False) -> np.ndarray:
+        arr = self._cache.get(name)
+        if arr is None:
+            with self._mu:
+                arr = self._cache.get(name)
+                if arr is None:
+                    arr = self.table(name)
+                    if real:
+                        arr = np.ascontiguousarray(arr.real)
+                    arr.setflags(write=False)
+                    self._cache[name] = arr
+        return arr
+
+    @property
+    def kernel_data(self) -> KernelData:
+        return KernelData(v_samples=self._host("v"), kernel_samples=self._host("ks"),
+                          coefficients=self._host("L"), derivative_samples=self._host("dL"))
+
+    @property
+    def node_weights(self) -> np.ndarray:
+        return self._host("nw")
+
+    @property
+    def h1_coefficients(self) -> np.ndarray:
+        return self._host("decay", real=True)
+
+    @property
+    def coef_scale(self) -> np.ndarray:
+        return self._host("coef", real=True)
+
+
+def _charge_plan(f: FlopCounter | None, P: int, params: MethodParams):
+    """build_kernel_data + build_plan charges (lagrange.py:57-164, inverse.py:79-86)."""
+    if f is None:
+        return
+    taps = 2 * params.spread_width + 1
+    R = params.eta * P
+    f.complex_exp(R - 1)
+    f.real_mul(R - 1)
+    _fl.charge_type1(f, P, R, taps)
+    _fl.charge_conv_tail(f, R, P, True)
+    f.real_add(P)
+    f.complex_add(P)
+    f.complex_exp(P)
+    f.complex_exp(P)
+    f.fft(P)
+    f.complex_exp(1)
+    f.real_mul(1 + P)
+    f.complex_add(1)
+    f.real_mul(2 * P)
+    f.real_mul(2 * P)
+    _fl.charge_type2(f, P, P, taps)
+    f.complex_exp(P)
+    f.real_mul(2 * P)
+    f.complex_exp(2 * P + 1)
+    f.real_mul(2 * P)
+    f.complex_add(P)
+    f.complex_div(2 * P)
+    f.complex_mul(P)
+
+
+def build_plan(grid: NonuniformGrid, params: MethodParams, flops: FlopCounter | None = None,
+               device=None) -> InversePlan:
+    """Precompute everything grid-dependent for type-4/type-5 solves (inverse.py:58-98)."""
+    P = grid.size
+    dev = _device.device_index(device)
+    kernel_fine = kernel_for_size(params.eta * P, params.spread_width)
+    kernel_base = kernel_for_size(P, params.spread_width)
+    _amplification_check(P, params.damping_a)
+    gptr = grid.device_handle(dev)
+    out = ctypes.c_void_p()
+    _lib.call("nfft45_plan_create", gptr, float(params.damping_a), int(params.eta), int(params.spread_width),
+              _device.stream_handle(dev), ctypes.byref(out))
+    _charge_plan(flops, P, params)
+    return InversePlan(grid, params, _PlanHandle(out.value, grid), dev, kernel_fine, kernel_base)
+
+
+def _charge_type5(f, P, taps):
+    if f is None:
+        return
+    _fl.charge_type1(f, P, P, taps)
+    _fl.charge_conv_tail(f, P, P, True)
+    f.complex_mul(2 * P)
+    f.fft(P)
+    f.real_mul(2 * P)
+
+
+def _charge_type4(f, P, taps):
+    if f is None:
+        return
+    _fl.charge_type2(f, P, P, taps)
+    f.real_mul(2 * P)
+    f.fft(P)
+    f.complex_mul(P)
+    f.fft(P)
+    f.real_mul(2 * P)
+    f.complex_mul(P)
+
+
+def _solve(name: str, plan: InversePlan, data, label: str, passes: int | None):
+    a = _device.operand(data, plan.device, length=plan.size, name=label)
+    out = a.empty_like_rows(plan.size)
+    st = _device.stream_handle(plan.device)
+    if passes is None:
+        _lib.call(f"nfft45_{name}", plan.handle, a.ptr, a.rows, out.data_ptr(), st)
+    else:
+        _lib.call(f"nfft45_refine_{name}", plan.handle, a.ptr, a.rows, int(passes), out.data_ptr(), st)
+    return a.finish(out)
+
+
+def type5(plan: InversePlan, samples, flops: FlopCounter | None = None):
+    """Coefficients S with sum_p S_p e^{2 pi i p t_q} = samples_q (inverse.py:101-120, Fig. 2)."""
+    out = _solve("type5", plan, samples, "samples", None)
+    _charge_type5(flops, plan.size, plan.kernel_base.taps)
+    return out
+
+
+def type4(plan: InversePlan, spectrum, flops: FlopCounter | None = None):
+    """Amplitudes a with sum_q a_q e^{-2 pi i p t_q} = spectrum_p (inverse.py:123-143, Fig. 3)."""
+    out = _solve("type4", plan, spectrum, "spectrum", None)
+    _charge_type4(flops, plan.size, plan.kernel_base.taps)
+    return out
+
+
+def refine_type4(plan: InversePlan, spectrum, passes: int | None = None, flops: FlopCounter | None = None):
+    """type4 plus residual-correction passes (inverse.py:165-185, Section V)."""
+    if passes is None:
+        passes = plan.params.refine_passes
+    out = _solve("type4", plan, spectrum, "spectrum", passes)
+    P, taps = plan.size, plan.kernel_base.taps
+    _charge_type4(flops, P, taps)
+    for _ in range(passes):
+        if flops is not None:
+            _fl.charge_type1(flops, P, P, taps)
+            flops.complex_add(2 * P)
+        _charge_type4(flops, P, taps)
+    return out
+
+
+def refine_type5(plan: InversePlan, samples, passes: int | None = None, flops: FlopCounter | None = None):
+    """type5 plus residual-correction passes in the sample domain (inverse.py:188-202)."""
+    if passes is None:
+        passes = plan.params.refine_passes
+    out = _solve("type5", plan, samples, "samples", passes)
+    P, taps = plan.size, plan.kernel_base.taps
+    _charge_type5(flops, P, taps)
+    for _ in range(passes):
+        if flops is not None:
+            _fl.charge_type2(flops, P, P, taps)
+            flops.complex_add(2 * P)
+        _charge_type5(flops, P, taps)
+    return out
