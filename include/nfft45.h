@@ -61,6 +61,14 @@ int nfft45_version(void);
  * (all threads); used by bench.py to report `gpu_launches`. */
 int64_t nfft45_launch_count(void);
 
+/* Per-launch device timing (for bench.py's roofline): while enabled, every
+ * kernel launch of this library is bracketed by CUDA events recorded on the
+ * launching stream.  nfft45_profile_read synchronizes on them, writes lines
+ * "<kernel> <launches> <total_ms>\n" into buf (NUL-terminated, at most cap
+ * bytes), clears the record and returns the full text length. */
+int nfft45_profile_enable(int on);
+int nfft45_profile_read(char* buf, int64_t cap);
+
 /* --------------------------------------------------------------- grids */
 
 /* validate_grid(instants, min_gap) — grid.py:64-96.  Host-side range /

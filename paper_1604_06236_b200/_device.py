@@ -41,11 +41,12 @@ def stream_handle(dev: int) -> int:
 class Operand:
     """A validated complex128 operand resident on one device."""
 
-    __slots__ = ("tensor", "is_torch", "batched", "rows", "n")
+    __slots__ = ("tensor", "is_torch", "host", "batched", "rows", "n")
 
-    def __init__(self, tensor, is_torch: bool, batched: bool):
+    def __init__(self, tensor, is_torch: bool, batched: bool, host: bool = False):
         self.tensor = tensor
         self.is_torch = is_torch
+        self.host = host  # caller passed a CPU torch tensor: results go back to the host
         self.batched = batched
         self.rows = tensor.shape[0] if batched else 1
         self.n = tensor.shape[-1]
@@ -58,10 +59,17 @@ class Operand:
         shape = (self.rows, n) if self.batched else (n,)
         return torch.empty(shape, dtype=torch.complex128, device=self.tensor.device)
 
-    def finish(self, out):
-        """Return `out` in the caller's convention (numpy in -> numpy out)."""
+    def finish(self, out, dest=None):
+        """Return `out` in the caller's convention: numpy in -> numpy out; CUDA
+        tensor in -> CUDA tensor out (async); CPU tensor in -> CPU tensor out
+        (written into `dest` when given, e.g. a pinned buffer)."""
+        if dest is not None:
+            dest.copy_(out.reshape(dest.shape), non_blocking=True)
+            if not dest.is_cuda:
+                torch.cuda.current_stream(out.device).synchronize()
+            return dest
         if self.is_torch:
-            return out
+            return out.cpu() if self.host else out
         return out.cpu().numpy()
 
 
@@ -75,8 +83,9 @@ def operand(values, dev: int, length: int | None = None, name: str = "vector") -
             raise LengthMismatchError(f"{name} must be nonempty")
         if length is not None and t.shape[-1] != length:
             raise LengthMismatchError(f"{name} has length {t.shape[-1]}, expected {length}")
-        t = t.to(device=f"cuda:{dev}", dtype=torch.complex128).contiguous()
-        return Operand(t, True, t.dim() == 2)
+        host = not t.is_cuda
+        t = t.to(device=f"cuda:{dev}", dtype=torch.complex128, non_blocking=True).contiguous()
+        return Operand(t, True, t.dim() == 2, host)
     arr = np.asarray(values, dtype=np.complex128)
     if arr.ndim not in (1, 2):
         raise LengthMismatchError(f"{name} must be one-dimensional, got shape {arr.shape}")

@@ -23,6 +23,8 @@ _SIGS = {
     "nfft45_last_error": (ctypes.c_char_p, []),
     "nfft45_version": (ctypes.c_int, []),
     "nfft45_launch_count": (_i64, []),
+    "nfft45_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "nfft45_profile_read": (ctypes.c_int, [ctypes.c_char_p, _i64]),
     "nfft45_validate_grid": (ctypes.c_int, [ctypes.c_void_p, _i64, ctypes.c_double, ctypes.c_void_p]),
     "nfft45_grid_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _i64, ctypes.c_int,
                                           ctypes.POINTER(ctypes.c_void_p)]),
@@ -112,3 +114,19 @@ def check(status: int):
 
 def call(name: str, *args):
     check(getattr(load(), name)(*args))
+
+
+def profile_enable(on: bool):
+    load().nfft45_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{kernel name: (launches, total_ms)} recorded since profiling was enabled."""
+    lib = load()
+    buf = ctypes.create_string_buffer(1 << 20)
+    lib.nfft45_profile_read(buf, len(buf))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.rsplit(" ", 2)
+        out[name] = (int(cnt), float(ms))
+    return out

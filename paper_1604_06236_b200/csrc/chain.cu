@@ -1,0 +1,388 @@
+// chain.cu — fused FFT chains of the type-4 / type-5 solves (P = M*M).
+//
+// With P = M1*M2 (M1 = M2 = M here), the fine grid n = 2P and K = P/2, the
+// four-step FFT decompositions of FFT_2P, IFFT_P, FFT_P and IFFT_2P can be
+// chosen so that the row pass of one transform produces exactly the columns
+// the next transform's column pass needs (the band (p - K) mod n of a
+// row k1 is a column of the P-point layout because K = 0 mod M).  Each
+// kernel below therefore does  row FFT -> elementwise stage -> column FFT
+// on C rows of one signal entirely in shared memory, so every fused stage
+// costs one HBM read and one HBM write instead of two of each:
+//
+//   type 5:  spread -> colFFT_2P -> [rowFFT_2P | band*deconv*decay | colIFFT_P]
+//            -> [rowIFFT_P | *ks | colFFT_P] -> [rowFFT_P | *coef]
+//   type 4:  [colIFFT_P *decay] -> [rowIFFT_P | *ks | colFFT_P]
+//            -> [rowFFT_P | *coef*deconv, pad | colIFFT_2P] -> rowIFFT_2P -> gather
+//
+// (reference: inverse.py:101-143, forward.py:26-102, 133-162).
+#include "fft_fast.cuh"
+#include "ops.cuh"
+
+namespace nfft45 {
+
+namespace {
+
+__device__ __forceinline__ double2 rscale(double2 v, double s) { return make_double2(v.x * s, v.y * s); }
+
+__device__ __forceinline__ double2 tw_pair(const double2* __restrict__ lo, const double2* __restrict__ hi, int s,
+                                           int64_t e) {
+  return cmul(__ldg(&hi[e >> s]), __ldg(&lo[e & ((int64_t(1) << s) - 1)]));
+}
+
+}  // namespace
+
+// K3: rows k1 of the FFT_2P pass-A output (length 2M) -> band select
+// p = k1 + M m1 (m1 < M) with (X deconv [- sub]) decay -> column IFFT_P
+// (length M) -> twiddle W_P^{+m2 k1'} -> U[k1' M + m2].
+template <int M, int C>
+__global__ void __launch_bounds__(fast_threads<2 * M, C>(), 2) kc_band(
+    const double2* __restrict__ T, double2* __restrict__ U, const double2* __restrict__ twR,
+    const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
+    const double* __restrict__ deconv, const double* __restrict__ decay, const double2* __restrict__ sub) {
+  constexpr int64_t P = (int64_t)M * M, n = 2 * P;
+  constexpr int NR = 2 * M;
+  extern __shared__ double2 sm[];
+  const int r0 = blockIdx.x * C;
+  const int64_t bi = blockIdx.y;
+  const double2* Tin = T + bi * n;
+  auto ld1 = [&](int i, int c) -> double2 { return Tin[(int64_t)(r0 + c) * NR + i]; };
+  auto st1 = [&](int k2, int c, double2 v) {
+    const int m1 = (k2 + M / 2) & (NR - 1);  // (k2 + K/N1) mod 2M, K/N1 = M/2
+    if (m1 < M) {
+      const int64_t p = (int64_t)(r0 + c) + (int64_t)M * m1;
+      v = rscale(v, __ldg(&deconv[p]));
+      if (sub) v = csub(v, sub[bi * P + p]);
+      v = rscale(v, __ldg(&decay[p]));
+      sm[sidx<M, C, true>(m1, c)] = v;
+    }
+  };
+  fast_tile_fft<NR, C, -1, true>(sm, ld1, st1, twR);
+  __syncthreads();
+  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, C, true>(i, c)]; };
+  auto st2 = [&](int k1, int c, double2 v) {
+    const int m2 = r0 + c;
+    const double2 w = tw_pair(loP, hiP, sP, (int64_t)m2 * k1);
+    U[bi * P + (int64_t)k1 * M + m2] = cmulc(v, w);
+  };
+  fast_tile_fft_smem<M, C, +1, true>(sm, ld2, st2, twC);
+}
+
+// K4 / K2': rows k1' of U (length M) -> row IFFT_P -> * ks[k1' + M k2'] ->
+// column FFT_P (length M, column m2' = k1') -> twiddle W_P^{-m2' k1''} ->
+// Z[k1'' M + m2'].
+template <int M, int C>
+__global__ void __launch_bounds__(fast_threads<M, C>()) kc_mid(const double2* __restrict__ U, double2* __restrict__ Z,
+                                                              const double2* __restrict__ tw,
+                                                              const double2* __restrict__ loP,
+                                                              const double2* __restrict__ hiP, int sP,
+                                                              const double2* __restrict__ ks) {
+  constexpr int64_t P = (int64_t)M * M;
+  extern __shared__ double2 sm[];
+  const int r0 = blockIdx.x * C;
+  const int64_t bi = blockIdx.y;
+  const double2* Uin = U + bi * P;
+  auto ld1 = [&](int i, int c) -> double2 { return Uin[(int64_t)(r0 + c) * M + i]; };
+  auto st1 = [&](int k2, int c, double2 v) {
+    const int64_t p = (int64_t)(r0 + c) + (int64_t)M * k2;
+    sm[sidx<M, C, true>(k2, c)] = cmul(v, __ldg(&ks[p]));
+  };
+  fast_tile_fft<M, C, +1, true>(sm, ld1, st1, tw);
+  __syncthreads();
+  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, C, true>(i, c)]; };
+  auto st2 = [&](int k1, int c, double2 v) {
+    const int m2 = r0 + c;
+    const double2 w = tw_pair(loP, hiP, sP, (int64_t)m2 * k1);
+    Z[bi * P + (int64_t)k1 * M + m2] = cmul(v, w);
+  };
+  fast_tile_fft_smem<M, C, -1, true>(sm, ld2, st2, tw);
+}
+
+// K3' / K5+: rows k1'' of Z (length M) -> row FFT_P -> S_p * coef_p
+// (p = k1'' + M k2''); optional x = xsub - S (refinement) stored to xout;
+// then * deconv_p, zero-padded into the IFFT_2P column (length 2M) at
+// n1 = (k2'' - M/2) mod 2M -> column IFFT -> twiddle W_n^{+n2 k1'''} ->
+// Y[k1''' M + n2].
+template <int M, int C>
+__global__ void __launch_bounds__(fast_threads<2 * M, C>(), 2) kc_pad(
+    const double2* __restrict__ Z, double2* __restrict__ Y, const double2* __restrict__ twR,
+    const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
+    const double* __restrict__ coef, const double* __restrict__ deconv, const double2* __restrict__ xsub,
+    double2* __restrict__ xout) {
+  constexpr int64_t P = (int64_t)M * M, n = 2 * P;
+  constexpr int NC = 2 * M;
+  extern __shared__ double2 sm[];
+  const int r0 = blockIdx.x * C;
+  const int64_t bi = blockIdx.y;
+  const double2* Zin = Z + bi * P;
+  auto ld1 = [&](int i, int c) -> double2 { return Zin[(int64_t)(r0 + c) * M + i]; };
+  auto st1 = [&](int k2, int c, double2 v) {
+    const int64_t p = (int64_t)(r0 + c) + (int64_t)M * k2;
+    v = rscale(v, __ldg(&coef[p]));
+    if (xsub) v = csub(xsub[bi * P + p], v);
+    if (xout) xout[bi * P + p] = v;
+    v = rscale(v, __ldg(&deconv[p]));
+    const int n1 = (k2 - M / 2) & (NC - 1);
+    sm[sidx<NC, C, true>(n1, c)] = v;
+    sm[sidx<NC, C, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
+  };
+  fast_tile_fft<M, C, -1, true>(sm, ld1, st1, twR);
+  __syncthreads();
+  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, C, true>(i, c)]; };
+  auto st2 = [&](int k1, int c, double2 v) {
+    const int n2 = r0 + c;
+    const double2 w = tw_pair(loN, hiN, sN, (int64_t)n2 * k1);
+    Y[bi * n + (int64_t)k1 * M + n2] = cmulc(v, w);
+  };
+  fast_tile_fft_smem<NC, C, +1, true>(sm, ld2, st2, twC);
+}
+
+// K5 / K4': rows of length L (row pass), output index k1 + R1 k2 with
+// optional real post-table and optional out = xsub - v.
+template <int L, int C, int S>
+__global__ void __launch_bounds__(fast_threads<L, C>()) kc_row(const double2* __restrict__ in,
+                                                              double2* __restrict__ out, int64_t len, int64_t R1,
+                                                              const double2* __restrict__ tw,
+                                                              const double* __restrict__ post,
+                                                              const double2* __restrict__ xsub) {
+  extern __shared__ double2 sm[];
+  const int r0 = blockIdx.x * C;
+  const int64_t base = (int64_t)blockIdx.y * len;
+  auto ld = [&](int i, int c) -> double2 { return in[base + (int64_t)(r0 + c) * L + i]; };
+  auto st = [&](int k2, int c, double2 v) {
+    const int64_t idx = (int64_t)(r0 + c) + R1 * k2;
+    if (post) v = rscale(v, __ldg(&post[idx]));
+    if (xsub) v = csub(xsub[base + idx], v);
+    out[base + idx] = v;
+  };
+  fast_tile_fft<L, C, S, true>(sm, ld, st, tw);
+}
+
+// column pass (four-step pass A) with optional real pre-table: columns n2
+// of x[n1 * L2 + n2] (length L), twiddle W_N^{S n2 k1}, stored in place-layout.
+template <int L, int C, int S>
+__global__ void __launch_bounds__(fast_threads<L, C>()) kc_col(const double2* __restrict__ in,
+                                                              double2* __restrict__ out, int64_t N, int L2,
+                                                              const double2* __restrict__ tw,
+                                                              const double2* __restrict__ lo,
+                                                              const double2* __restrict__ hi, int s,
+                                                              const double* __restrict__ pre) {
+  extern __shared__ double2 sm[];
+  const int c0 = blockIdx.x * C;
+  const int64_t base = (int64_t)blockIdx.y * N;
+  auto ld = [&](int i, int c) -> double2 {
+    const int64_t idx = (int64_t)i * L2 + c0 + c;
+    double2 v = in[base + idx];
+    if (pre) v = rscale(v, __ldg(&pre[idx]));
+    return v;
+  };
+  auto st = [&](int k1, int c, double2 v) {
+    const int64_t n2 = c0 + c;
+    const double2 w = tw_pair(lo, hi, s, n2 * k1);
+    out[base + (int64_t)k1 * L2 + n2] = S < 0 ? cmul(v, w) : cmulc(v, w);
+  };
+  fast_tile_fft<L, C, S, true>(sm, ld, st, tw);
+}
+
+// ------------------------------------------------------------ host side
+
+template <int M>
+constexpr int chain_cols() { return (2 * M * 8 <= 4096) ? 8 : 4096 / (2 * M); }
+
+template <typename K>
+static int chain_attr(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) NFFT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return NFFT45_OK;
+}
+
+struct ChainTabs {
+  const double2 *twM, *tw2M;        // tile twiddles for lengths M and 2M
+  const FftTables *tP, *tN;         // four-step twiddles for P and n = 2P
+};
+
+static int chain_tables(int64_t M, ChainTabs* t, cudaStream_t st) {
+  int status = NFFT45_OK;
+  const FftTables* a = fft_tables(M, st, &status);
+  if (!a) return status;
+  const FftTables* b = fft_tables(2 * M, st, &status);
+  if (!b) return status;
+  t->twM = a->tw;
+  t->tw2M = b->tw;
+  t->tP = fft_tables(M * M, st, &status);
+  if (!t->tP) return status;
+  t->tN = fft_tables(2 * M * M, st, &status);
+  if (!t->tN) return status;
+  return NFFT45_OK;
+}
+
+template <int M>
+struct Chain {
+  static constexpr int C = chain_cols<M>();
+  static constexpr int64_t P = (int64_t)M * M;
+
+  // colFFT over a [len = rows*L2] signal: rows of length L2, columns of length L
+  template <int L, int S>
+  static int col(const double2* in, double2* out, int64_t batch, int64_t N, int L2, const double2* tw,
+                 const FftTables* t4, const double* pre, cudaStream_t st) {
+    constexpr int CC = (L * 8 <= 4096) ? 8 : 4096 / L;
+    auto chain_col = kc_col<L, CC, S>;
+    constexpr size_t smem = fast_smem<L, CC>();
+    NFFT_CHECK(chain_attr(chain_col, smem));
+    constexpr int T = fast_threads<L, CC>();
+    dim3 grid((unsigned)(L2 / CC), (unsigned)batch);
+    LAUNCH(chain_col, grid, T, smem, st, in, out, N, L2, tw, t4->lo, t4->hi, t4->s, pre);
+    return NFFT45_OK;
+  }
+
+  static int band(const double2* T_, double2* U, int64_t batch, const ChainTabs& t, const double* deconv,
+                  const double* decay, const double2* sub, cudaStream_t st) {
+    auto chain_band = kc_band<M, C>;
+    constexpr size_t smem = fast_smem<2 * M, C>();
+    NFFT_CHECK(chain_attr(chain_band, smem));
+    constexpr int T = fast_threads<2 * M, C>();
+    dim3 grid((unsigned)(M / C), (unsigned)batch);
+    LAUNCH(chain_band, grid, T, smem, st, T_, U, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s, deconv, decay, sub);
+    return NFFT45_OK;
+  }
+
+  static int mid(const double2* U, double2* Z, int64_t batch, const ChainTabs& t, const double2* ks,
+                 cudaStream_t st) {
+    auto chain_mid = kc_mid<M, C>;
+    constexpr size_t smem = fast_smem<M, C>();
+    NFFT_CHECK(chain_attr(chain_mid, smem));
+    constexpr int T = fast_threads<M, C>();
+    dim3 grid((unsigned)(M / C), (unsigned)batch);
+    LAUNCH(chain_mid, grid, T, smem, st, U, Z, t.twM, t.tP->lo, t.tP->hi, t.tP->s, ks);
+    return NFFT45_OK;
+  }
+
+  static int pad(const double2* Z, double2* Y, int64_t batch, const ChainTabs& t, const double* coef,
+                 const double* deconv, const double2* xsub, double2* xout, cudaStream_t st) {
+    auto chain_pad = kc_pad<M, C>;
+    constexpr size_t smem = fast_smem<2 * M, C>();
+    NFFT_CHECK(chain_attr(chain_pad, smem));
+    constexpr int T = fast_threads<2 * M, C>();
+    dim3 grid((unsigned)(M / C), (unsigned)batch);
+    LAUNCH(chain_pad, grid, T, smem, st, Z, Y, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s, coef, deconv, xsub, xout);
+    return NFFT45_OK;
+  }
+
+  template <int S>
+  static int row(const double2* in, double2* out, int64_t batch, int64_t len, int64_t R1, int rows,
+                 const double2* tw, const double* post, const double2* xsub, cudaStream_t st) {
+    auto chain_row = kc_row<M, C, S>;
+    constexpr size_t smem = fast_smem<M, C>();
+    NFFT_CHECK(chain_attr(chain_row, smem));
+    constexpr int T = fast_threads<M, C>();
+    dim3 grid((unsigned)(rows / C), (unsigned)batch);
+    LAUNCH(chain_row, grid, T, smem, st, in, out, len, R1, tw, post, xsub);
+    return NFFT45_OK;
+  }
+};
+
+// Buffers for one chained solve (all [batch][len], stream-ordered scratch).
+struct ChainBufs {
+  double2 *H, *U, *Z;
+};
+
+template <int M>
+static int t5_front(const ChainPlanView& pv, const double2* s_or_r, int64_t batch, NodeFactor f, const double2* sub,
+                    const ChainTabs& t, ChainBufs& b, cudaStream_t st) {
+  using Ch = Chain<M>;
+  constexpr int64_t P = Ch::P, n = 2 * P;
+  Window win = Window::make(kFastM);
+  NFFT_CHECK(spread(*pv.g, n, win, s_or_r, batch, f, b.H, st));
+  NFFT_CHECK((Ch::template col<M, -1>(b.H, b.H, batch, n, 2 * M, t.twM, t.tN, nullptr, st)));
+  NFFT_CHECK(Ch::band(b.H, b.U, batch, t, pv.deconv, pv.decay, sub, st));
+  NFFT_CHECK(Ch::mid(b.U, b.Z, batch, t, pv.ks, st));
+  return NFFT45_OK;
+}
+
+template <int M>
+static int chain_solve(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes,
+                       double2* out, double* norms, cudaStream_t st) {
+  using Ch = Chain<M>;
+  constexpr int64_t P = Ch::P, n = 2 * P;
+  ChainTabs t;
+  NFFT_CHECK(chain_tables(M, &t, st));
+  Window win = Window::make(kFastM);
+  const GridDev& g = *pv.g;
+  double2* base = nullptr;
+  const size_t need = sizeof(double2) * batch * (n + P + P + n + P);
+  NFFT_CUDA(cudaMallocAsync(&base, need, st));
+  ChainBufs b;
+  b.H = base;
+  b.U = b.H + batch * n;
+  b.Z = b.U + batch * P;
+  double2* Y = b.Z + batch * P;    // [batch][n]
+  double2* R = Y + batch * n;      // [batch][P] residual
+  int status = NFFT45_OK;
+  auto run = [&]() -> int {
+    if (kind == 5) {
+      NodeFactor fc5{pv.c5, 0.0, 0};
+      NFFT_CHECK(t5_front<M>(pv, data, batch, fc5, nullptr, t, b, st));
+      for (int pass = 0; pass <= passes; pass++) {
+        const bool last = (pass == passes);
+        const double2* xsub = pass > 0 ? out : nullptr;
+        if (last) {
+          // K5: S = rowFFT_P(Z) * coef  (or x - S)
+          NFFT_CHECK((Ch::template row<-1>(b.Z, out, batch, P, M, M, t.twM, pv.coef, xsub, st)));
+        } else {
+          // K5+: x (= S*coef or x - S*coef) stored, padded into IFFT_2P (type-2 of x)
+          NFFT_CHECK(Ch::pad(b.Z, Y, batch, t, pv.coef, pv.deconv, xsub, out, st));
+          NFFT_CHECK((Ch::template row<+1>(Y, b.H, batch, n, 2 * M, 2 * M, t.twM, nullptr, nullptr, st)));
+          NodeFactor ph{nullptr, (double)(P / 2), +1};
+          NFFT_CHECK(gather(g, n, win, b.H, batch, ph, data, R, st));  // r = type2(x) - s
+          if (norms) NFFT_CHECK(row_norms(R, P, batch, norms + (int64_t)pass * batch, st));
+          NFFT_CHECK(t5_front<M>(pv, R, batch, fc5, nullptr, t, b, st));
+        }
+      }
+    } else {
+      // type 4: K1' colIFFT_P * decay -> K2' -> K3' -> K4' -> gather * c4
+      auto back = [&](const double2* A_or_r, double2* dst, const double2* xsub, bool from_cols) -> int {
+        if (from_cols)
+          NFFT_CHECK((Ch::template col<M, +1>(A_or_r, b.U, batch, P, M, t.twM, t.tP, pv.decay, st)));
+        NFFT_CHECK(Ch::mid(b.U, b.Z, batch, t, pv.ks, st));
+        NFFT_CHECK(Ch::pad(b.Z, Y, batch, t, pv.coef, pv.deconv, nullptr, nullptr, st));
+        NFFT_CHECK((Ch::template row<+1>(Y, b.H, batch, n, 2 * M, 2 * M, t.twM, nullptr, nullptr, st)));
+        NodeFactor fc4{pv.c4, 0.0, 0};
+        return gather_mode(g, n, win, b.H, batch, fc4, xsub, xsub ? 2 : 0, dst, st);
+      };
+      NFFT_CHECK(back(data, out, nullptr, true));
+      for (int pass = 0; pass < passes; pass++) {
+        // r = type1(x) - A, then r*decay -> IFFT_P column pass (fused in K3)
+        NodeFactor ph{nullptr, (double)(P / 2), -1};
+        NFFT_CHECK(spread(g, n, win, out, batch, ph, b.H, st));
+        NFFT_CHECK((Ch::template col<M, -1>(b.H, b.H, batch, n, 2 * M, t.twM, t.tN, nullptr, st)));
+        NFFT_CHECK(Ch::band(b.H, b.U, batch, t, pv.deconv, pv.decay, data, st));
+        NFFT_CHECK(back(nullptr, out, out, false));
+      }
+    }
+    return NFFT45_OK;
+  };
+  status = run();
+  cudaFreeAsync(base, st);
+  return status;
+}
+
+bool chain_supported(int64_t P, int m) {
+  if (m != kFastM) return false;
+  switch (P) {
+    case 1024: case 4096: case 16384: case 65536: case 262144: case 1048576: return true;
+  }
+  return false;
+}
+
+int chain_run(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes, double2* out,
+              double* norms, cudaStream_t st) {
+  switch (pv.P) {
+    case 1024: return chain_solve<32>(pv, kind, data, batch, passes, out, norms, st);
+    case 4096: return chain_solve<64>(pv, kind, data, batch, passes, out, norms, st);
+    case 16384: return chain_solve<128>(pv, kind, data, batch, passes, out, norms, st);
+    case 65536: return chain_solve<256>(pv, kind, data, batch, passes, out, norms, st);
+    case 262144: return chain_solve<512>(pv, kind, data, batch, passes, out, norms, st);
+    case 1048576: return chain_solve<1024>(pv, kind, data, batch, passes, out, norms, st);
+  }
+  return NFFT45_ERR_INVALID_ARGUMENT;
+}
+
+}  // namespace nfft45

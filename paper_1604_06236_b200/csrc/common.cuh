@@ -30,10 +30,17 @@ int cuda_fail(cudaError_t e, const char* what);
 
 // Every kernel launch of this library goes through LAUNCH so that
 // nfft45_launch_count() can report how many of OUR kernels ran.
+// When profiling is enabled (nfft45_profile_enable), each launch is
+// bracketed by CUDA events recorded on its own stream, keyed by kernel name.
 extern std::atomic<int64_t> g_launches;
+extern std::atomic<int> g_profiling;
+int prof_begin(cudaStream_t st);
+void prof_end(int slot, const char* name, cudaStream_t st);
 #define LAUNCH(kernel, grid, block, smem, stream, ...)                     \
   do {                                                                     \
+    int _ps = g_profiling.load(std::memory_order_relaxed) ? prof_begin(stream) : -1; \
     kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);            \
+    if (_ps >= 0) prof_end(_ps, #kernel, stream);                          \
     g_launches.fetch_add(1, std::memory_order_relaxed);                    \
     cudaError_t _le = cudaGetLastError();                                  \
     if (_le != cudaSuccess) return cuda_fail(_le, #kernel);                \

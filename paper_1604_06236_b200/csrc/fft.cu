@@ -3,7 +3,7 @@
 #include <mutex>
 #include <tuple>
 
-#include "fft.cuh"
+#include "fft_fast.cuh"
 
 namespace nfft45 {
 
@@ -27,21 +27,33 @@ FftSeq fft_seq(int N) {
   return s;
 }
 
+static bool pass_size(int64_t N);
+
+// Runtime-radix tiles need blockDim >= Nt*C/12 with blockDim <= 256.
+constexpr int kRtTileMax = 3072;
+
 bool fft_split(int64_t N, int* N1, int* N2) {
-  // balanced split, both factors smooth and <= kTileMax; prefer powers of two
-  int best1 = 0, best2 = 0;
-  double bestScore = 1e300;
-  for (int64_t a = 2; a <= kTileMax; a++) {
-    if (N % a) continue;
-    int64_t b = N / a;
-    if (b > kTileMax || !fft_smooth(a) || !fft_smooth(b)) continue;
-    double score = fabs(log((double)a) - log((double)b)) + (is_pow2(a) ? 0 : 0.5) + (is_pow2(b) ? 0 : 0.5);
-    if (score < bestScore) { bestScore = score; best1 = (int)a; best2 = (int)b; }
+  // Prefer a balanced split into two compile-time tile sizes; otherwise two
+  // smooth runtime tiles <= kRtTileMax.
+  for (int pass = 0; pass < 2; pass++) {
+    int best1 = 0, best2 = 0;
+    double bestScore = 1e300;
+    for (int64_t a = 2; a <= kTileMax; a++) {
+      if (N % a) continue;
+      int64_t b = N / a;
+      bool ok = pass == 0 ? (pass_size(a) && pass_size(b))
+                          : (a <= kRtTileMax && b <= kRtTileMax && fft_smooth(a) && fft_smooth(b));
+      if (!ok) continue;
+      double score = fabs(log((double)a) - log((double)b));
+      if (score < bestScore) { bestScore = score; best1 = (int)a; best2 = (int)b; }
+    }
+    if (best1) {
+      *N1 = best1;
+      *N2 = best2;
+      return true;
+    }
   }
-  if (!best1) return false;
-  *N1 = best1;
-  *N2 = best2;
-  return true;
+  return false;
 }
 
 // -------------------------------------------------------------- twiddles
@@ -78,7 +90,7 @@ const FftTables* fft_tables(int64_t N, cudaStream_t st, int* status) {
   };
   int s = NFFT45_OK;
   if (N <= kTileMax || !fft_smooth(N)) s = fill(&t->tw, N, 1);
-  if (s == NFFT45_OK && N > kTileMax && fft_smooth(N)) {
+  if (s == NFFT45_OK && N > 1 && fft_smooth(N)) {
     int bits = 0;
     while ((int64_t(1) << (2 * bits)) < N) bits++;
     t->s = bits;
@@ -113,7 +125,7 @@ __device__ __forceinline__ void tile_coords(int e, int Nt, int C, bool cfast, in
 
 // Single-pass: columns are signals. in/out[b][N]
 template <int S>
-__global__ void __launch_bounds__(1024) k_fft_single(const double2* __restrict__ in, double2* __restrict__ out,
+__global__ void __launch_bounds__(256) k_fft_single(const double2* __restrict__ in, double2* __restrict__ out,
                                                      int64_t batch, FftSeq seq, int C,
                                                      const double2* __restrict__ tw,
                                                      const double2* __restrict__ pre,
@@ -148,7 +160,7 @@ __global__ void __launch_bounds__(1024) k_fft_single(const double2* __restrict__
 // Four-step pass A: column FFTs of length N1 over x[n1*N2 + n2], C columns
 // per CTA, then the twiddle W_N^{n2 k1}; stored in place-layout [k1][n2].
 template <int S>
-__global__ void __launch_bounds__(1024) k_fft_passA(const double2* __restrict__ in, double2* __restrict__ out,
+__global__ void __launch_bounds__(256) k_fft_passA(const double2* __restrict__ in, double2* __restrict__ out,
                                                     int64_t N, int N2, FftSeq seq, int C,
                                                     const double2* __restrict__ tw,
                                                     const double2* __restrict__ lo,
@@ -183,7 +195,7 @@ __global__ void __launch_bounds__(1024) k_fft_passA(const double2* __restrict__ 
 // Four-step pass B: row FFTs of length N2 over t[k1*N2 + n2], C rows per CTA;
 // X[k1 + N1 k2] stored in natural order.
 template <int S>
-__global__ void __launch_bounds__(1024) k_fft_passB(const double2* __restrict__ in, double2* __restrict__ out,
+__global__ void __launch_bounds__(256) k_fft_passB(const double2* __restrict__ in, double2* __restrict__ out,
                                                     int64_t N, int N1, FftSeq seq, int C,
                                                     const double2* __restrict__ tw,
                                                     const double2* __restrict__ post) {
@@ -245,6 +257,175 @@ __global__ void k_scale_copy(const double2* __restrict__ in, double2* __restrict
   out[e] = v;
 }
 
+// ---------------------------------------------------- compile-time sized kernels
+
+template <int N, int C, int S>
+__global__ void __launch_bounds__(fast_threads<N, C>()) kf_single(const double2* __restrict__ in,
+                                                                 double2* __restrict__ out, int64_t batch,
+                                                                 const double2* __restrict__ tw,
+                                                                 const double2* __restrict__ pre,
+                                                                 const double2* __restrict__ post) {
+  extern __shared__ double2 sm[];
+  const int64_t b0 = (int64_t)blockIdx.x * C;
+  auto ld = [&](int i, int c) -> double2 {
+    const int64_t b = b0 + c;
+    if (b >= batch) return make_double2(0.0, 0.0);
+    double2 v = in[b * N + i];
+    if (pre) v = cmul(v, __ldg(&pre[i]));
+    return v;
+  };
+  auto st = [&](int k, int c, double2 v) {
+    const int64_t b = b0 + c;
+    if (b < batch) {
+      if (post) v = cmul(v, __ldg(&post[k]));
+      out[b * N + k] = v;
+    }
+  };
+  fast_tile_fft<N, C, S, false>(sm, ld, st, tw);
+}
+
+template <int N1, int C, int S>
+__global__ void __launch_bounds__(fast_threads<N1, C>()) kf_passA(const double2* __restrict__ in,
+                                                                 double2* __restrict__ out, int64_t N, int N2,
+                                                                 const double2* __restrict__ tw,
+                                                                 const double2* __restrict__ lo,
+                                                                 const double2* __restrict__ hi, int tws,
+                                                                 const double2* __restrict__ pre) {
+  extern __shared__ double2 sm[];
+  const int c0 = blockIdx.x * C;
+  const int64_t base = (int64_t)blockIdx.y * N;
+  const int64_t mask = (int64_t(1) << tws) - 1;
+  auto ld = [&](int i, int c) -> double2 {
+    const int64_t idx = (int64_t)i * N2 + c0 + c;
+    double2 v = in[base + idx];
+    if (pre) v = cmul(v, __ldg(&pre[idx]));
+    return v;
+  };
+  auto st = [&](int k1, int c, double2 v) {
+    const int64_t n2 = c0 + c;
+    const int64_t ex = n2 * k1;
+    const double2 w = cmul(__ldg(&hi[ex >> tws]), __ldg(&lo[ex & mask]));
+    out[base + (int64_t)k1 * N2 + n2] = S < 0 ? cmul(v, w) : cmulc(v, w);
+  };
+  fast_tile_fft<N1, C, S, true>(sm, ld, st, tw);
+}
+
+template <int N2, int C, int S>
+__global__ void __launch_bounds__(fast_threads<N2, C>()) kf_passB(const double2* __restrict__ in,
+                                                                 double2* __restrict__ out, int64_t N, int N1,
+                                                                 const double2* __restrict__ tw,
+                                                                 const double2* __restrict__ post) {
+  extern __shared__ double2 sm[];
+  const int r0 = blockIdx.x * C;
+  const int64_t base = (int64_t)blockIdx.y * N;
+  auto ld = [&](int i, int c) -> double2 { return in[base + (int64_t)(r0 + c) * N2 + i]; };
+  auto st = [&](int k2, int c, double2 v) {
+    const int64_t idx = (int64_t)(r0 + c) + (int64_t)N1 * k2;
+    if (post) v = cmul(v, __ldg(&post[idx]));
+    out[base + idx] = v;
+  };
+  fast_tile_fft<N2, C, S, true>(sm, ld, st, tw);
+}
+
+template <int N>
+constexpr int single_cols() { return FastTraits<N>::pow2 ? 4096 / N : 6144 / N; }
+template <int N>
+constexpr int pass_cols() { return single_cols<N>() < 8 ? single_cols<N>() : 8; }
+
+template <typename K>
+static int fast_attr(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) NFFT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return NFFT45_OK;
+}
+
+template <int N, int S>
+static int launch_single(const double2* in, double2* out, int64_t batch, const double2* tw, const double2* pre,
+                         const double2* post, cudaStream_t st) {
+  constexpr int C = single_cols<N>();
+  constexpr size_t smem = fast_smem<N, C>();
+  auto fft_single = kf_single<N, C, S>;
+  NFFT_CHECK(fast_attr(fft_single, smem));
+  constexpr int T = fast_threads<N, C>();
+  LAUNCH(fft_single, (unsigned)ceil_div(batch, C), T, smem, st, in, out, batch, tw, pre, post);
+  return NFFT45_OK;
+}
+
+template <int N1, int S>
+static int launch_passA(const double2* in, double2* out, int64_t batch, int64_t N, int N2, const double2* tw,
+                        const FftTables* tN, const double2* pre, cudaStream_t st) {
+  constexpr int C = pass_cols<N1>();
+  constexpr size_t smem = fast_smem<N1, C>();
+  auto fft_passA = kf_passA<N1, C, S>;
+  NFFT_CHECK(fast_attr(fft_passA, smem));
+  dim3 grid((unsigned)(N2 / C), (unsigned)batch);
+  constexpr int T = fast_threads<N1, C>();
+  LAUNCH(fft_passA, grid, T, smem, st, in, out, N, N2, tw, tN->lo, tN->hi, tN->s, pre);
+  return NFFT45_OK;
+}
+
+template <int N2, int S>
+static int launch_passB(const double2* in, double2* out, int64_t batch, int64_t N, int N1, const double2* tw,
+                        const double2* post, cudaStream_t st) {
+  constexpr int C = pass_cols<N2>();
+  constexpr size_t smem = fast_smem<N2, C>();
+  auto fft_passB = kf_passB<N2, C, S>;
+  NFFT_CHECK(fast_attr(fft_passB, smem));
+  dim3 grid((unsigned)(N1 / C), (unsigned)batch);
+  constexpr int T = fast_threads<N2, C>();
+  LAUNCH(fft_passB, grid, T, smem, st, in, out, N, N1, tw, post);
+  return NFFT45_OK;
+}
+
+#define NFFT_FAST_SIZES(X) \
+  X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) \
+  X(3) X(6) X(12) X(24) X(48) X(96) X(192) X(384) X(768) X(1536) X(3072)
+#define NFFT_PASS_SIZES(X) \
+  X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(96) X(192) X(384) X(768) X(1536) X(3072)
+
+static bool fast_size(int64_t N) {
+#define X(n) if (N == n) return true;
+  NFFT_FAST_SIZES(X)
+#undef X
+  return false;
+}
+static bool pass_size(int64_t N) {
+#define X(n) if (N == n) return true;
+  NFFT_PASS_SIZES(X)
+#undef X
+  return false;
+}
+
+template <int S>
+static int dispatch_single(int64_t N, const double2* in, double2* out, int64_t batch, const double2* tw,
+                           const double2* pre, const double2* post, cudaStream_t st) {
+  switch (N) {
+#define X(n) case n: return launch_single<n, S>(in, out, batch, tw, pre, post, st);
+    NFFT_FAST_SIZES(X)
+#undef X
+  }
+  return NFFT45_ERR_INVALID_ARGUMENT;
+}
+template <int S>
+static int dispatch_passA(int N1, const double2* in, double2* out, int64_t batch, int64_t N, int N2,
+                          const double2* tw, const FftTables* tN, const double2* pre, cudaStream_t st) {
+  switch (N1) {
+#define X(n) case n: return launch_passA<n, S>(in, out, batch, N, N2, tw, tN, pre, st);
+    NFFT_PASS_SIZES(X)
+#undef X
+  }
+  return NFFT45_ERR_INVALID_ARGUMENT;
+}
+template <int S>
+static int dispatch_passB(int N2, const double2* in, double2* out, int64_t batch, int64_t N, int N1,
+                          const double2* tw, const double2* post, cudaStream_t st) {
+  switch (N2) {
+#define X(n) case n: return launch_passB<n, S>(in, out, batch, N, N1, tw, post, st);
+    NFFT_PASS_SIZES(X)
+#undef X
+  }
+  return NFFT45_ERR_INVALID_ARGUMENT;
+}
+
 // ------------------------------------------------------------ host driver
 
 template <typename K>
@@ -286,11 +467,16 @@ static int fft_run_s(const double2* in, double2* out, int64_t batch, int64_t N, 
     if (tmp) NFFT_CUDA(cudaFreeAsync(tmp, st));
     return NFFT45_OK;
   }
-  if (N <= kTileMax) {
+  if (fast_size(N)) {
+    const FftTables* t = fft_tables(N, st, &status);
+    if (!t) return status;
+    return dispatch_single<S>(N, in, out, batch, t->tw, pre, post, st);
+  }
+  if (N <= kRtTileMax) {
     const FftTables* t = fft_tables(N, st, &status);
     if (!t) return status;
     int C = 1;
-    while (C < 512 && N * C * 2 <= kTileMax) C *= 2;
+    while (C < 512 && N * C * 2 <= kRtTileMax) C *= 2;
     if (C > batch) {
       C = 1;
       while (C < batch) C *= 2;
@@ -315,9 +501,15 @@ static int fft_run_s(const double2* in, double2* out, int64_t batch, int64_t N, 
   if (!t2) return status;
   double2* tmp = nullptr;
   NFFT_CUDA(cudaMallocAsync(&tmp, sizeof(double2) * batch * N, st));
+  if (pass_size(N1) && pass_size(N2)) {
+    NFFT_CHECK(dispatch_passA<S>(N1, in, tmp, batch, N, N2, t1->tw, tN, pre, st));
+    NFFT_CHECK(dispatch_passB<S>(N2, tmp, out, batch, N, N1, t2->tw, post, st));
+    NFFT_CUDA(cudaFreeAsync(tmp, st));
+    return NFFT45_OK;
+  }
   {
     int C = 8;
-    while (C > 1 && N1 * C > kTileMax) C /= 2;
+    while (C > 1 && N1 * C > kRtTileMax) C /= 2;
     while (C > 1 && N2 % C) C /= 2;
     FftSeq seq = fft_seq(N1);
     size_t smem = tile_smem_bytes(N1, C);
@@ -328,7 +520,7 @@ static int fft_run_s(const double2* in, double2* out, int64_t batch, int64_t N, 
   }
   {
     int C = 8;
-    while (C > 1 && N2 * C > kTileMax) C /= 2;
+    while (C > 1 && N2 * C > kRtTileMax) C /= 2;
     while (C > 1 && N1 % C) C /= 2;
     FftSeq seq = fft_seq(N2);
     size_t smem = tile_smem_bytes(N2, C);

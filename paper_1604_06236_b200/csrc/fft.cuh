@@ -140,7 +140,7 @@ __device__ __forceinline__ void bfly(double2* v) {
 }
 
 // Per-thread butterfly capacity per pass; launch with
-// blockDim.x >= Nt * C / 12 so that every radix fits (R * (16 / R) >= 12).
+// blockDim.x >= Nt * C / 12 so that every radix fits (R * (MAXE / R) >= 12).
 constexpr int kTileElemsPerThread = 16;
 
 // One Stockham pass of radix R over all C columns of an [Nt][C] tile.
@@ -207,7 +207,7 @@ inline int tile_threads(int Nt, int C) {
   int need = (Nt * C + 11) / 12;
   int T = ((need + 31) / 32) * 32;
   if (T < 32) T = 32;
-  if (T > 1024) T = 1024;
+  if (T > 256) T = 256;
   return T;
 }
 inline size_t tile_smem_bytes(int Nt, int C) {

@@ -1,0 +1,201 @@
+// fft_fast.cuh — compile-time-sized Stockham tile FFTs (fp64 complex).
+//
+// A tile is C independent length-N FFTs ("columns") done by one CTA of
+// T = N*C/E threads, each thread owning E elements in registers:
+//   pass 0      : loads its butterfly inputs straight from global memory
+//                 through the caller's loader functor (fused prologue),
+//   middle      : exchange through padded shared memory,
+//   last pass   : stores straight to global memory through the caller's
+//                 storer functor (fused epilogue: twiddles, tables, band
+//                 selection ...).
+// All index arithmetic is compile-time (shifts / masks).  Two thread
+// mappings: CF (column-fast lanes, for column-contiguous global layouts)
+// and JF (butterfly-fast lanes, for row-contiguous layouts).
+#pragma once
+
+#include "fft.cuh"
+
+namespace nfft45 {
+
+__host__ __device__ constexpr bool is_pow2_c(int n) { return n > 0 && (n & (n - 1)) == 0; }
+__host__ __device__ constexpr int log2_c(int n) { return n <= 1 ? 0 : 1 + log2_c(n >> 1); }
+
+// elements per thread: 16 for 2^a, 24 for 3*2^a (divisible by 2,3,4,8)
+template <int N>
+struct FastTraits {
+  static constexpr bool pow2 = is_pow2_c(N);
+  static constexpr int E = pow2 ? 16 : 24;
+  static constexpr int m2 = pow2 ? N : N / 3;  // power-of-two part
+  static constexpr int a = log2_c(m2);
+  // schedule for 2^a with radix-16 passes (pow2) or radix-8 passes (3*2^a);
+  // the leftover small radix goes first (pass 0 has no twiddles).
+  static constexpr int big = pow2 ? 16 : 8;
+  static constexpr int bigbits = pow2 ? 4 : 3;
+  static constexpr int rem = a % bigbits;
+  static constexpr int nbig = a / bigbits;
+  static constexpr int np = (pow2 ? 0 : 1) + (rem ? 1 : 0) + nbig;
+  __host__ __device__ static constexpr int radix(int p) {
+    // pass order: [3], [2^rem], big, big, ...
+    return (!pow2 && p == 0) ? 3 : ((rem && p == (pow2 ? 0 : 1)) ? (1 << rem) : big);
+  }
+};
+
+template <int S>
+__device__ __forceinline__ void bfly16(double2* v) {
+  // radix-16 = 4 x radix-4 with W16 twiddles in between
+  double2 a[16];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    a[i] = v[i];
+    a[4 + i] = v[4 + i];
+    a[8 + i] = v[8 + i];
+    a[12 + i] = v[12 + i];
+  }
+  // columns: elements {q, q+4, q+8, q+12} for q = 0..3
+#pragma unroll
+  for (int q = 0; q < 4; q++) bfly4<S>(a[q], a[q + 4], a[q + 8], a[q + 12]);
+  // twiddle a[q + 4 p] *= W16^{q p}
+  const double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, h = 0.70710678118654752440;
+  const double2 w[10] = {
+      make_double2(c1, S * s1), make_double2(h, S * h), make_double2(s1, S * c1),     // q=1: p=1,2,3
+      make_double2(h, S * h), make_double2(0.0, S * 1.0), make_double2(-h, S * h),   // q=2
+      make_double2(s1, S * c1), make_double2(-h, S * h), make_double2(-c1, -S * s1), // q=3
+      make_double2(0, 0)};
+#pragma unroll
+  for (int q = 1; q < 4; q++)
+#pragma unroll
+    for (int p = 1; p < 4; p++) a[q + 4 * p] = cmul(a[q + 4 * p], w[(q - 1) * 3 + (p - 1)]);
+  // rows: radix-4 over q for each p; output index p + 4 * k
+#pragma unroll
+  for (int p = 0; p < 4; p++) {
+    double2 x0 = a[4 * p], x1 = a[4 * p + 1], x2 = a[4 * p + 2], x3 = a[4 * p + 3];
+    bfly4<S>(x0, x1, x2, x3);
+    v[p] = x0;
+    v[p + 4] = x1;
+    v[p + 8] = x2;
+    v[p + 12] = x3;
+  }
+}
+
+template <int R, int S>
+__device__ __forceinline__ void bfly_fast(double2* v) {
+  if constexpr (R == 16) bfly16<S>(v);
+  else bfly<R, S>(v);
+}
+
+// Stockham twiddles w[r] = W^{r e} (r = 1..R-1) from the table W_N[.]:
+// powers of two are loaded, the rest are products of at most three loaded
+// values (<= 3 roundings), cutting L1 traffic from R-1 loads to log2(R).
+template <int R>
+__device__ __forceinline__ void twiddles(const double2* __restrict__ tw, int e, double2* w) {
+  if constexpr (R == 3 || R == 5) {
+#pragma unroll
+    for (int r = 1; r < R; r++) w[r] = __ldg(&tw[r * e]);
+  } else {
+    w[1] = __ldg(&tw[e]);
+    if constexpr (R >= 4) {
+      w[2] = __ldg(&tw[2 * e]);
+      w[3] = cmul(w[1], w[2]);
+    }
+    if constexpr (R >= 8) {
+      w[4] = __ldg(&tw[4 * e]);
+      w[5] = cmul(w[1], w[4]);
+      w[6] = cmul(w[2], w[4]);
+      w[7] = cmul(w[3], w[4]);
+    }
+    if constexpr (R >= 16) {
+      w[8] = __ldg(&tw[8 * e]);
+#pragma unroll
+      for (int r = 1; r < 8; r++) w[8 + r] = cmul(w[r], w[8]);
+    }
+  }
+}
+
+template <int N, int C, bool CF>
+__device__ __forceinline__ int sidx(int i, int c) {
+  return CF ? tpad(i * C + c) : tpad(c * N + i);
+}
+
+// One pass; FIRST reads through `ld`, LAST writes through `st`.  Threads
+// with threadIdx.x >= T (a CTA sized for a bigger FFT of a chain) idle but
+// still meet every barrier.  SYNC0: the first pass reads shared memory that
+// its own stores overwrite (chain kernels), so it needs a barrier too.
+template <int N, int C, int S, bool CF, bool SYNC0, int P, int Ns, class Ld, class St>
+__device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw) {
+  using Tr = FastTraits<N>;
+  constexpr int E = Tr::E;
+  constexpr int R = Tr::radix(P);
+  constexpr int T = N * C / E;
+  constexpr int MB = E / R;
+  constexpr int stride = N / R;
+  constexpr bool FIRST = (P == 0);
+  constexpr bool LAST = (P == Tr::np - 1);
+  const int tid = threadIdx.x;
+  const bool active = tid < T;
+  double2 v[MB][R];
+  if (active) {
+#pragma unroll
+  for (int u = 0; u < MB; u++) {
+    const int bf = tid + u * T;
+    const int c = CF ? (bf % C) : (bf / (N / R));
+    const int j = CF ? (bf / C) : (bf % (N / R));
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int i = j + r * stride;
+      if constexpr (FIRST) v[u][r] = ld(i, c);
+      else v[u][r] = sm[sidx<N, C, CF>(i, c)];
+    }
+  }
+  }
+  if constexpr (!FIRST || SYNC0) __syncthreads();  // everyone has read before anyone overwrites
+  if (active) {
+#pragma unroll
+  for (int u = 0; u < MB; u++) {
+    const int bf = tid + u * T;
+    const int c = CF ? (bf % C) : (bf / (N / R));
+    const int j = CF ? (bf / C) : (bf % (N / R));
+    const int k = j % Ns;
+    if constexpr (Ns > 1) {
+      constexpr int tstep = N / (Ns * R);
+      double2 w[R];
+      twiddles<R>(tw, k * tstep, w);
+#pragma unroll
+      for (int r = 1; r < R; r++) v[u][r] = S < 0 ? cmul(v[u][r], w[r]) : cmulc(v[u][r], w[r]);
+    }
+    bfly_fast<R, S>(v[u]);
+    const int d = (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      if constexpr (LAST) st(d + r * Ns, c, v[u][r]);
+      else sm[sidx<N, C, CF>(d + r * Ns, c)] = v[u][r];
+    }
+  }
+  }
+  if constexpr (!LAST) {
+    __syncthreads();
+    fast_passes<N, C, S, CF, SYNC0, P + 1, Ns * R>(sm, ld, st, tw);
+  }
+}
+
+template <int N, int C, int S, bool CF, class Ld, class St>
+__device__ __forceinline__ void fast_tile_fft(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw) {
+  fast_passes<N, C, S, CF, false, 0, 1>(sm, ld, st, tw);
+}
+
+// Variant whose first pass reads the tile from shared memory (via `ld`)
+// that later passes overwrite.
+template <int N, int C, int S, bool CF, class Ld, class St>
+__device__ __forceinline__ void fast_tile_fft_smem(double2* sm, const Ld& ld, const St& st,
+                                                   const double2* __restrict__ tw) {
+  fast_passes<N, C, S, CF, true, 0, 1>(sm, ld, st, tw);
+}
+
+template <int N, int C>
+constexpr int fast_threads() { return N * C / FastTraits<N>::E; }
+
+template <int N, int C>
+constexpr size_t fast_smem() {
+  return FastTraits<N>::np > 1 ? ((size_t)N * C + (size_t)N * C / 8 + 1) * sizeof(double2) : 16;
+}
+
+}  // namespace nfft45

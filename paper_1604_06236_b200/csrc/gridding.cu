@@ -151,13 +151,22 @@ __global__ void __launch_bounds__(256) k_spread(const double* __restrict__ ts, c
       }
       __syncthreads();
       if (j < j1) {
-        for (int idx = 0; idx < cnt; idx++) {
+        // staged centres ascend: the nodes reaching cell j are [lo, hi)
+        int lo = 0, hi = cnt;
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (csm[mid] >= j - m) hi = mid; else lo = mid + 1;
+        }
+        int hi2 = lo, top = cnt;
+        while (hi2 < top) {
+          int mid = (hi2 + top) >> 1;
+          if (csm[mid] > j + m) top = mid; else hi2 = mid + 1;
+        }
+        for (int idx = lo; idx < hi2; idx++) {
           int k = (int)(j - csm[idx]);
-          if (k >= -m && k <= m) {
-            double wk = wsm[(size_t)idx * taps + k + m];
+          double wk = wsm[(size_t)idx * taps + k + m];
 #pragma unroll
-            for (int sb = 0; sb < SB; sb++) caxpy(acc[sb], wk, asm_[sb * NB + idx]);
-          }
+          for (int sb = 0; sb < SB; sb++) caxpy(acc[sb], wk, asm_[sb * NB + idx]);
         }
       }
     }
@@ -206,6 +215,7 @@ int spread(const GridDev& g, int64_t n, const Window& win, const double2* amp, i
            double2* H, cudaStream_t st) {
   if (batch <= 0) return NFFT45_OK;
   bool fast = (win.m == kFastM);
+  if (fast && batch >= 32 && n >= 128) return spread_batched(g, n, win, amp, batch, f, H, st, batch >= 64 ? 2 : 1);
   if (batch >= 4) return fast ? spread_launch<4, kFastM>(g, n, win, amp, batch, f, H, st)
                               : spread_launch<4, 0>(g, n, win, amp, batch, f, H, st);
   return fast ? spread_launch<1, kFastM>(g, n, win, amp, batch, f, H, st)
@@ -220,7 +230,7 @@ template <int SB, int M>
 __global__ void __launch_bounds__(256) k_gather(const double* __restrict__ ts, const int* __restrict__ perm,
                                                 int64_t Q, int64_t n, int m, double alpha, GaussTab G,
                                                 const double2* __restrict__ H, int64_t batch, NodeFactor nf,
-                                                const double2* __restrict__ sub, double2* __restrict__ out) {
+                                                const double2* __restrict__ sub, int mode, double2* __restrict__ out) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= Q) return;
   const int64_t b0 = (int64_t)blockIdx.y * SB;
@@ -267,7 +277,8 @@ __global__ void __launch_bounds__(256) k_gather(const double* __restrict__ ts, c
     int64_t b = b0 + s;
     if (b < batch) {
       double2 v = cmul(acc[s], fq);
-      if (sub) v = csub(v, sub[b * Q + pq]);
+      if (mode == 1) v = csub(v, sub[b * Q + pq]);
+      else if (mode == 2) v = csub(sub[b * Q + pq], v);
       out[b * Q + pq] = v;
     }
   }
@@ -275,21 +286,28 @@ __global__ void __launch_bounds__(256) k_gather(const double* __restrict__ ts, c
 
 template <int SB, int M>
 static int gather_launch(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch,
-                         NodeFactor f, const double2* sub, double2* out, cudaStream_t st) {
+                         NodeFactor f, const double2* sub, int mode, double2* out, cudaStream_t st) {
   dim3 grid((unsigned)ceil_div(g.Q, 128), (unsigned)ceil_div(batch, SB));
   LAUNCH((k_gather<SB, M>), grid, 128, 0, st, g.ts, g.perm, g.Q, n, win.m, win.alpha, gauss_tab(win), H, batch,
-         f, sub, out);
+         f, sub, mode, out);
   return NFFT45_OK;
+}
+
+int gather_mode(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch, NodeFactor f,
+                const double2* sub, int mode, double2* out, cudaStream_t st) {
+  if (batch <= 0) return NFFT45_OK;
+  if (!sub) mode = 0;
+  bool fast = (win.m == kFastM);
+  if (fast && batch >= 32 && n >= 128) return gather_batched(g, n, win, H, batch, f, sub, mode, out, st);
+  if (batch >= 4) return fast ? gather_launch<4, kFastM>(g, n, win, H, batch, f, sub, mode, out, st)
+                              : gather_launch<4, 0>(g, n, win, H, batch, f, sub, mode, out, st);
+  return fast ? gather_launch<1, kFastM>(g, n, win, H, batch, f, sub, mode, out, st)
+              : gather_launch<1, 0>(g, n, win, H, batch, f, sub, mode, out, st);
 }
 
 int gather(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch, NodeFactor f,
            const double2* sub, double2* out, cudaStream_t st) {
-  if (batch <= 0) return NFFT45_OK;
-  bool fast = (win.m == kFastM);
-  if (batch >= 4) return fast ? gather_launch<4, kFastM>(g, n, win, H, batch, f, sub, out, st)
-                              : gather_launch<4, 0>(g, n, win, H, batch, f, sub, out, st);
-  return fast ? gather_launch<1, kFastM>(g, n, win, H, batch, f, sub, out, st)
-              : gather_launch<1, 0>(g, n, win, H, batch, f, sub, out, st);
+  return gather_mode(g, n, win, H, batch, f, sub, sub ? 1 : 0, out, st);
 }
 
 // ------------------------------------------------------- band kernels

@@ -1,0 +1,388 @@
+// gridding_b.cu — batched Gaussian spreading / interpolation (many signals,
+// one node set), half-width m = 14.
+//
+// Both kernels treat the banded window as small dense blocks: the lanes of
+// a warp run over SIGNALS (so every shared-memory access is a contiguous,
+// conflict-free 512-byte row and the window weights are warp-uniform
+// broadcasts), and each thread keeps a block of cells (spread) or nodes
+// (gather) in registers so one staged operand feeds 8 FMAs.  The
+// accumulation order is fixed (ascending nodes / ascending cells), so
+// results are bitwise reproducible and independent of the batch split.
+#include "ops.cuh"
+
+namespace nfft45 {
+
+namespace {
+
+constexpr int kM = kFastM;       // 14
+constexpr int kWRow = 44;        // padded weight row: taps -m-7 .. m+7 (+1 parity shift), 16-B aligned
+constexpr int kCPW = 8;          // spread: cells per warp
+constexpr int kSpreadWarps = 8;  // spread: warps per CTA -> 64 cells
+constexpr int kSpreadTile = kCPW * kSpreadWarps;
+constexpr int kSpreadCap = 72;   // nodes staged per batch
+constexpr int kNPW = 8;          // gather: nodes per warp
+constexpr int kGatherWarps = 4;  // gather: warps per CTA -> 32 nodes
+constexpr int kGatherNodes = kNPW * kGatherWarps;
+constexpr int kGatherSpan = 112; // cells staged per chunk
+constexpr int kWTSpan = 64;      // per-warp weight-table cells per chunk
+
+__device__ __forceinline__ int swz(int sig, int row) { return sig ^ (row & 7); }
+
+// 16-byte global -> shared async copy (LDGSTS); `valid == false` zero-fills.
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(n));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// 29 factorised Gaussian taps of one node (see gridding.cu gauss_fast).
+__device__ __forceinline__ void taps29(double f, double alpha, const GaussTab& G, double* w) {
+  double e1 = exp(-alpha * f * f);
+  double E = exp(2.0 * alpha * f);
+  double Ei = 1.0 / E;
+  w[kM] = e1;
+  double pp = e1, pn = e1;
+#pragma unroll
+  for (int k = 1; k <= kM; k++) {
+    pp *= E;
+    pn *= Ei;
+    w[kM + k] = pp * G.g[k];
+    w[kM - k] = pn * G.g[k];
+  }
+}
+
+__device__ __forceinline__ double2 factor_at(const NodeFactor& f, int64_t q, double t) {
+  if (f.fac) return f.fac[q];
+  if (f.phaseK != 0.0) {
+    double x = turns_of_product(f.phaseK, t);
+    return cis_turns(f.phase_sign < 0 ? -x : x);
+  }
+  return make_double2(1.0, 0.0);
+}
+
+__device__ __forceinline__ int64_t floordiv_b(int64_t a, int64_t b) {
+  int64_t q = a / b;
+  if ((a % b != 0) && ((a < 0) != (b < 0))) q--;
+  return q;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- spread
+
+// CTA: 64 consecutive cells x (32*SPL) signals; warp w owns cells
+// [j0 + 8w, j0 + 8w + 8).  Contributing nodes (all periodic images, from
+// `ranges`) are streamed through shared memory in batches of kSpreadCap:
+// per node one padded weight row (zeros outside the window, so the 8-cell
+// inner product needs no predicates) and the node's amplitudes for every
+// signal of the CTA.
+template <int SPL>
+__global__ void __launch_bounds__(256, 2) k_spread_b(const double* __restrict__ ts, const int* __restrict__ perm,
+                                                    int64_t Q, int64_t n, double alpha, GaussTab G,
+                                                    const double2* __restrict__ amp, int64_t batch, NodeFactor nf,
+                                                    double2* __restrict__ H, const int2* __restrict__ ranges,
+                                                    int NS) {
+  constexpr int SIG = 32 * SPL;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double2* A = reinterpret_cast<double2*>(smraw);                              // [cap][SIG] swizzled
+  double* W = reinterpret_cast<double*>(A + kSpreadCap * SIG);                 // [cap][kWRow]
+  double2* F = reinterpret_cast<double2*>(W + kSpreadCap * kWRow);             // [cap] node factor
+  int* Cc = reinterpret_cast<int*>(F + kSpreadCap);                            // [cap] image index (scratch)
+  int* Pi = Cc + kSpreadCap;                                                   // [cap] caller index
+  int* Qs = Pi + kSpreadCap;                                                   // [cap] ascending index
+  int* Cc2 = Qs + kSpreadCap;                                                  // [cap] effective centre
+  __shared__ int s_cnt[8];
+  __shared__ int s_off[8];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t j0 = (int64_t)blockIdx.x * kSpreadTile;
+  const int64_t b0 = (int64_t)blockIdx.y * SIG;
+  const int jw = (int)j0 + warp * kCPW;  // first cell of this warp
+  const int64_t s_lo = floordiv_b(-kM - (min(j0 + kSpreadTile, n) - 1) + n - 1, n);
+
+  // concatenated node list over periodic images
+  if (tid == 0) {
+    int acc = 0;
+    for (int si = 0; si < NS && si < 8; si++) {
+      int2 r = ranges[blockIdx.x * (int64_t)NS + si];
+      s_off[si] = acc;
+      s_cnt[si] = r.y - r.x;
+      acc += r.y - r.x;
+    }
+  }
+  __syncthreads();
+  int total = 0;
+  for (int si = 0; si < NS && si < 8; si++) total += s_cnt[si];
+
+  double2 acc[kCPW][SPL];
+#pragma unroll
+  for (int c = 0; c < kCPW; c++)
+#pragma unroll
+    for (int s = 0; s < SPL; s++) acc[c][s] = make_double2(0.0, 0.0);
+
+  for (int base = 0; base < total; base += kSpreadCap) {
+    const int cnt = min(kSpreadCap, total - base);
+    __syncthreads();
+    // phase 0: node index and caller position (sources of the async copies)
+    for (int e = tid; e < cnt; e += blockDim.x) {
+      int g = base + e, si = 0;
+      while (si + 1 < NS && si + 1 < 8 && g >= s_off[si + 1]) si++;
+      const int64_t q = ranges[blockIdx.x * (int64_t)NS + si].x + (g - s_off[si]);
+      Qs[e] = (int)q;
+      Pi[e] = perm[q];
+      Cc[e] = si;  // image index for now
+    }
+    __syncthreads();
+    // phase 1: amplitudes, transposed to [node][signal] with async copies
+    // (one signal row per warp pass: lanes read consecutive nodes)
+    for (int sig = warp; sig < SIG; sig += kSpreadWarps) {
+      const int64_t b = b0 + sig;
+      const bool ok = b < batch;
+      const double2* row = amp + (ok ? b : 0) * Q;
+      for (int e = lane; e < cnt; e += 32) cp_async16(&A[e * SIG + swz(sig, e)], row + Pi[e], ok);
+    }
+    // phase 2 (overlaps the copies): geometry, padded weight rows, factors
+    for (int e = tid; e < cnt; e += blockDim.x) {
+      const int64_t q = Qs[e];
+      const int si = Cc[e];
+      const double t = ts[q];
+      const NodeGeo geo = node_geo(t, (double)n);
+      const int ce = (int)((int64_t)geo.i0 - (s_lo + si) * n);
+      F[e] = factor_at(nf, q, t);
+      double w[2 * kM + 1];
+      taps29(geo.f, alpha, G, w);
+      double* row = W + e * kWRow;
+      // parity shift makes every 8-cell read 16-byte aligned; two unrolled
+      // variants keep w[] in registers
+      if ((ce + 1) & 1) {
+#pragma unroll
+        for (int x = 0; x < kWRow; x++) {
+          const int k = x - 1 - kM - 7;
+          row[x] = (k >= -kM && k <= kM) ? w[(k >= -kM && k <= kM) ? k + kM : 0] : 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int x = 0; x < kWRow; x++) {
+          const int k = x - kM - 7;
+          row[x] = (k >= -kM && k <= kM) ? w[(k >= -kM && k <= kM) ? k + kM : 0] : 0.0;
+        }
+      }
+      Cc2[e] = ce;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // phase 3: every warp accumulates its 8 cells for all nodes of the batch
+    for (int e = 0; e < cnt; e++) {
+      const int ce = Cc2[e];
+      const int o = jw - ce;  // tap index of cell jw
+      if (o < -kM - 7 || o > kM) continue;
+      const int x = o + kM + 7 + ((ce + 1) & 1);
+      const double2* wr = reinterpret_cast<const double2*>(W + e * kWRow + x);
+      const double2 w01 = wr[0], w23 = wr[1], w45 = wr[2], w67 = wr[3];
+      const double wc[8] = {w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, w67.x, w67.y};
+      const double2 fe = F[e];
+#pragma unroll
+      for (int s = 0; s < SPL; s++) {
+        const double2 a = cmul(A[e * SIG + swz(lane + 32 * s, e)], fe);
+#pragma unroll
+        for (int c = 0; c < kCPW; c++) caxpy(acc[c][s], wc[c], a);
+      }
+    }
+  }
+  // write: stage [cell][signal] then coalesced rows per signal
+  __syncthreads();
+  double2* O = A;  // reuse (kSpreadCap * SIG >= kSpreadTile * SIG)
+#pragma unroll
+  for (int c = 0; c < kCPW; c++)
+#pragma unroll
+    for (int s = 0; s < SPL; s++) {
+      const int cell = warp * kCPW + c;
+      O[cell * SIG + swz(lane + 32 * s, cell)] = acc[c][s];
+    }
+  __syncthreads();
+  const int ncell = (int)min((int64_t)kSpreadTile, n - j0);
+  for (int sig = warp; sig < SIG; sig += kSpreadWarps) {
+    const int64_t b = b0 + sig;
+    if (b >= batch) break;
+    for (int cell = lane; cell < ncell; cell += 32) H[b * n + j0 + cell] = O[cell * SIG + swz(sig, cell)];
+  }
+}
+
+int spread_batched(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch, NodeFactor f,
+                   double2* H, cudaStream_t st, int spl) {
+  const int64_t ntiles = ceil_div(n, kSpreadTile);
+  const int NS = (int)((2 * win.m + kSpreadTile - 1) / n + 3);
+  if (NS > 8) return NFFT45_ERR_INVALID_ARGUMENT;  // tiny grids use the generic kernel
+  int2* ranges = nullptr;
+  NFFT_CUDA(cudaMallocAsync(&ranges, sizeof(int2) * ntiles * NS, st));
+  LAUNCH(k_tile_ranges, (unsigned)ceil_div(ntiles * NS, 128), 128, 0, st, g.ts, g.Q, n, win.m, kSpreadTile, ntiles,
+         NS, ranges);
+  GaussTab G = gauss_tab(win);
+  if (spl == 2) {
+    constexpr int SIG = 64;
+    size_t smem = (size_t)kSpreadCap * SIG * 16 + (size_t)kSpreadCap * kWRow * 8 + kSpreadCap * 16 + kSpreadCap * 16;
+    auto spread_b = k_spread_b<2>;
+    NFFT_CUDA(cudaFuncSetAttribute(spread_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((unsigned)ntiles, (unsigned)ceil_div(batch, SIG));
+    LAUNCH(spread_b, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, amp, batch, f, H, ranges, NS);
+  } else {
+    constexpr int SIG = 32;
+    size_t smem = (size_t)kSpreadCap * SIG * 16 + (size_t)kSpreadCap * kWRow * 8 + kSpreadCap * 16 + kSpreadCap * 16;
+    auto spread_b = k_spread_b<1>;
+    NFFT_CUDA(cudaFuncSetAttribute(spread_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((unsigned)ntiles, (unsigned)ceil_div(batch, SIG));
+    LAUNCH(spread_b, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, amp, batch, f, H, ranges, NS);
+  }
+  NFFT_CUDA(cudaFreeAsync(ranges, st));
+  return NFFT45_OK;
+}
+
+// ------------------------------------------------------------- gather
+
+// CTA: 32 consecutive ascending nodes x 32 signals (lane = signal); warp w
+// owns nodes 8w..8w+7.  The cells under the CTA's windows are staged as
+// [cell][signal] in chunks of kGatherSpan; each warp builds a dense weight
+// table WT[cell][8 nodes] for its own cells (zeros outside windows) so one
+// staged cell value feeds 8 FMAs with one 64-byte broadcast of weights.
+__global__ void __launch_bounds__(128, 3) k_gather_b(const double* __restrict__ ts, const int* __restrict__ perm,
+                                                    int64_t Q, int64_t n, double alpha, GaussTab G,
+                                                    const double2* __restrict__ H, int64_t batch, NodeFactor nf,
+                                                    const double2* __restrict__ sub, int mode,
+                                                    double2* __restrict__ out) {
+  constexpr int SIG = 32;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double2* Y = reinterpret_cast<double2*>(smraw);                                // [span][SIG]
+  double* WT = reinterpret_cast<double*>(Y + kGatherSpan * SIG);                 // [warps][kWTSpan][8]
+  __shared__ int s_c0[kGatherNodes];
+  __shared__ double s_f[kGatherNodes];
+  __shared__ double2 s_fac[kGatherNodes];
+  __shared__ int s_pq[kGatherNodes];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t q0 = (int64_t)blockIdx.x * kGatherNodes;
+  const int64_t b0 = (int64_t)blockIdx.y * SIG;
+  const int nq = (int)min((int64_t)kGatherNodes, Q - q0);
+
+  if (tid < kGatherNodes) {
+    int c = 0;
+    double f = 0.0;
+    if (tid < nq) {
+      const double t = ts[q0 + tid];
+      NodeGeo geo = node_geo(t, (double)n);
+      c = geo.i0;
+      f = geo.f;
+      s_fac[tid] = factor_at(nf, q0 + tid, t);
+      s_pq[tid] = perm[q0 + tid];
+    } else if (nq > 0) {
+      NodeGeo geo = node_geo(ts[q0 + nq - 1], (double)n);
+      c = geo.i0;
+    }
+    s_c0[tid] = c;
+    s_f[tid] = f;
+  }
+  __syncthreads();
+  // unwrapped cell span of the CTA and of this warp (centres ascend)
+  const int cta_lo = s_c0[0] - kM, cta_hi = s_c0[kGatherNodes - 1] + kM;
+  const int w_lo = s_c0[warp * kNPW] - kM, w_hi = s_c0[warp * kNPW + kNPW - 1] + kM;
+  double* wt = WT + warp * kWTSpan * kNPW;
+
+  double2 acc[kNPW];
+#pragma unroll
+  for (int i = 0; i < kNPW; i++) acc[i] = make_double2(0.0, 0.0);
+
+  for (int cs = cta_lo; cs <= cta_hi; cs += kGatherSpan) {
+    const int ce = min(cs + kGatherSpan - 1, cta_hi);
+    const int len = ce - cs + 1;
+    __syncthreads();  // previous chunk fully consumed
+    // stage cells [cs, ce] (mod n) for the CTA's signals
+    for (int sig = warp; sig < SIG; sig += kGatherWarps) {
+      const int64_t b = b0 + sig;
+      const bool ok = b < batch;
+      const double2* row = H + (ok ? b : 0) * n;
+      for (int c = lane; c < len; c += 32) {
+        int64_t cell = (int64_t)(cs + c);
+        if (cell < 0) cell += n;
+        if (cell >= n) cell -= n;
+        if (cell < 0 || cell >= n) {  // tiny grids: full reduction
+          cell %= n;
+          if (cell < 0) cell += n;
+        }
+        cp_async16(&Y[c * SIG + swz(sig, c)], row + cell, ok);
+      }
+    }
+    // this warp's cells inside the chunk, in sub-chunks of kWTSpan (warp-private
+    // table); the first table is built while the copies are in flight
+    const int a_lo = max(w_lo, cs), a_hi = min(w_hi, ce);
+    auto build = [&](int ws, int we) {
+      const int wl = we - ws + 1;
+      __syncwarp();
+      for (int i = lane; i < wl * kNPW; i += 32) wt[i] = 0.0;
+      __syncwarp();
+      if (lane < kNPW && warp * kNPW + lane < nq) {
+        double w[2 * kM + 1];
+        taps29(s_f[warp * kNPW + lane], alpha, G, w);
+        const int c0 = s_c0[warp * kNPW + lane] - kM;
+#pragma unroll
+        for (int k = 0; k < 2 * kM + 1; k++) {
+          const int c = c0 + k;
+          if (c >= ws && c <= we) wt[(c - ws) * kNPW + lane] = w[k];
+        }
+      }
+      __syncwarp();
+    };
+    if (a_lo <= a_hi) build(a_lo, min(a_lo + kWTSpan - 1, a_hi));
+    cp_async_wait_all();
+    __syncthreads();
+    for (int ws = a_lo; ws <= a_hi; ws += kWTSpan) {
+      const int we = min(ws + kWTSpan - 1, a_hi);
+      if (ws != a_lo) build(ws, we);
+      for (int c = ws; c <= we; c++) {
+        const double2 y = Y[(c - cs) * SIG + swz(lane, c - cs)];
+        const double2* wr = reinterpret_cast<const double2*>(wt + (c - ws) * kNPW);
+        const double2 w01 = wr[0], w23 = wr[1], w45 = wr[2], w67 = wr[3];
+        caxpy(acc[0], w01.x, y);
+        caxpy(acc[1], w01.y, y);
+        caxpy(acc[2], w23.x, y);
+        caxpy(acc[3], w23.y, y);
+        caxpy(acc[4], w45.x, y);
+        caxpy(acc[5], w45.y, y);
+        caxpy(acc[6], w67.x, y);
+        caxpy(acc[7], w67.y, y);
+      }
+    }
+  }
+  // epilogue: factor, optional subtraction, transposed coalesced store
+  __syncthreads();
+  double2* O = Y;  // [node][SIG]
+#pragma unroll
+  for (int i = 0; i < kNPW; i++) {
+    const int e = warp * kNPW + i;
+    O[e * SIG + swz(lane, e)] = acc[i];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < kGatherNodes * SIG; idx += blockDim.x) {
+    const int e = idx & (kGatherNodes - 1), sig = idx / kGatherNodes;
+    const int64_t b = b0 + sig;
+    if (b >= batch || e >= nq) continue;
+    const double2 fq = s_fac[e];
+    double2 v = cmul(O[e * SIG + swz(sig, e)], fq);
+    const int64_t pq = s_pq[e];
+    if (mode == 1) v = csub(v, sub[b * Q + pq]);
+    else if (mode == 2) v = csub(sub[b * Q + pq], v);
+    out[b * Q + pq] = v;
+  }
+}
+
+int gather_batched(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch, NodeFactor f,
+                   const double2* sub, int mode, double2* out, cudaStream_t st) {
+  size_t smem = (size_t)kGatherSpan * 32 * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8;
+  auto gather_b = k_gather_b;
+  NFFT_CUDA(cudaFuncSetAttribute(gather_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)ceil_div(g.Q, kGatherNodes), (unsigned)ceil_div(batch, 32));
+  LAUNCH(gather_b, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), H, batch, f, sub,
+         mode, out);
+  return NFFT45_OK;
+}
+
+}  // namespace nfft45

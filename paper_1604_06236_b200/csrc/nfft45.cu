@@ -15,7 +15,35 @@
 namespace nfft45 {
 
 std::atomic<int64_t> g_launches{0};
+std::atomic<int> g_profiling{0};
 static thread_local std::string tl_err;
+
+// ------------------------------------------------- per-launch profiling
+struct ProfRec {
+  cudaEvent_t e0, e1;
+  std::string name;
+  bool used;
+};
+static std::mutex g_prof_mu;
+static std::vector<ProfRec> g_prof;
+
+int prof_begin(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  ProfRec r;
+  if (cudaEventCreate(&r.e0) != cudaSuccess || cudaEventCreate(&r.e1) != cudaSuccess) return -1;
+  r.used = false;
+  cudaEventRecord(r.e0, st);
+  g_prof.push_back(r);
+  return (int)g_prof.size() - 1;
+}
+
+void prof_end(int slot, const char* name, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (slot < 0 || slot >= (int)g_prof.size()) return;
+  g_prof[slot].name = name;
+  g_prof[slot].used = true;
+  cudaEventRecord(g_prof[slot].e1, st);
+}
 
 void set_error(int code, const std::string& msg) {
   (void)code;
@@ -95,6 +123,8 @@ struct nfft45_plan {
   double2* tables;  // one allocation holding everything below
   double2 *v, *ks, *L, *dL, *nw, *decay, *coef;
   double2 *c5, *c4;  // ascending-node fused factors nw * cis(-/+ K t)
+  double* rtab;      // real copies: decay, coef_scale, deconvolution (length P each)
+  double *rdecay, *rcoef, *rdeconv;
 };
 
 // ------------------------------------------------------------- kernels
@@ -198,6 +228,17 @@ __global__ void k_plan_tables(const double* __restrict__ t, const double* __rest
   double2 ct = cis_turns(tq >= 0.5 ? tq - 1.0 : tq);
   double2 w = cdiv(h, cmul(dL[q], ct));
   nw[q] = w;
+}
+
+// real solve tables for the fused chains
+__global__ void k_real_tables(const double2* __restrict__ decay, const double2* __restrict__ coef, int64_t P,
+                              double b, double* __restrict__ rdecay, double* __restrict__ rcoef,
+                              double* __restrict__ rdeconv) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  rdecay[p] = decay[p].x;
+  rcoef[p] = coef[p].x;
+  rdeconv[p] = deconv_weight(p, P / 2, 2 * P, b);
 }
 
 __global__ void k_fused_factors(const double* __restrict__ ts, const int* __restrict__ perm,
@@ -330,7 +371,26 @@ static int check_guards(const double* d_guard, int have_re, int have_dl, cudaStr
 
 // ------------------------------------------------------------- solves
 
+static ChainPlanView chain_view(const nfft45_plan* p) {
+  ChainPlanView v;
+  v.g = &p->g->d;
+  v.P = p->P;
+  v.ks = p->ks;
+  v.c5 = p->c5;
+  v.c4 = p->c4;
+  v.decay = p->rdecay;
+  v.coef = p->rcoef;
+  v.deconv = p->rdeconv;
+  return v;
+}
+
+static bool use_chain(const nfft45_plan* p) {
+  static const bool off = getenv("NFFT45_NO_CHAIN") != nullptr;  // A/B switch for tests
+  return !off && chain_supported(p->P, p->m);
+}
+
 static int type5_core(const nfft45_plan* p, const double2* s, int64_t batch, double2* out, cudaStream_t st) {
+  if (use_chain(p)) return chain_run(chain_view(p), 5, s, batch, 0, out, nullptr, st);
   const GridDev& g = p->g->d;
   const int64_t P = p->P, n = 2 * P, K = P / 2;
   Window win = Window::make(p->m);
@@ -347,6 +407,7 @@ static int type5_core(const nfft45_plan* p, const double2* s, int64_t batch, dou
 }
 
 static int type4_core(const nfft45_plan* p, const double2* A, int64_t batch, double2* out, cudaStream_t st) {
+  if (use_chain(p)) return chain_run(chain_view(p), 4, A, batch, 0, out, nullptr, st);
   const GridDev& g = p->g->d;
   const int64_t P = p->P, n = 2 * P, K = P / 2;
   Window win = Window::make(p->m);
@@ -366,8 +427,34 @@ typedef int (*SolveFn)(const nfft45_plan*, const double2*, int64_t, double2*, cu
 
 // Section V refinement (inverse.py:146-162).  fwd5: residual via type-2
 // (sample domain) else via type-1 of length P (spectrum domain).
+static int check_norms(const double* d_norms, int64_t batch, int passes, cudaStream_t st) {
+  std::vector<double> h((size_t)batch * passes);
+  NFFT_CUDA(cudaMemcpyAsync(h.data(), d_norms, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+  NFFT_CUDA(cudaStreamSynchronize(st));
+  for (int pass = 1; pass < passes; pass++)
+    for (int64_t b = 0; b < batch; b++) {
+      double prev = h[(size_t)(pass - 1) * batch + b], cur = h[(size_t)pass * batch + b];
+      if (cur > prev) {
+        char buf[200];
+        snprintf(buf, sizeof buf,
+                 "residual norm grew between passes (%.3e -> %.3e); method error >= 1 at these parameters", prev,
+                 cur);
+        return fail(NFFT45_ERR_NON_CONVERGENCE, buf);
+      }
+    }
+  return NFFT45_OK;
+}
+
 static int refine_core(const nfft45_plan* p, const double2* data, int64_t batch, int passes, double2* out,
                        bool type5, cudaStream_t st) {
+  if (use_chain(p) && (type5 || passes <= 1)) {
+    Scratch norms(st);
+    if (passes >= 2) NFFT_CHECK(norms.alloc(sizeof(double) * batch * passes));
+    NFFT_CHECK(chain_run(chain_view(p), type5 ? 5 : 4, data, batch, passes, out, passes >= 2 ? norms.d() : nullptr,
+                         st));
+    if (passes >= 2) return check_norms(norms.d(), batch, passes, st);
+    return NFFT45_OK;
+  }
   SolveFn solve = type5 ? type5_core : type4_core;
   NFFT_CHECK(solve(p, data, batch, out, st));
   if (passes <= 0) return NFFT45_OK;
@@ -412,6 +499,41 @@ extern "C" {
 const char* nfft45_last_error(void) { return tl_err.c_str(); }
 int nfft45_version(void) { return 100; }
 int64_t nfft45_launch_count(void) { return g_launches.load(); }
+
+int nfft45_profile_enable(int on) {
+  g_profiling.store(on ? 1 : 0);
+  return NFFT45_OK;
+}
+
+int nfft45_profile_read(char* buf, int64_t cap) {
+  // synchronizes on every recorded event; emits "name count total_ms\n" lines
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  std::vector<std::pair<std::string, std::pair<int64_t, double>>> agg;
+  for (auto& r : g_prof) {
+    float ms = 0.f;
+    if (r.used && cudaEventSynchronize(r.e1) == cudaSuccess && cudaEventElapsedTime(&ms, r.e0, r.e1) == cudaSuccess) {
+      bool found = false;
+      for (auto& a : agg)
+        if (a.first == r.name) { a.second.first++; a.second.second += ms; found = true; break; }
+      if (!found) agg.push_back({r.name, {1, (double)ms}});
+    }
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  g_prof.clear();
+  std::string out;
+  for (auto& a : agg) {
+    char line[512];
+    snprintf(line, sizeof line, "%s %lld %.6f\n", a.first.c_str(), (long long)a.second.first, a.second.second);
+    out += line;
+  }
+  if (buf && cap > 0) {
+    size_t n = std::min<size_t>(out.size(), (size_t)cap - 1);
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int)out.size();
+}
 
 int nfft45_validate_grid(const double* t, int64_t Q, double min_gap, int64_t* order) {
   char buf[256];
@@ -627,11 +749,15 @@ int nfft45_plan_create(const nfft45_grid* g, double a, int eta, int m, void* st,
   p->a = a;
   p->eta = eta;
   p->m = m;
-  cudaError_t e = cudaMalloc(&p->tables, sizeof(double2) * 9 * P);
+  cudaError_t e = cudaMalloc(&p->tables, sizeof(double2) * 9 * P + sizeof(double) * 3 * P);
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "cudaMalloc(plan)");
   }
+  p->rtab = reinterpret_cast<double*>(p->tables + 9 * P);
+  p->rdecay = p->rtab;
+  p->rcoef = p->rtab + P;
+  p->rdeconv = p->rtab + 2 * P;
   double2* t = p->tables;
   p->v = t;
   p->ks = t + P;
@@ -656,6 +782,9 @@ int nfft45_plan_create(const nfft45_grid* g, double a, int eta, int m, void* st,
       g_launches++;
       k_fused_factors<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(g->d.ts, g->d.perm, p->nw, P, (double)(P / 2),
                                                                 p->c5, p->c4);
+      g_launches++;
+      k_real_tables<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(p->decay, p->coef, P, Window::make(m).b, p->rdecay,
+                                                              p->rcoef, p->rdeconv);
       g_launches++;
       cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) status = cuda_fail(le, "plan tables");

@@ -41,6 +41,22 @@ int spread(const GridDev& g, int64_t n, const Window& win, const double2* amp, i
 // (forward.py:91-102).  Node-indexed vectors are in caller order.
 int gather(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch,
            NodeFactor f, const double2* sub, double2* out, cudaStream_t st);
+// mode 0: out = v;  1: out = v - sub;  2: out = sub - v  (v = factor * window sum)
+int gather_mode(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch,
+                NodeFactor f, const double2* sub, int mode, double2* out, cudaStream_t st);
+
+// Read-only view of a plan for the fused chains (chain.cu).
+struct ChainPlanView {
+  const GridDev* g;
+  int64_t P;
+  const double2 *ks, *c5, *c4;         // complex tables (c5/c4 in ascending-node order)
+  const double *decay, *coef, *deconv;  // real tables of length P
+};
+bool chain_supported(int64_t P, int m);
+// kind 5: type-5 (+ passes refinements); kind 4: type-4.  norms (may be
+// null): [passes][batch] residual norms for the type-5 refinement.
+int chain_run(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes, double2* out,
+              double* norms, cudaStream_t st);
 
 // out[b][q] = sum_{e<eta} X(eP + q),  X(p) = H[b][(p - K) mod n] * deconv(p) * tab[p]
 // (forward.py:64 band select + deconvolution, forward.py:153-154 fold).
@@ -64,6 +80,17 @@ int csub_batch(const double2* x, const double2* d, double2* y, int64_t total, cu
 
 // Per-signal l2 norms of r[b][0..len) into norms[b] (fixed-order reduction).
 int row_norms(const double2* r, int64_t len, int64_t batch, double* norms, cudaStream_t st);
+
+// Node range of every (tile of TC cells, periodic image) pair (gridding.cu).
+__global__ void k_tile_ranges(const double* __restrict__ ts, int64_t Q, int64_t n, int m, int TC, int64_t ntiles,
+                              int NS, int2* __restrict__ ranges);
+
+// Batched m = 14 kernels (gridding_b.cu): lanes over signals.  spl = signals
+// per lane (1 or 2) for the spread.
+int spread_batched(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch, NodeFactor f,
+                   double2* H, cudaStream_t st, int spl);
+int gather_batched(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch, NodeFactor f,
+                   const double2* sub, int mode, double2* out, cudaStream_t st);
 
 // Device deconvolution weight 1/(n Psi(nu)) of gridding.py:90.
 __device__ __forceinline__ double deconv_weight(int64_t p, int64_t K, int64_t n, double b) {

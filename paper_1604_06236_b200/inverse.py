@@ -169,36 +169,43 @@ def _charge_type4(f, P, taps):
     f.complex_mul(P)
 
 
-def _solve(name: str, plan: InversePlan, data, label: str, passes: int | None):
+def _solve(name: str, plan: InversePlan, data, label: str, passes: int | None, dest=None):
     a = _device.operand(data, plan.device, length=plan.size, name=label)
-    out = a.empty_like_rows(plan.size)
+    if dest is not None and dest.is_cuda and dest.dtype == _device.torch.complex128 and dest.is_contiguous():
+        out = dest.reshape(a.tensor.shape)
+        dest = None
+    else:
+        out = a.empty_like_rows(plan.size)
     st = _device.stream_handle(plan.device)
     if passes is None:
         _lib.call(f"nfft45_{name}", plan.handle, a.ptr, a.rows, out.data_ptr(), st)
     else:
         _lib.call(f"nfft45_refine_{name}", plan.handle, a.ptr, a.rows, int(passes), out.data_ptr(), st)
-    return a.finish(out)
+    return a.finish(out, dest)
 
 
-def type5(plan: InversePlan, samples, flops: FlopCounter | None = None):
-    """Coefficients S with sum_p S_p e^{2 pi i p t_q} = samples_q (inverse.py:101-120, Fig. 2)."""
-    out = _solve("type5", plan, samples, "samples", None)
+def type5(plan: InversePlan, samples, flops: FlopCounter | None = None, out=None):
+    """Coefficients S with sum_p S_p e^{2 pi i p t_q} = samples_q (inverse.py:101-120, Fig. 2).
+
+    `out` (extension): optional preallocated torch tensor (device, or pinned host) for the result."""
+    out = _solve("type5", plan, samples, "samples", None, out)
     _charge_type5(flops, plan.size, plan.kernel_base.taps)
     return out
 
 
-def type4(plan: InversePlan, spectrum, flops: FlopCounter | None = None):
+def type4(plan: InversePlan, spectrum, flops: FlopCounter | None = None, out=None):
     """Amplitudes a with sum_q a_q e^{-2 pi i p t_q} = spectrum_p (inverse.py:123-143, Fig. 3)."""
-    out = _solve("type4", plan, spectrum, "spectrum", None)
+    out = _solve("type4", plan, spectrum, "spectrum", None, out)
     _charge_type4(flops, plan.size, plan.kernel_base.taps)
     return out
 
 
-def refine_type4(plan: InversePlan, spectrum, passes: int | None = None, flops: FlopCounter | None = None):
+def refine_type4(plan: InversePlan, spectrum, passes: int | None = None, flops: FlopCounter | None = None,
+                 out=None):
     """type4 plus residual-correction passes (inverse.py:165-185, Section V)."""
     if passes is None:
         passes = plan.params.refine_passes
-    out = _solve("type4", plan, spectrum, "spectrum", passes)
+    out = _solve("type4", plan, spectrum, "spectrum", passes, out)
     P, taps = plan.size, plan.kernel_base.taps
     _charge_type4(flops, P, taps)
     for _ in range(passes):
@@ -209,11 +216,12 @@ def refine_type4(plan: InversePlan, spectrum, passes: int | None = None, flops: 
     return out
 
 
-def refine_type5(plan: InversePlan, samples, passes: int | None = None, flops: FlopCounter | None = None):
+def refine_type5(plan: InversePlan, samples, passes: int | None = None, flops: FlopCounter | None = None,
+                 out=None):
     """type5 plus residual-correction passes in the sample domain (inverse.py:188-202)."""
     if passes is None:
         passes = plan.params.refine_passes
-    out = _solve("type5", plan, samples, "samples", passes)
+    out = _solve("type5", plan, samples, "samples", passes, out)
     P, taps = plan.size, plan.kernel_base.taps
     _charge_type5(flops, P, taps)
     for _ in range(passes):

@@ -56,7 +56,7 @@ for i in range(int(z["plan_count"])):
         print(f"plan{i} FAILED {type(ex).__name__}: {ex}")
 
 # bigger: P=2^16 and 2^20 vs oracle (refined)
-for P, J, B in ((4096, 0.3, 4), (1 << 16, 0.3, 2), (1 << 20, 0.4, 1)):
+for P, J, B in ((4096, 0.3, 4), (4096, 0.3, 64), (1 << 16, 0.3, 2), (1 << 16, 0.45, 40), (1 << 20, 0.4, 1)):
     t, data = O.make_inputs(P, J, B, 7)
     g = nf.validate_grid(t)
     prm = nf.MethodParams.from_mu(1e-15, P, 2)
@@ -71,7 +71,12 @@ for P, J, B in ((4096, 0.3, 4), (1 << 16, 0.3, 2), (1 << 20, 0.4, 1)):
     # batched == loop
     if B > 1:
         single = nf.refine_type5(plan, x[1], passes=1)
-        print("batch==single bitwise:", np.array_equal(single, nf.refine_type5(plan, x, passes=1)[1]))
+        full = nf.refine_type5(plan, x, passes=1)
+        print("batch vs single: bitwise", np.array_equal(single, full[1]), "rel", rel(single, full[1]),
+              "repeat bitwise", np.array_equal(full, nf.refine_type5(plan, x, passes=1)))
+        if B >= 32:
+            for j in (0, B - 1):
+                print(f"  signal {j}: t5 err {rel(O.refine5(op, x[j], 1), full[j]):.2e}")
     print(f"P={P}: plan gpu {tp:.3f}s oracle {to:.3f}s")
 print("WORST", worst)
 print("launches", nf._lib.load().nfft45_launch_count())
