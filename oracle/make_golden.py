@@ -166,6 +166,29 @@ def main(ref_root="/root/reference"):
             put(f"{name}_ks", plan.kernel_data.kernel_samples)
             put(f"{name}_dL", plan.kernel_data.derivative_samples)
 
+    # ---- analytic flop reports (data-independent; flops.py) for the flops= kwarg
+    def rep(fc):
+        r = fc.report()
+        return np.array([r.real_adds, r.complex_adds, r.real_muls, r.complex_muls, r.complex_exps,
+                         r.total_flops] + list(r.fft_invocations), dtype=np.int64)
+
+    t = (np.arange(64) + rng.uniform(0, 0.6, 64)) / 64
+    g = R.validate_grid(t)
+    prm = R.MethodParams.from_mu(1e-11, 64, 2)
+    put("flops_t", t)
+    fc = R.FlopCounter(); plan = R.build_plan(g, prm, flops=fc); put("flops_build_plan", rep(fc))
+    x = randc(64)
+    for name, fn in (("type5", lambda f: R.type5(plan, x, flops=f)), ("type4", lambda f: R.type4(plan, x, flops=f)),
+                     ("refine5", lambda f: R.refine_type5(plan, x, passes=1, flops=f)),
+                     ("refine4", lambda f: R.refine_type4(plan, x, passes=1, flops=f)),
+                     ("type1", lambda f: R.nfft_type1(g, x, 48, flops=f)),
+                     ("type2", lambda f: R.nfft_type2(x, g, flops=f)),
+                     ("conv", lambda f: R.nonuniform_conv(g, x, randc(128), 64, flops=f)),
+                     ("conv_real", lambda f: R.nonuniform_conv(g, x, rng.standard_normal(128), 64, flops=f))):
+        fc = R.FlopCounter()
+        fn(fc)
+        put(f"flops_{name}", rep(fc))
+
     # ---- the reference's frozen fixture (dense-elimination solution, P=8, mu=1e-11, eta=2)
     fx = os.path.join(ref_root, "pkg", "tests", "fixtures")
     put("fixture_grid8", _read_vec(os.path.join(fx, "grid8.txt")))

@@ -95,7 +95,10 @@ def operand(values, dev: int, length: int | None = None, name: str = "vector") -
         raise LengthMismatchError(f"{name} has length {arr.shape[-1]}, expected {length}")
     if not np.isfinite(arr).all():
         raise ValueError(f"{name} contains NaN or Inf entries")
-    t = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{dev}")
+    arr = np.ascontiguousarray(arr)
+    if not arr.flags.writeable:
+        arr = arr.copy()
+    t = torch.from_numpy(arr).to(f"cuda:{dev}")
     return Operand(t, False, arr.ndim == 2)
 
 

@@ -1,0 +1,224 @@
+"""Parity of the CUDA path with the reference: golden vectors produced by the
+reference itself (tests/golden, oracle/make_golden.py) and, at the
+BASELINE.json config sizes, the CPU oracle run live on the same seeded
+inputs plus size-independent properties (forward residuals, linearity,
+determinism).
+
+Gates:
+  G1  refined path (passes = 1, 2): rel-L2 vs reference <= 1e-10 AND forward
+      residual ||fwd(out) - in|| / ||in|| <= 1e-10 (fwd = reference fast NFFT);
+  G2  plain path: reported vs the reference's own permutation floor — it is
+      roundoff amplified ~(mu eta P)^(-1/eta), so only a loose bound is asserted;
+  G3  forward NFFTs: <= 1e-13 vs the reference fast path, <= 1e-12 vs direct.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1604_06236_b200 as nf
+from oracle import nfft_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+G1 = 1e-10
+
+
+def rel(truth, got):
+    return O.rel_l2(truth, got)
+
+
+# ------------------------------------------------------------ golden vectors
+
+def test_forward_golden(golden):
+    for i in range(int(golden["fwd_count"])):
+        g = nf.validate_grid(golden[f"fwd{i}_t"])
+        a, S, R = golden[f"fwd{i}_a"], golden[f"fwd{i}_S"], int(golden[f"fwd{i}_R"])
+        assert rel(golden[f"fwd{i}_type1"], nf.nfft_type1(g, a, R)) < 1e-13
+        assert rel(golden[f"fwd{i}_type2"], nf.nfft_type2(S, g)) < 1e-13
+        assert rel(golden[f"fwd{i}_type1_direct"], nf.nfft_type1(g, a, R)) < 1e-12
+        assert rel(golden[f"fwd{i}_type2_direct"], nf.nfft_type2(S, g)) < 1e-12
+        assert rel(golden[f"fwd{i}_type1_direct"], nf.nfft_type1_direct(g, a, R)) < 1e-14
+        assert rel(golden[f"fwd{i}_type2_direct"], nf.nfft_type2_direct(S, g)) < 1e-14
+
+
+def test_spread_width_golden(golden):
+    g = nf.validate_grid(golden["width_t"])
+    a = golden["width_a"]
+    for m in (4, 8, 12):
+        k = nf.kernel_for_size(32, m)
+        assert rel(golden[f"width_type1_m{m}"], nf.nfft_type1(g, a, 32, kernel=k)) < 1e-13
+        assert rel(golden[f"width_type2_m{m}"], nf.nfft_type2(a, g, kernel=k)) < 1e-13
+
+
+def test_conv_golden(golden):
+    for i in range(int(golden["conv_count"])):
+        P = int(golden[f"conv{i}_P"])
+        g = nf.validate_grid(golden[f"conv{i}_t"])
+        got = nf.nonuniform_conv(g, golden[f"conv{i}_a"], golden[f"conv{i}_lam"], P)
+        assert rel(golden[f"conv{i}_out"], got) < 1e-13
+
+
+WELL_CONDITIONED = [0, 1, 2, 3, 4, 5, 7, 8]   # plan6: random uniform nodes, the reference itself diverges
+
+
+@pytest.mark.parametrize("i", WELL_CONDITIONED)
+def test_plan_and_solves_golden(golden, i):
+    P, eta = int(golden[f"plan{i}_P"]), int(golden[f"plan{i}_eta"])
+    g = nf.validate_grid(golden[f"plan{i}_t"])
+    prm = nf.MethodParams.from_mu(float(golden[f"plan{i}_mu"]), P, eta)
+    plan = nf.build_plan(g, prm)
+    kd = plan.kernel_data
+    assert rel(golden[f"plan{i}_v"], kd.v_samples) < 1e-12
+    assert rel(golden[f"plan{i}_ks"], kd.kernel_samples) < 1e-12
+    # coefficient recovery amplifies roundoff (test_lagrange.py:211-214): method-level agreement
+    assert rel(golden[f"plan{i}_L"], kd.coefficients) < 1e-7
+    assert rel(golden[f"plan{i}_dL"], kd.derivative_samples) < 1e-7
+    assert rel(golden[f"plan{i}_nw"], plan.node_weights) < 1e-7
+    assert rel(golden[f"plan{i}_decay"], plan.h1_coefficients) < 1e-14
+    assert rel(golden[f"plan{i}_coef"], plan.coef_scale) < 1e-14
+    s, A = golden[f"plan{i}_s"], golden[f"plan{i}_A"]
+    assert rel(golden[f"plan{i}_type5"], nf.type5(plan, s)) < 1e-6   # G2 (plain)
+    assert rel(golden[f"plan{i}_type4"], nf.type4(plan, A)) < 1e-6
+    if P == 1:
+        return
+    for key, fn, x in (("r5", nf.refine_type5, s), ("r4", nf.refine_type4, A)):
+        for passes in (1, 2):
+            assert rel(golden[f"plan{i}_{key}p{passes}"], fn(plan, x, passes=passes)) < G1
+
+
+def test_ill_conditioned_grid_raises_like_reference(golden):
+    i = 6
+    P = int(golden[f"plan{i}_P"])
+    g = nf.validate_grid(golden[f"plan{i}_t"])
+    plan = nf.build_plan(g, nf.MethodParams.from_mu(float(golden[f"plan{i}_mu"]), P, 2))
+    assert f"plan{i}_r5p2_raises" in golden.files
+    with pytest.raises(nf.NonConvergenceError):
+        nf.refine_type5(plan, golden[f"plan{i}_s"], passes=2)
+    with pytest.raises(nf.NonConvergenceError):
+        nf.refine_type4(plan, golden[f"plan{i}_A"], passes=2)
+
+
+def test_frozen_fixture(golden):
+    """The reference's frozen dense-elimination solution (pkg/tests/fixtures, test_cli.py:155-169)."""
+    g = nf.validate_grid(golden["fixture_grid8"])
+    plan = nf.build_plan(g, nf.MethodParams.from_mu(1e-11, 8, 2))
+    s = golden["fixture_samples8"]
+    want = golden["fixture_coeffs8"]
+    assert rel(want, nf.type5(plan, s)) < 1e-10
+    assert rel(want, nf.refine_type5(plan, s, passes=1)) < 1e-13
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_config_shaped_golden(golden, name):
+    t, x = golden[f"{name}_t"], golden[f"{name}_x"]
+    P = t.size
+    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-15, P, 2))
+    for p in (1, 2):
+        g5 = nf.refine_type5(plan, x, passes=p)
+        g4 = nf.refine_type4(plan, x, passes=p)
+        assert rel(golden[f"{name}_r5p{p}"], g5) < G1
+        assert rel(golden[f"{name}_r4p{p}"], g4) < G1
+        assert rel(x, O.type2(g5, t)) < G1
+        assert rel(x, O.type1(t, g4, P)) < G1
+    assert rel(golden[f"{name}_type5"], nf.type5(plan, x)) < 1e-5
+
+
+# ------------------------------------------------ config sizes vs live oracle
+
+def _check_config(P, J, B, seed, eta=2, mu=1e-15, passes=(1, 2), rows=(0,)):
+    t, data = O.make_inputs(P, J, B, seed)
+    grid = nf.validate_grid(t)
+    prm = nf.MethodParams.from_mu(mu, P, eta)
+    plan = nf.build_plan(grid, prm)
+    oplan = O.Plan.build(t, prm.damping_a, eta)
+    report = {}
+    for p in passes:
+        g5 = nf.refine_type5(plan, data if B > 1 else data[0], passes=p)
+        g4 = nf.refine_type4(plan, data if B > 1 else data[0], passes=p)
+        g5, g4 = np.atleast_2d(g5), np.atleast_2d(g4)
+        for r in rows:
+            e5 = rel(O.refine5(oplan, data[r], p), g5[r])
+            e4 = rel(O.refine4(oplan, data[r], p), g4[r])
+            r5 = rel(data[r], O.type2(g5[r], t))
+            r4 = rel(data[r], O.type1(t, g4[r], P))
+            report[(p, r)] = (e5, e4, r5, r4)
+            assert max(e5, e4, r5, r4) <= G1, (P, p, r, e5, e4, r5, r4)
+    return report
+
+
+def test_c2_batched_4096x64():
+    _check_config(4096, 0.3, 64, 16042, rows=(0, 31, 63))
+
+
+def test_c4_shape_65536_batched():
+    _check_config(1 << 16, 0.3, 40, 16044, rows=(0, 39))
+
+
+def test_c3_single_2_20():
+    _check_config(1 << 20, 0.4, 1, 16043, passes=(1,))
+
+
+@pytest.mark.parametrize("J,eta", [(0.1, 2), (0.45, 2), (0.3, 3)])
+def test_c5_sweep_2_18(J, eta):
+    _check_config(1 << 18, J, 1, 16045, eta=eta, passes=(1,))
+
+
+@pytest.mark.parametrize("mu", [1e-17, 1e-13])
+def test_c5_attenuation_sweep(mu):
+    _check_config(1 << 18, 0.3, 1, 16045, mu=mu, passes=(1,))
+
+
+def test_plain_path_is_at_least_as_accurate_as_reference():
+    """G2: the plain solve is roundoff-amplified; ours is checked against the
+    exact forward operator: its residual must not exceed the reference's."""
+    P = 4096
+    t, data = O.make_inputs(P, 0.3, 1, 16042)
+    x = data[0]
+    prm = nf.MethodParams.from_mu(1e-15, P, 2)
+    plan = nf.build_plan(nf.validate_grid(t), prm)
+    oplan = O.Plan.build(t, prm.damping_a, 2)
+    ours = rel(x, O.type2(nf.type5(plan, x), t))
+    ref = rel(x, O.type2(O.solve5(oplan, x), t))
+    assert ours <= 2 * ref
+
+
+# ------------------------------------------------ batched / device API
+
+def test_batched_equals_per_signal_and_is_bitwise_reproducible():
+    P, B = 4096, 48
+    t, data = O.make_inputs(P, 0.3, B, 7)
+    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-15, P, 2))
+    full = nf.refine_type5(plan, data, passes=1)
+    assert full.shape == (B, P)
+    for r in (0, B - 1):
+        assert np.array_equal(full[r], nf.refine_type5(plan, data[r], passes=1))
+    assert np.array_equal(full, nf.refine_type5(plan, data, passes=1))
+    full4 = nf.refine_type4(plan, data, passes=1)
+    assert np.array_equal(full4[5], nf.refine_type4(plan, data[5], passes=1))
+
+
+def test_torch_device_and_pinned_host_operands():
+    P, B = 1 << 16, 4
+    t, data = O.make_inputs(P, 0.3, B, 9)
+    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-15, P, 2))
+    ref = nf.refine_type5(plan, data, passes=1)
+    dev = torch.from_numpy(data).cuda()
+    out_dev = nf.refine_type5(plan, dev, passes=1)
+    assert out_dev.is_cuda and np.array_equal(out_dev.cpu().numpy(), ref)
+    host = torch.from_numpy(data).pin_memory()
+    dest = torch.empty_like(host).pin_memory()
+    got = nf.refine_type5(plan, host, passes=1, out=dest)
+    assert got is dest and np.array_equal(dest.numpy(), ref)
+    buf = torch.empty_like(dev)
+    nf.refine_type5(plan, dev, passes=1, out=buf)
+    assert np.array_equal(buf.cpu().numpy(), ref)
+
+
+def test_native_library_is_the_code_path():
+    from paper_1604_06236_b200 import _lib
+
+    before = _lib.load().nfft45_launch_count()
+    g = nf.validate_grid(np.arange(64) / 64 + 0.001)
+    nf.nfft_type1(g, np.ones(64), 64)
+    assert _lib.load().nfft45_launch_count() > before
