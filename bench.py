@@ -62,6 +62,14 @@ ALGO_BYTES_PER_POINT_STEP = {
     "chain_mid": 4 * 32,         # 4 x (IFFT_P row pass + FFT_P column pass)
     "chain_pad": 3 * 48,         # 3 x (FFT_P row pass + IFFT_2P column pass)
     "chain_row": 3 * 32 + 16,    # 3 x (IFFT_2P row pass) + 1 x (FFT_P row pass)
+    # batch-minor chains (batches >= 16): same stages, plus the two layout-boundary kernels
+    "bm_col": 3 * 32,            # 3 x FFT_2P column pass
+    "bm_colin": 16,              # 1 x IFFT_P column pass (type-4 input, signal-major -> batch-minor)
+    "bm_band": 3 * 48,
+    "bm_mid": 4 * 32,
+    "bm_pad": 3 * 48,
+    "bm_row": 3 * 32,            # 3 x IFFT_2P row pass
+    "bm_rowout": 16,             # 1 x FFT_P row pass (type-5 output, batch-minor -> signal-major)
 }
 
 
@@ -266,6 +274,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
+                    help="run the step's type-5 and type-4 solves on 1 or 2 CUDA streams")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = CONFIGS[args.config]
@@ -302,10 +312,18 @@ def main():
     out5 = torch.empty_like(s_in)
     out4 = torch.empty_like(A_in)
     stream = torch.cuda.current_stream(dev)
+    side = torch.cuda.Stream(dev)  # the type-4 solve of a step runs beside the type-5 solve
 
     def step():
-        nf.refine_type5(plan, s_in, passes=PASSES, out=out5)
-        nf.refine_type4(plan, A_in, passes=PASSES, out=out4)
+        if args.streams == 2:
+            side.wait_stream(stream)
+            nf.refine_type5(plan, s_in, passes=PASSES, out=out5)
+            with torch.cuda.stream(side):
+                nf.refine_type4(plan, A_in, passes=PASSES, out=out4)
+            stream.wait_stream(side)
+        else:
+            nf.refine_type5(plan, s_in, passes=PASSES, out=out5)
+            nf.refine_type4(plan, A_in, passes=PASSES, out=out4)
 
     for _ in range(args.warmup):
         step()
@@ -375,7 +393,7 @@ def main():
         traffic = None
         tfile = os.path.join(REPO, "profiles", f"traffic_{args.config}.json")
         if os.path.exists(tfile):
-            traffic = json.load(open(tfile)).get(tname.strip("()").split("<")[0])
+            traffic = json.load(open(tfile)).get(tname)
         roof = {"kernel": tname, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes_per_launch": algo,
                 "avg_launch_ms": avg_ms, "launches": tcount, "share_of_kernel_time": tms / step_kernel_ms,
@@ -393,7 +411,7 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["label"], "P": P, "signals_per_gpu": B, "global_batch": B * world, "eta": ETA,
                    "mu": MU, "damping_a": params.damping_a, "spread_width": 14, "refine_passes": PASSES,
-                   "jitter": cfg["J"], "parallelism": f"signal-sharded x{world}",
+                   "jitter": cfg["J"], "parallelism": f"signal-sharded x{world}", "streams": args.streams,
                    "l2": f"inputs larger than L2 ({2 * B * P * 16 / 2**30:.2f} GiB per step)" if B * P >= 1 << 22
                    else "inputs fit in L2 (small config)"},
         "roofline": roof,

@@ -24,10 +24,6 @@ namespace {
 
 __device__ __forceinline__ double2 rscale(double2 v, double s) { return make_double2(v.x * s, v.y * s); }
 
-__device__ __forceinline__ double2 tw_pair(const double2* __restrict__ lo, const double2* __restrict__ hi, int s,
-                                           int64_t e) {
-  return cmul(__ldg(&hi[e >> s]), __ldg(&lo[e & ((int64_t(1) << s) - 1)]));
-}
 
 }  // namespace
 
@@ -38,7 +34,8 @@ template <int M, int C>
 __global__ void __launch_bounds__(fast_threads<2 * M, C>(), 2) kc_band(
     const double2* __restrict__ T, double2* __restrict__ U, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
-    const double* __restrict__ deconv, const double* __restrict__ decay, const double2* __restrict__ sub) {
+    const double* __restrict__ deconv, const double* __restrict__ decay, const double* __restrict__ dd,
+    const double2* __restrict__ sub, const double2* __restrict__ twQ, int Q) {
   constexpr int64_t P = (int64_t)M * M, n = 2 * P;
   constexpr int NR = 2 * M;
   extern __shared__ double2 sm[];
@@ -50,21 +47,22 @@ __global__ void __launch_bounds__(fast_threads<2 * M, C>(), 2) kc_band(
     const int m1 = (k2 + M / 2) & (NR - 1);  // (k2 + K/N1) mod 2M, K/N1 = M/2
     if (m1 < M) {
       const int64_t p = (int64_t)(r0 + c) + (int64_t)M * m1;
-      v = rscale(v, __ldg(&deconv[p]));
-      if (sub) v = csub(v, sub[bi * P + p]);
-      v = rscale(v, __ldg(&decay[p]));
+      if (sub) {  // type-4 residual: (X deconv - A) decay
+        v = rscale(v, __ldg(&deconv[p]));
+        v = csub(v, sub[bi * P + p]);
+        v = rscale(v, __ldg(&decay[p]));
+      } else {
+        v = rscale(v, __ldg(&dd[p]));  // deconv * decay
+      }
       sm[sidx<M, C, true>(m1, c)] = v;
     }
   };
   fast_tile_fft<NR, C, -1, true>(sm, ld1, st1, twR);
   __syncthreads();
   auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, C, true>(i, c)]; };
-  auto st2 = [&](int k1, int c, double2 v) {
-    const int m2 = r0 + c;
-    const double2 w = tw_pair(loP, hiP, sP, (int64_t)m2 * k1);
-    U[bi * P + (int64_t)k1 * M + m2] = cmulc(v, w);
-  };
-  fast_tile_fft_smem<M, C, +1, true>(sm, ld2, st2, twC);
+  auto st2 = [&](int k1, int c, double2 v) { U[bi * P + (int64_t)k1 * M + r0 + c] = v; };
+  const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, r0, -1};
+  fast_tile_fft_smem<M, C, +1, true>(sm, ld2, st2, twC, pt);
 }
 
 // K4 / K2': rows k1' of U (length M) -> row IFFT_P -> * ks[k1' + M k2'] ->
@@ -75,7 +73,8 @@ __global__ void __launch_bounds__(fast_threads<M, C>()) kc_mid(const double2* __
                                                               const double2* __restrict__ tw,
                                                               const double2* __restrict__ loP,
                                                               const double2* __restrict__ hiP, int sP,
-                                                              const double2* __restrict__ ks) {
+                                                              const double2* __restrict__ ks,
+                                                              const double2* __restrict__ twQ, int Q) {
   constexpr int64_t P = (int64_t)M * M;
   extern __shared__ double2 sm[];
   const int r0 = blockIdx.x * C;
@@ -89,12 +88,9 @@ __global__ void __launch_bounds__(fast_threads<M, C>()) kc_mid(const double2* __
   fast_tile_fft<M, C, +1, true>(sm, ld1, st1, tw);
   __syncthreads();
   auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, C, true>(i, c)]; };
-  auto st2 = [&](int k1, int c, double2 v) {
-    const int m2 = r0 + c;
-    const double2 w = tw_pair(loP, hiP, sP, (int64_t)m2 * k1);
-    Z[bi * P + (int64_t)k1 * M + m2] = cmul(v, w);
-  };
-  fast_tile_fft_smem<M, C, -1, true>(sm, ld2, st2, tw);
+  auto st2 = [&](int k1, int c, double2 v) { Z[bi * P + (int64_t)k1 * M + r0 + c] = v; };
+  const FourStepTw<-1> pt{loP, hiP, sP, twQ, Q, r0, -1};
+  fast_tile_fft_smem<M, C, -1, true>(sm, ld2, st2, tw, pt);
 }
 
 // K3' / K5+: rows k1'' of Z (length M) -> row FFT_P -> S_p * coef_p
@@ -106,8 +102,8 @@ template <int M, int C>
 __global__ void __launch_bounds__(fast_threads<2 * M, C>(), 2) kc_pad(
     const double2* __restrict__ Z, double2* __restrict__ Y, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
-    const double* __restrict__ coef, const double* __restrict__ deconv, const double2* __restrict__ xsub,
-    double2* __restrict__ xout) {
+    const double* __restrict__ coef, const double* __restrict__ deconv, const double* __restrict__ cd,
+    const double2* __restrict__ xsub, double2* __restrict__ xout, const double2* __restrict__ twQ, int Q) {
   constexpr int64_t P = (int64_t)M * M, n = 2 * P;
   constexpr int NC = 2 * M;
   extern __shared__ double2 sm[];
@@ -117,10 +113,14 @@ __global__ void __launch_bounds__(fast_threads<2 * M, C>(), 2) kc_pad(
   auto ld1 = [&](int i, int c) -> double2 { return Zin[(int64_t)(r0 + c) * M + i]; };
   auto st1 = [&](int k2, int c, double2 v) {
     const int64_t p = (int64_t)(r0 + c) + (int64_t)M * k2;
-    v = rscale(v, __ldg(&coef[p]));
-    if (xsub) v = csub(xsub[bi * P + p], v);
-    if (xout) xout[bi * P + p] = v;
-    v = rscale(v, __ldg(&deconv[p]));
+    if (xout) {  // refinement: x = (xsub -) S coef is stored, then deconvolved
+      v = rscale(v, __ldg(&coef[p]));
+      if (xsub) v = csub(xsub[bi * P + p], v);
+      xout[bi * P + p] = v;
+      v = rscale(v, __ldg(&deconv[p]));
+    } else {
+      v = rscale(v, __ldg(&cd[p]));  // coef * deconv
+    }
     const int n1 = (k2 - M / 2) & (NC - 1);
     sm[sidx<NC, C, true>(n1, c)] = v;
     sm[sidx<NC, C, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
@@ -128,12 +128,9 @@ __global__ void __launch_bounds__(fast_threads<2 * M, C>(), 2) kc_pad(
   fast_tile_fft<M, C, -1, true>(sm, ld1, st1, twR);
   __syncthreads();
   auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, C, true>(i, c)]; };
-  auto st2 = [&](int k1, int c, double2 v) {
-    const int n2 = r0 + c;
-    const double2 w = tw_pair(loN, hiN, sN, (int64_t)n2 * k1);
-    Y[bi * n + (int64_t)k1 * M + n2] = cmulc(v, w);
-  };
-  fast_tile_fft_smem<NC, C, +1, true>(sm, ld2, st2, twC);
+  auto st2 = [&](int k1, int c, double2 v) { Y[bi * n + (int64_t)k1 * M + r0 + c] = v; };
+  const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r0, -1};
+  fast_tile_fft_smem<NC, C, +1, true>(sm, ld2, st2, twC, pt);
 }
 
 // K5 / K4': rows of length L (row pass), output index k1 + R1 k2 with
@@ -165,7 +162,8 @@ __global__ void __launch_bounds__(fast_threads<L, C>()) kc_col(const double2* __
                                                               const double2* __restrict__ tw,
                                                               const double2* __restrict__ lo,
                                                               const double2* __restrict__ hi, int s,
-                                                              const double* __restrict__ pre) {
+                                                              const double* __restrict__ pre,
+                                                              const double2* __restrict__ twQ, int Q) {
   extern __shared__ double2 sm[];
   const int c0 = blockIdx.x * C;
   const int64_t base = (int64_t)blockIdx.y * N;
@@ -175,12 +173,9 @@ __global__ void __launch_bounds__(fast_threads<L, C>()) kc_col(const double2* __
     if (pre) v = rscale(v, __ldg(&pre[idx]));
     return v;
   };
-  auto st = [&](int k1, int c, double2 v) {
-    const int64_t n2 = c0 + c;
-    const double2 w = tw_pair(lo, hi, s, n2 * k1);
-    out[base + (int64_t)k1 * L2 + n2] = S < 0 ? cmul(v, w) : cmulc(v, w);
-  };
-  fast_tile_fft<L, C, S, true>(sm, ld, st, tw);
+  auto st = [&](int k1, int c, double2 v) { out[base + (int64_t)k1 * L2 + c0 + c] = v; };
+  const FourStepTw<S> pt{lo, hi, s, twQ, Q, c0, -1};
+  fast_tile_fft<L, C, S, true>(sm, ld, st, tw, pt);
 }
 
 // ------------------------------------------------------------ host side
@@ -198,6 +193,12 @@ struct ChainTabs {
   const double2 *twM, *tw2M;        // tile twiddles for lengths M and 2M
   const FftTables *tP, *tN;         // four-step twiddles for P and n = 2P
 };
+
+// W_Q table (Q = N / last-pass stride) for the four-step post twiddles
+static const double2* q_table(int64_t Q, cudaStream_t st, int* status) {
+  const FftTables* t = fft_tables(Q, st, status);
+  return t ? t->tw : nullptr;
+}
 
 static int chain_tables(int64_t M, ChainTabs* t, cudaStream_t st) {
   int status = NFFT45_OK;
@@ -228,19 +229,28 @@ struct Chain {
     constexpr size_t smem = fast_smem<L, CC>();
     NFFT_CHECK(chain_attr(chain_col, smem));
     constexpr int T = fast_threads<L, CC>();
+    const int64_t Q = N / last_stride<L>();
+    int status = NFFT45_OK;
+    const double2* twQ = q_table(Q, st, &status);
+    if (!twQ) return status;
     dim3 grid((unsigned)(L2 / CC), (unsigned)batch);
-    LAUNCH(chain_col, grid, T, smem, st, in, out, N, L2, tw, t4->lo, t4->hi, t4->s, pre);
+    LAUNCH(chain_col, grid, T, smem, st, in, out, N, L2, tw, t4->lo, t4->hi, t4->s, pre, twQ, (int)Q);
     return NFFT45_OK;
   }
 
   static int band(const double2* T_, double2* U, int64_t batch, const ChainTabs& t, const double* deconv,
-                  const double* decay, const double2* sub, cudaStream_t st) {
+                  const double* decay, const double* dd, const double2* sub, cudaStream_t st) {
     auto chain_band = kc_band<M, C>;
     constexpr size_t smem = fast_smem<2 * M, C>();
     NFFT_CHECK(chain_attr(chain_band, smem));
     constexpr int T = fast_threads<2 * M, C>();
+    const int64_t Q = P / last_stride<M>();
+    int status = NFFT45_OK;
+    const double2* twQ = q_table(Q, st, &status);
+    if (!twQ) return status;
     dim3 grid((unsigned)(M / C), (unsigned)batch);
-    LAUNCH(chain_band, grid, T, smem, st, T_, U, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s, deconv, decay, sub);
+    LAUNCH(chain_band, grid, T, smem, st, T_, U, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s, deconv, decay, dd, sub,
+           twQ, (int)Q);
     return NFFT45_OK;
   }
 
@@ -250,19 +260,28 @@ struct Chain {
     constexpr size_t smem = fast_smem<M, C>();
     NFFT_CHECK(chain_attr(chain_mid, smem));
     constexpr int T = fast_threads<M, C>();
+    const int64_t Q = P / last_stride<M>();
+    int status = NFFT45_OK;
+    const double2* twQ = q_table(Q, st, &status);
+    if (!twQ) return status;
     dim3 grid((unsigned)(M / C), (unsigned)batch);
-    LAUNCH(chain_mid, grid, T, smem, st, U, Z, t.twM, t.tP->lo, t.tP->hi, t.tP->s, ks);
+    LAUNCH(chain_mid, grid, T, smem, st, U, Z, t.twM, t.tP->lo, t.tP->hi, t.tP->s, ks, twQ, (int)Q);
     return NFFT45_OK;
   }
 
   static int pad(const double2* Z, double2* Y, int64_t batch, const ChainTabs& t, const double* coef,
-                 const double* deconv, const double2* xsub, double2* xout, cudaStream_t st) {
+                 const double* deconv, const double* cd, const double2* xsub, double2* xout, cudaStream_t st) {
     auto chain_pad = kc_pad<M, C>;
     constexpr size_t smem = fast_smem<2 * M, C>();
     NFFT_CHECK(chain_attr(chain_pad, smem));
     constexpr int T = fast_threads<2 * M, C>();
+    const int64_t Q = 2 * P / last_stride<2 * M>();
+    int status = NFFT45_OK;
+    const double2* twQ = q_table(Q, st, &status);
+    if (!twQ) return status;
     dim3 grid((unsigned)(M / C), (unsigned)batch);
-    LAUNCH(chain_pad, grid, T, smem, st, Z, Y, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s, coef, deconv, xsub, xout);
+    LAUNCH(chain_pad, grid, T, smem, st, Z, Y, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s, coef, deconv, cd, xsub,
+           xout, twQ, (int)Q);
     return NFFT45_OK;
   }
 
@@ -292,7 +311,7 @@ static int t5_front(const ChainPlanView& pv, const double2* s_or_r, int64_t batc
   Window win = Window::make(kFastM);
   NFFT_CHECK(spread(*pv.g, n, win, s_or_r, batch, f, b.H, st));
   NFFT_CHECK((Ch::template col<M, -1>(b.H, b.H, batch, n, 2 * M, t.twM, t.tN, nullptr, st)));
-  NFFT_CHECK(Ch::band(b.H, b.U, batch, t, pv.deconv, pv.decay, sub, st));
+  NFFT_CHECK(Ch::band(b.H, b.U, batch, t, pv.deconv, pv.decay, pv.dd, sub, st));
   NFFT_CHECK(Ch::mid(b.U, b.Z, batch, t, pv.ks, st));
   return NFFT45_OK;
 }
@@ -328,7 +347,7 @@ static int chain_solve(const ChainPlanView& pv, int kind, const double2* data, i
           NFFT_CHECK((Ch::template row<-1>(b.Z, out, batch, P, M, M, t.twM, pv.coef, xsub, st)));
         } else {
           // K5+: x (= S*coef or x - S*coef) stored, padded into IFFT_2P (type-2 of x)
-          NFFT_CHECK(Ch::pad(b.Z, Y, batch, t, pv.coef, pv.deconv, xsub, out, st));
+          NFFT_CHECK(Ch::pad(b.Z, Y, batch, t, pv.coef, pv.deconv, pv.cd, xsub, out, st));
           NFFT_CHECK((Ch::template row<+1>(Y, b.H, batch, n, 2 * M, 2 * M, t.twM, nullptr, nullptr, st)));
           NodeFactor ph{nullptr, (double)(P / 2), +1};
           NFFT_CHECK(gather(g, n, win, b.H, batch, ph, data, R, st));  // r = type2(x) - s
@@ -342,7 +361,7 @@ static int chain_solve(const ChainPlanView& pv, int kind, const double2* data, i
         if (from_cols)
           NFFT_CHECK((Ch::template col<M, +1>(A_or_r, b.U, batch, P, M, t.twM, t.tP, pv.decay, st)));
         NFFT_CHECK(Ch::mid(b.U, b.Z, batch, t, pv.ks, st));
-        NFFT_CHECK(Ch::pad(b.Z, Y, batch, t, pv.coef, pv.deconv, nullptr, nullptr, st));
+        NFFT_CHECK(Ch::pad(b.Z, Y, batch, t, pv.coef, pv.deconv, pv.cd, nullptr, nullptr, st));
         NFFT_CHECK((Ch::template row<+1>(Y, b.H, batch, n, 2 * M, 2 * M, t.twM, nullptr, nullptr, st)));
         NodeFactor fc4{pv.c4, 0.0, 0};
         return gather_mode(g, n, win, b.H, batch, fc4, xsub, xsub ? 2 : 0, dst, st);
@@ -353,7 +372,7 @@ static int chain_solve(const ChainPlanView& pv, int kind, const double2* data, i
         NodeFactor ph{nullptr, (double)(P / 2), -1};
         NFFT_CHECK(spread(g, n, win, out, batch, ph, b.H, st));
         NFFT_CHECK((Ch::template col<M, -1>(b.H, b.H, batch, n, 2 * M, t.twM, t.tN, nullptr, st)));
-        NFFT_CHECK(Ch::band(b.H, b.U, batch, t, pv.deconv, pv.decay, data, st));
+        NFFT_CHECK(Ch::band(b.H, b.U, batch, t, pv.deconv, pv.decay, pv.dd, data, st));
         NFFT_CHECK(back(nullptr, out, out, false));
       }
     }
@@ -374,6 +393,8 @@ bool chain_supported(int64_t P, int m) {
 
 int chain_run(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes, double2* out,
               double* norms, cudaStream_t st) {
+  static const bool no_bm = getenv("NFFT45_NO_BATCH_MINOR") != nullptr;  // A/B switch
+  if (batch >= 16 && !no_bm) return chain_run_bm(pv, kind, data, batch, passes, out, norms, st);
   switch (pv.P) {
     case 1024: return chain_solve<32>(pv, kind, data, batch, passes, out, norms, st);
     case 4096: return chain_solve<64>(pv, kind, data, batch, passes, out, norms, st);

@@ -1,0 +1,421 @@
+// chain_bm.cu — the fused FFT chains of chain.cu for BATCHES, on a
+// batch-minor internal layout X[index][signal] (signal stride 1, padded
+// batch Bp = multiple of 8).
+//
+// Every tile is one row (or column) of the four-step layout for 8 signals,
+// so (i) global loads/stores are contiguous 128-byte runs over signals,
+// (ii) the per-index tables (ks, deconv*decay, coef*deconv) and the
+// four-step twiddles are warp-uniform broadcasts instead of per-element
+// loads — the L1 data pipe, which limits the signal-major tiles, carries
+// little more than the data itself.  The user's signal-major operands are
+// converted in two boundary kernels with 2-D tiles (4 rows x 4 signals):
+// kbm_colin (type-4 input) and kbm_rowout (type-5 output); the gridding
+// kernels transpose through shared memory (gridding_b.cu).
+//
+// Stage semantics are those of chain.cu (inverse.py:101-143, forward.py:26-102).
+#include "fft_fast.cuh"
+#include "ops.cuh"
+
+namespace nfft45 {
+
+namespace {
+constexpr int kSig = 8;  // signals per tile (batch-minor kernels)
+
+__device__ __forceinline__ double2 rsc(double2 v, double s) { return make_double2(v.x * s, v.y * s); }
+}  // namespace
+
+// column pass: columns n2 = blockIdx.x of x[i * L2 + n2] (length L), optional
+// real pre-table, twiddle W_N^{S n2 k1}, in place-layout.
+template <int L, int S>
+__global__ void __launch_bounds__(fast_threads<L, kSig>(), 4) kbm_col(
+    const double2* __restrict__ in, double2* __restrict__ out, int L2, int64_t Bp, const double2* __restrict__ tw,
+    const double2* __restrict__ lo, const double2* __restrict__ hi, int sh, const double2* __restrict__ twQ, int Q,
+    const double* __restrict__ pre) {
+  extern __shared__ double2 sm[];
+  const int n2 = blockIdx.x;
+  const int64_t b0 = (int64_t)blockIdx.y * kSig;
+  auto ld = [&](int i, int c) -> double2 {
+    const int64_t idx = (int64_t)i * L2 + n2;
+    double2 v = in[idx * Bp + b0 + c];
+    if (pre) v = rsc(v, __ldg(&pre[idx]));
+    return v;
+  };
+  auto st = [&](int k1, int c, double2 v) { out[((int64_t)k1 * L2 + n2) * Bp + b0 + c] = v; };
+  const FourStepTw<S> pt{lo, hi, sh, twQ, Q, n2, 0};
+  fast_tile_fft<L, kSig, S, true>(sm, ld, st, tw, pt);
+}
+
+// row FFT_2P (row k1 = blockIdx.x, length 2M) -> band p = k1 + M m1 with
+// deconv*decay (or (X deconv - sub) decay) -> column IFFT_P (length M) ->
+// W_P^{+k1 k1'} -> U[(k1' M + k1)][b].
+template <int M>
+__global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 2) kbm_band(
+    const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
+    const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
+    const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
+    const double* __restrict__ dd, const double2* __restrict__ sub) {
+  constexpr int NR = 2 * M;
+  extern __shared__ double2 sm[];
+  const int k1 = blockIdx.x;
+  const int64_t b0 = (int64_t)blockIdx.y * kSig;
+  auto ld1 = [&](int i, int c) -> double2 { return T[((int64_t)k1 * NR + i) * Bp + b0 + c]; };
+  auto st1 = [&](int k2, int c, double2 v) {
+    const int m1 = (k2 + M / 2) & (NR - 1);
+    if (m1 < M) {
+      const int64_t p = (int64_t)k1 + (int64_t)M * m1;
+      if (sub) {
+        v = rsc(v, __ldg(&deconv[p]));
+        v = csub(v, sub[p * Bp + b0 + c]);
+        v = rsc(v, __ldg(&decay[p]));
+      } else {
+        v = rsc(v, __ldg(&dd[p]));
+      }
+      sm[sidx<M, kSig, true>(m1, c)] = v;
+    }
+  };
+  fast_tile_fft<NR, kSig, -1, true>(sm, ld1, st1, twR);
+  __syncthreads();
+  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, kSig, true>(i, c)]; };
+  auto st2 = [&](int k1p, int c, double2 v) { U[((int64_t)k1p * M + k1) * Bp + b0 + c] = v; };
+  const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, k1, 0};
+  fast_tile_fft_smem<M, kSig, +1, true>(sm, ld2, st2, twC, pt);
+}
+
+// row IFFT_P (row r) -> * ks -> column FFT_P (column r) -> W_P^{-r k} -> Z.
+template <int M>
+__global__ void __launch_bounds__(fast_threads<M, kSig>(), 4) kbm_mid(
+    const double2* __restrict__ U, double2* __restrict__ Z, int64_t Bp, const double2* __restrict__ tw,
+    const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
+    const double2* __restrict__ ks) {
+  extern __shared__ double2 sm[];
+  const int r = blockIdx.x;
+  const int64_t b0 = (int64_t)blockIdx.y * kSig;
+  auto ld1 = [&](int i, int c) -> double2 { return U[((int64_t)r * M + i) * Bp + b0 + c]; };
+  auto st1 = [&](int k2, int c, double2 v) {
+    sm[sidx<M, kSig, true>(k2, c)] = cmul(v, __ldg(&ks[(int64_t)r + (int64_t)M * k2]));
+  };
+  fast_tile_fft<M, kSig, +1, true>(sm, ld1, st1, tw);
+  __syncthreads();
+  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, kSig, true>(i, c)]; };
+  auto st2 = [&](int k, int c, double2 v) { Z[((int64_t)k * M + r) * Bp + b0 + c] = v; };
+  const FourStepTw<-1> pt{loP, hiP, sP, twQ, Q, r, 0};
+  fast_tile_fft_smem<M, kSig, -1, true>(sm, ld2, st2, tw, pt);
+}
+
+// row FFT_P (row r) -> * coef (x = [xsub -] S coef stored when xout) *
+// deconv -> zero-padded column IFFT_2P (length 2M, column r) -> W_n^{+r k} -> Y.
+template <int M>
+__global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 2) kbm_pad(
+    const double2* __restrict__ Z, double2* __restrict__ Y, int64_t Bp, const double2* __restrict__ twR,
+    const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
+    const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
+    const double* __restrict__ cd, const double2* __restrict__ xsub, double2* __restrict__ xout) {
+  constexpr int NC = 2 * M;
+  extern __shared__ double2 sm[];
+  const int r = blockIdx.x;
+  const int64_t b0 = (int64_t)blockIdx.y * kSig;
+  auto ld1 = [&](int i, int c) -> double2 { return Z[((int64_t)r * M + i) * Bp + b0 + c]; };
+  auto st1 = [&](int k2, int c, double2 v) {
+    const int64_t p = (int64_t)r + (int64_t)M * k2;
+    if (xout) {
+      v = rsc(v, __ldg(&coef[p]));
+      if (xsub) v = csub(xsub[p * Bp + b0 + c], v);
+      xout[p * Bp + b0 + c] = v;
+      v = rsc(v, __ldg(&deconv[p]));
+    } else {
+      v = rsc(v, __ldg(&cd[p]));
+    }
+    const int n1 = (k2 - M / 2) & (NC - 1);
+    sm[sidx<NC, kSig, true>(n1, c)] = v;
+    sm[sidx<NC, kSig, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
+  };
+  fast_tile_fft<M, kSig, -1, true>(sm, ld1, st1, twR);
+  __syncthreads();
+  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, kSig, true>(i, c)]; };
+  auto st2 = [&](int k, int c, double2 v) { Y[((int64_t)k * M + r) * Bp + b0 + c] = v; };
+  const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r, 0};
+  fast_tile_fft_smem<NC, kSig, +1, true>(sm, ld2, st2, twC, pt);
+}
+
+// row pass: row r = blockIdx.x (length L), output index r + R1 k.
+template <int L, int S>
+__global__ void __launch_bounds__(fast_threads<L, kSig>(), 4) kbm_row(const double2* __restrict__ in,
+                                                                  double2* __restrict__ out, int64_t Bp, int64_t R1,
+                                                                  const double2* __restrict__ tw) {
+  extern __shared__ double2 sm[];
+  const int r = blockIdx.x;
+  const int64_t b0 = (int64_t)blockIdx.y * kSig;
+  auto ld = [&](int i, int c) -> double2 { return in[((int64_t)r * L + i) * Bp + b0 + c]; };
+  auto st = [&](int k, int c, double2 v) { out[((int64_t)r + R1 * k) * Bp + b0 + c] = v; };
+  fast_tile_fft<L, kSig, S, true>(sm, ld, st, tw);
+}
+
+// Boundary, type-4 input: signal-major A[b][P] -> column IFFT_P * decay
+// (columns m2 = 4 blockIdx.x + (c & 3), signals b = 4 blockIdx.y + (c >> 2))
+// -> batch-minor U; optionally also a batch-minor copy AT of A.
+template <int M>
+__global__ void __launch_bounds__(fast_threads<M, 16>()) kbm_colin(
+    const double2* __restrict__ A, int64_t batch, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ tw,
+    const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
+    const double* __restrict__ decay, double2* __restrict__ AT) {
+  constexpr int64_t P = (int64_t)M * M;
+  extern __shared__ double2 sm[];
+  const int m20 = blockIdx.x * 4;
+  const int64_t bb = (int64_t)blockIdx.y * 4;
+  auto ld = [&](int i, int c) -> double2 {
+    const int64_t idx = (int64_t)i * M + m20 + (c & 3);
+    const int64_t b = bb + (c >> 2);
+    double2 v = b < batch ? A[b * P + idx] : make_double2(0.0, 0.0);
+    if (AT) AT[idx * Bp + b] = v;
+    return rsc(v, __ldg(&decay[idx]));
+  };
+  auto st = [&](int k1, int c, double2 v) {
+    U[((int64_t)k1 * M + m20 + (c & 3)) * Bp + bb + (c >> 2)] = v;
+  };
+  const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, m20, 3};
+  fast_tile_fft<M, 16, +1, true>(sm, ld, st, tw, pt);
+}
+
+// Boundary, type-5 output: batch-minor Z rows r = 4 blockIdx.x + (c & 3) ->
+// row FFT_P * coef [xsub (batch-minor) - .] -> signal-major out[b][P].
+template <int M>
+__global__ void __launch_bounds__(fast_threads<M, 16>()) kbm_rowout(
+    const double2* __restrict__ Z, double2* __restrict__ out, int64_t batch, int64_t Bp,
+    const double2* __restrict__ tw, const double* __restrict__ coef, const double2* __restrict__ xsub) {
+  constexpr int64_t P = (int64_t)M * M;
+  extern __shared__ double2 sm[];
+  const int r0 = blockIdx.x * 4;
+  const int64_t bb = (int64_t)blockIdx.y * 4;
+  auto ld = [&](int i, int c) -> double2 {
+    return Z[((int64_t)(r0 + (c & 3)) * M + i) * Bp + bb + (c >> 2)];
+  };
+  auto st = [&](int k, int c, double2 v) {
+    const int64_t p = (int64_t)(r0 + (c & 3)) + (int64_t)M * k;
+    const int64_t b = bb + (c >> 2);
+    v = rsc(v, __ldg(&coef[p]));
+    if (xsub) v = csub(xsub[p * Bp + b], v);
+    if (b < batch) out[b * P + p] = v;
+  };
+  fast_tile_fft<M, 16, -1, true>(sm, ld, st, tw);
+}
+
+// ------------------------------------------------------------ host side
+
+template <typename K>
+static int bm_attr(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) NFFT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return NFFT45_OK;
+}
+
+struct BmTabs {
+  const double2 *twM, *tw2M;
+  const FftTables *tP, *tN;
+};
+
+template <int M>
+struct ChainBM {
+  static constexpr int64_t P = (int64_t)M * M, n = 2 * P;
+  BmTabs t;
+  int64_t Bp, batch;
+  unsigned groups;  // Bp / 8
+  cudaStream_t st;
+
+  int qtab(int64_t Q, const double2** out) {
+    int status = NFFT45_OK;
+    const FftTables* tq = fft_tables(Q, st, &status);
+    if (!tq) return status;
+    *out = tq->tw;
+    return NFFT45_OK;
+  }
+
+  template <int L, int S>
+  int col(const double2* in, double2* out, int L2, int64_t N, const FftTables* t4, const double2* tw,
+          const double* pre) {
+    auto bm_col = kbm_col<L, S>;
+    constexpr size_t smem = fast_smem<L, kSig>();
+    NFFT_CHECK(bm_attr(bm_col, smem));
+    constexpr int T = fast_threads<L, kSig>();
+    const int64_t Q = N / last_stride<L>();
+    const double2* twQ = nullptr;
+    NFFT_CHECK(qtab(Q, &twQ));
+    LAUNCH(bm_col, dim3((unsigned)L2, groups), T, smem, st, in, out, L2, Bp, tw, t4->lo, t4->hi, t4->s, twQ, (int)Q,
+           pre);
+    return NFFT45_OK;
+  }
+
+  int band(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub) {
+    auto bm_band = kbm_band<M>;
+    constexpr size_t smem = fast_smem<2 * M, kSig>();
+    NFFT_CHECK(bm_attr(bm_band, smem));
+    constexpr int T = fast_threads<2 * M, kSig>();
+    const int64_t Q = P / last_stride<M>();
+    const double2* twQ = nullptr;
+    NFFT_CHECK(qtab(Q, &twQ));
+    LAUNCH(bm_band, dim3((unsigned)M, groups), T, smem, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s,
+           twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
+    return NFFT45_OK;
+  }
+
+  int mid(const double2* U, double2* Z, const ChainPlanView& pv) {
+    auto bm_mid = kbm_mid<M>;
+    constexpr size_t smem = fast_smem<M, kSig>();
+    NFFT_CHECK(bm_attr(bm_mid, smem));
+    constexpr int T = fast_threads<M, kSig>();
+    const int64_t Q = P / last_stride<M>();
+    const double2* twQ = nullptr;
+    NFFT_CHECK(qtab(Q, &twQ));
+    LAUNCH(bm_mid, dim3((unsigned)M, groups), T, smem, st, U, Z, Bp, t.twM, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q,
+           pv.ks);
+    return NFFT45_OK;
+  }
+
+  int pad(const double2* Z, double2* Y, const ChainPlanView& pv, const double2* xsub, double2* xout) {
+    auto bm_pad = kbm_pad<M>;
+    constexpr size_t smem = fast_smem<2 * M, kSig>();
+    NFFT_CHECK(bm_attr(bm_pad, smem));
+    constexpr int T = fast_threads<2 * M, kSig>();
+    const int64_t Q = n / last_stride<2 * M>();
+    const double2* twQ = nullptr;
+    NFFT_CHECK(qtab(Q, &twQ));
+    LAUNCH(bm_pad, dim3((unsigned)M, groups), T, smem, st, Z, Y, Bp, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s, twQ,
+           (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout);
+    return NFFT45_OK;
+  }
+
+  // IFFT_2P row pass: 2M rows of length M -> natural-order grid
+  int row_grid(const double2* Y, double2* H) {
+    auto bm_row = kbm_row<M, +1>;
+    constexpr size_t smem = fast_smem<M, kSig>();
+    NFFT_CHECK(bm_attr(bm_row, smem));
+    constexpr int T = fast_threads<M, kSig>();
+    LAUNCH(bm_row, dim3((unsigned)(2 * M), groups), T, smem, st, Y, H, Bp, (int64_t)(2 * M), t.twM);
+    return NFFT45_OK;
+  }
+
+  int colin(const double2* A, double2* U, const ChainPlanView& pv, double2* AT) {
+    auto bm_colin = kbm_colin<M>;
+    constexpr size_t smem = fast_smem<M, 16>();
+    NFFT_CHECK(bm_attr(bm_colin, smem));
+    constexpr int T = fast_threads<M, 16>();
+    const int64_t Q = P / last_stride<M>();
+    const double2* twQ = nullptr;
+    NFFT_CHECK(qtab(Q, &twQ));
+    LAUNCH(bm_colin, dim3((unsigned)(M / 4), (unsigned)(Bp / 4)), T, smem, st, A, batch, U, Bp, t.twM, t.tP->lo,
+           t.tP->hi, t.tP->s, twQ, (int)Q, pv.decay, AT);
+    return NFFT45_OK;
+  }
+
+  int rowout(const double2* Z, double2* out, const ChainPlanView& pv, const double2* xsub) {
+    auto bm_rowout = kbm_rowout<M>;
+    constexpr size_t smem = fast_smem<M, 16>();
+    NFFT_CHECK(bm_attr(bm_rowout, smem));
+    constexpr int T = fast_threads<M, 16>();
+    LAUNCH(bm_rowout, dim3((unsigned)(M / 4), (unsigned)(Bp / 4)), T, smem, st, Z, out, batch, Bp, t.twM, pv.coef,
+           xsub);
+    return NFFT45_OK;
+  }
+};
+
+template <int M>
+static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes,
+                          double2* out, double* norms, cudaStream_t st) {
+  using Ch = ChainBM<M>;
+  constexpr int64_t P = Ch::P, n = Ch::n;
+  Ch ch;
+  ch.st = st;
+  ch.batch = batch;
+  ch.Bp = ceil_div(batch, kSig) * kSig;
+  ch.groups = (unsigned)(ch.Bp / kSig);
+  int status = NFFT45_OK;
+  {
+    const FftTables* a = fft_tables(M, st, &status);
+    if (!a) return status;
+    const FftTables* b = fft_tables(2 * M, st, &status);
+    if (!b) return status;
+    ch.t.twM = a->tw;
+    ch.t.tw2M = b->tw;
+    ch.t.tP = fft_tables(P, st, &status);
+    if (!ch.t.tP) return status;
+    ch.t.tN = fft_tables(n, st, &status);
+    if (!ch.t.tN) return status;
+  }
+  const int64_t Bp = ch.Bp;
+  const GridDev& g = *pv.g;
+  Window win = Window::make(kFastM);
+  double2* base = nullptr;
+  // H [n], Y [n], U [P], Z [P], X [P] (refinement x), R [P] (residual / A transposed)
+  const size_t need = sizeof(double2) * Bp * (2 * n + 4 * P);
+  NFFT_CUDA(cudaMallocAsync(&base, need, st));
+  double2* H = base;
+  double2* Y = H + Bp * n;  // padded IFFT_2P column-pass output
+  double2* U = Y + Bp * n;
+  double2* Z = U + Bp * P;
+  double2* X = Z + Bp * P;
+  double2* R = X + Bp * P;
+  auto run = [&]() -> int {
+    if (kind == 5) {
+      NodeFactor fc5{pv.c5, 0.0, 0};
+      // r (or s) -> spread -> colFFT_2P -> band -> mid -> Z
+      auto front = [&](const double2* src, bool src_bm) -> int {
+        NFFT_CHECK(spread_layout(g, n, win, src, batch, src_bm ? Bp : 0, fc5, H, Bp, st));
+        NFFT_CHECK((ch.template col<M, -1>(H, H, 2 * M, n, ch.t.tN, ch.t.twM, nullptr)));
+        NFFT_CHECK(ch.band(H, U, pv, nullptr));
+        NFFT_CHECK(ch.mid(U, Z, pv));
+        return NFFT45_OK;
+      };
+      NFFT_CHECK(front(data, false));
+      for (int pass = 0; pass <= passes; pass++) {
+        if (pass == passes) {
+          NFFT_CHECK(ch.rowout(Z, out, pv, pass > 0 ? X : nullptr));
+        } else {
+          NFFT_CHECK(ch.pad(Z, Y, pv, pass > 0 ? X : nullptr, X));
+          NFFT_CHECK(ch.row_grid(Y, H));
+          NodeFactor ph{nullptr, (double)(P / 2), +1};
+          // r = type2(x) - s  (s signal-major, r batch-minor)
+          NFFT_CHECK(gather_layout(g, n, win, H, Bp, batch, ph, data, 0, 1, R, Bp, st));
+          if (norms) NFFT_CHECK(norms_bm(R, P, batch, Bp, norms + (int64_t)pass * batch, st));
+          NFFT_CHECK(front(R, true));
+        }
+      }
+    } else {
+      double2* AT = passes > 0 ? R : nullptr;
+      NFFT_CHECK(ch.colin(data, U, pv, AT));
+      auto back = [&](double2* dst, int64_t dst_ld, const double2* xsub, int64_t xsub_ld) -> int {
+        NFFT_CHECK(ch.mid(U, Z, pv));
+        NFFT_CHECK(ch.pad(Z, Y, pv, nullptr, nullptr));
+        NFFT_CHECK(ch.row_grid(Y, H));
+        NodeFactor fc4{pv.c4, 0.0, 0};
+        return gather_layout(g, n, win, H, Bp, batch, fc4, xsub, xsub_ld, xsub ? 2 : 0, dst, dst_ld, st);
+      };
+      if (passes == 0) return back(out, 0, nullptr, 0);
+      NFFT_CHECK(back(X, Bp, nullptr, 0));
+      for (int pass = 0; pass < passes; pass++) {
+        const bool last = pass == passes - 1;
+        NodeFactor ph{nullptr, (double)(P / 2), -1};
+        NFFT_CHECK(spread_layout(g, n, win, X, batch, Bp, ph, H, Bp, st));
+        NFFT_CHECK((ch.template col<M, -1>(H, H, 2 * M, n, ch.t.tN, ch.t.twM, nullptr)));
+        NFFT_CHECK(ch.band(H, U, pv, AT));
+        NFFT_CHECK(back(last ? out : X, last ? 0 : Bp, X, Bp));
+      }
+    }
+    return NFFT45_OK;
+  };
+  status = run();
+  cudaFreeAsync(base, st);
+  return status;
+}
+
+int chain_run_bm(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes, double2* out,
+                 double* norms, cudaStream_t st) {
+  switch (pv.P) {
+    case 1024: return chain_solve_bm<32>(pv, kind, data, batch, passes, out, norms, st);
+    case 4096: return chain_solve_bm<64>(pv, kind, data, batch, passes, out, norms, st);
+    case 16384: return chain_solve_bm<128>(pv, kind, data, batch, passes, out, norms, st);
+    case 65536: return chain_solve_bm<256>(pv, kind, data, batch, passes, out, norms, st);
+    case 262144: return chain_solve_bm<512>(pv, kind, data, batch, passes, out, norms, st);
+    case 1048576: return chain_solve_bm<1024>(pv, kind, data, batch, passes, out, norms, st);
+  }
+  return NFFT45_ERR_INVALID_ARGUMENT;
+}
+
+}  // namespace nfft45

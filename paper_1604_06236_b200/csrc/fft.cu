@@ -89,7 +89,7 @@ const FftTables* fft_tables(int64_t N, cudaStream_t st, int* status) {
     return NFFT45_OK;
   };
   int s = NFFT45_OK;
-  if (N <= kTileMax || !fft_smooth(N)) s = fill(&t->tw, N, 1);
+  if (N <= 65536 || !fft_smooth(N)) s = fill(&t->tw, N, 1);
   if (s == NFFT45_OK && N > 1 && fft_smooth(N)) {
     int bits = 0;
     while ((int64_t(1) << (2 * bits)) < N) bits++;

@@ -116,12 +116,68 @@ __device__ __forceinline__ int sidx(int i, int c) {
   return CF ? tpad(i * C + c) : tpad(c * N + i);
 }
 
+// No post-twiddle (default for fast_tile_fft).
+struct NoPostTw {
+  template <int R, int STRIDE>
+  __device__ __forceinline__ void apply(int, int, double2*) const {}
+};
+
+// Four-step inter-pass twiddle applied in the last pass: output index
+// k = j + r*STRIDE of column `col` is multiplied by W_N^{S col k} with
+//   W_N^{col j}           (two-level table lo/hi of N: 2 loads),
+//   W_N^{col STRIDE 2^i}  (= W_Q^{col 2^i}, Q = N/STRIDE, 4 exact loads),
+// and products for the other powers (<= 4 roundings) — 6 loads per
+// butterfly instead of 2 per output element.
+template <int S>
+struct FourStepTw {
+  const double2* lo;
+  const double2* hi;
+  int sh;
+  const double2* twQ;  // W_Q^k, k < Q
+  int Q;
+  int col0;
+  int cmask;  // tile column c maps to FFT column col0 + (c & cmask)
+  template <int R, int STRIDE>
+  __device__ __forceinline__ void apply(int c, int j, double2* v) const {
+    const int64_t col = col0 + (c & cmask);
+    const int64_t e = col * j;
+    double2 base = cmul(__ldg(&hi[e >> sh]), __ldg(&lo[e & ((int64_t(1) << sh) - 1)]));
+    double2 w[R];
+    w[0] = base;
+    if constexpr (R > 1) {
+      double2 p[R];
+      p[1] = __ldg(&twQ[col]);  // col * 8 < Q for every chain size (no reduction)
+      if constexpr (R >= 4) {
+        p[2] = __ldg(&twQ[2 * col]);
+        p[3] = cmul(p[1], p[2]);
+      }
+      if constexpr (R >= 8) {
+        p[4] = __ldg(&twQ[4 * col]);
+        p[5] = cmul(p[1], p[4]);
+        p[6] = cmul(p[2], p[4]);
+        p[7] = cmul(p[3], p[4]);
+      }
+      if constexpr (R >= 16) {
+        p[8] = __ldg(&twQ[8 * col]);
+#pragma unroll
+        for (int r = 1; r < 8; r++) p[8 + r] = cmul(p[r], p[8]);
+      }
+      if constexpr (R == 3) p[2] = __ldg(&twQ[2 * col]);
+#pragma unroll
+      for (int r = 1; r < R; r++) w[r] = cmul(base, p[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) v[r] = S < 0 ? cmul(v[r], w[r]) : cmulc(v[r], w[r]);
+  }
+};
+
 // One pass; FIRST reads through `ld`, LAST writes through `st`.  Threads
 // with threadIdx.x >= T (a CTA sized for a bigger FFT of a chain) idle but
 // still meet every barrier.  SYNC0: the first pass reads shared memory that
 // its own stores overwrite (chain kernels), so it needs a barrier too.
-template <int N, int C, int S, bool CF, bool SYNC0, int P, int Ns, class Ld, class St>
-__device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw) {
+template <int N, int C, int S, bool CF, bool SYNC0, int P, int Ns, class Ld, class St, class PT>
+__device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
+                                            const PT& pt) {
   using Tr = FastTraits<N>;
   constexpr int E = Tr::E;
   constexpr int R = Tr::radix(P);
@@ -163,6 +219,7 @@ __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St&
       for (int r = 1; r < R; r++) v[u][r] = S < 0 ? cmul(v[u][r], w[r]) : cmulc(v[u][r], w[r]);
     }
     bfly_fast<R, S>(v[u]);
+    if constexpr (LAST) pt.template apply<R, stride>(c, j, v[u]);  // outputs k = j + r*stride
     const int d = (j - k) * R + k;
 #pragma unroll
     for (int r = 0; r < R; r++) {
@@ -173,22 +230,27 @@ __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St&
   }
   if constexpr (!LAST) {
     __syncthreads();
-    fast_passes<N, C, S, CF, SYNC0, P + 1, Ns * R>(sm, ld, st, tw);
+    fast_passes<N, C, S, CF, SYNC0, P + 1, Ns * R>(sm, ld, st, tw, pt);
   }
 }
 
-template <int N, int C, int S, bool CF, class Ld, class St>
-__device__ __forceinline__ void fast_tile_fft(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw) {
-  fast_passes<N, C, S, CF, false, 0, 1>(sm, ld, st, tw);
+template <int N, int C, int S, bool CF, class Ld, class St, class PT = NoPostTw>
+__device__ __forceinline__ void fast_tile_fft(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
+                                              const PT& pt = PT()) {
+  fast_passes<N, C, S, CF, false, 0, 1>(sm, ld, st, tw, pt);
 }
 
 // Variant whose first pass reads the tile from shared memory (via `ld`)
 // that later passes overwrite.
-template <int N, int C, int S, bool CF, class Ld, class St>
+template <int N, int C, int S, bool CF, class Ld, class St, class PT = NoPostTw>
 __device__ __forceinline__ void fast_tile_fft_smem(double2* sm, const Ld& ld, const St& st,
-                                                   const double2* __restrict__ tw) {
-  fast_passes<N, C, S, CF, true, 0, 1>(sm, ld, st, tw);
+                                                   const double2* __restrict__ tw, const PT& pt = PT()) {
+  fast_passes<N, C, S, CF, true, 0, 1>(sm, ld, st, tw, pt);
 }
+
+// the last-pass stride (= N / radix of the last pass) of a fast tile FFT
+template <int N>
+constexpr int last_stride() { return N / FastTraits<N>::radix(FastTraits<N>::np - 1); }
 
 template <int N, int C>
 constexpr int fast_threads() { return N * C / FastTraits<N>::E; }

@@ -310,6 +310,56 @@ int gather(const GridDev& g, int64_t n, const Window& win, const double2* H, int
   return gather_mode(g, n, win, H, batch, f, sub, sub ? 1 : 0, out, st);
 }
 
+int spread_layout(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch, int64_t amp_ld,
+                  NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st) {
+  static const bool no_pipe = getenv("NFFT45_NO_PIPE") != nullptr;  // A/B switch
+  if (!no_pipe && win.m == kFastM && n >= 128 && H_ld && amp)
+    return spread_pipelined(g, n, win, amp, batch, amp_ld, f, H, H_ld, st);
+  if (win.m == kFastM && n >= 128 && (amp_ld || H_ld || batch >= 32))
+    return spread_batched(g, n, win, amp, batch, f, H, st, batch >= 64 ? 2 : 1, amp_ld, H_ld);
+  if (amp_ld || H_ld) {
+    set_error(NFFT45_ERR_INVALID_ARGUMENT, "batch-minor spreading needs m = 14 and n >= 128");
+    return NFFT45_ERR_INVALID_ARGUMENT;
+  }
+  return spread(g, n, win, amp, batch, f, H, st);
+}
+
+int gather_layout(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t H_ld, int64_t batch,
+                  NodeFactor f, const double2* sub, int64_t sub_ld, int mode, double2* out, int64_t out_ld,
+                  cudaStream_t st) {
+  if (!sub) mode = 0;
+  if (win.m == kFastM && n >= 128 && (H_ld || sub_ld || out_ld || batch >= 32))
+    return gather_batched(g, n, win, H, batch, f, sub, mode, out, st, H_ld, sub_ld, out_ld);
+  if (H_ld || sub_ld || out_ld) {
+    set_error(NFFT45_ERR_INVALID_ARGUMENT, "batch-minor interpolation needs m = 14 and n >= 128");
+    return NFFT45_ERR_INVALID_ARGUMENT;
+  }
+  return gather_mode(g, n, win, H, batch, f, sub, mode, out, st);
+}
+
+__global__ void k_norms_bm(const double2* __restrict__ r, int64_t len, int64_t ld, double* __restrict__ norms) {
+  __shared__ double part[256];
+  const int64_t b = blockIdx.x;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+    double2 v = r[i * ld + b];
+    s = fma(v.x, v.x, fma(v.y, v.y, s));
+  }
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) norms[b] = sqrt(part[0]);
+}
+
+int norms_bm(const double2* r, int64_t len, int64_t batch, int64_t ld, double* norms, cudaStream_t st) {
+  if (batch <= 0) return NFFT45_OK;
+  LAUNCH(k_norms_bm, (unsigned)batch, 256, 0, st, r, len, ld, norms);
+  return NFFT45_OK;
+}
+
 // ------------------------------------------------------- band kernels
 
 __global__ void k_band_fold(const double2* __restrict__ H, int64_t n, int64_t R, int64_t K, int64_t P,

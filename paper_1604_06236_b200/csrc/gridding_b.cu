@@ -8,6 +8,8 @@
 // (gather) in registers so one staged operand feeds 8 FMAs.  The
 // accumulation order is fixed (ascending nodes / ascending cells), so
 // results are bitwise reproducible and independent of the batch split.
+#include <algorithm>
+
 #include "ops.cuh"
 
 namespace nfft45 {
@@ -20,8 +22,8 @@ constexpr int kCPW = 8;          // spread: cells per warp
 constexpr int kSpreadWarps = 8;  // spread: warps per CTA -> 64 cells
 constexpr int kSpreadTile = kCPW * kSpreadWarps;
 constexpr int kSpreadCap = 72;   // nodes staged per batch
-constexpr int kNPW = 8;          // gather: nodes per warp
-constexpr int kGatherWarps = 4;  // gather: warps per CTA -> 32 nodes
+constexpr int kNPW = 4;          // gather: nodes per warp
+constexpr int kGatherWarps = 8;  // gather: warps per CTA -> 32 nodes
 constexpr int kGatherNodes = kNPW * kGatherWarps;
 constexpr int kGatherSpan = 112; // cells staged per chunk
 constexpr int kWTSpan = 64;      // per-warp weight-table cells per chunk
@@ -35,6 +37,9 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool va
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(n));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // 29 factorised Gaussian taps of one node (see gridding.cu gauss_fast).
 __device__ __forceinline__ void taps29(double f, double alpha, const GaussTab& G, double* w) {
@@ -82,7 +87,9 @@ __global__ void __launch_bounds__(256, 2) k_spread_b(const double* __restrict__ 
                                                     int64_t Q, int64_t n, double alpha, GaussTab G,
                                                     const double2* __restrict__ amp, int64_t batch, NodeFactor nf,
                                                     double2* __restrict__ H, const int2* __restrict__ ranges,
-                                                    int NS) {
+                                                    int NS, int64_t amp_ld, int64_t H_ld) {
+  // amp_ld == 0: amp is [batch][Q] (signal-major), else amp[q * amp_ld + b];
+  // H_ld == 0: H is [batch][n], else H[j * H_ld + b] (H_ld >= batch, padded)
   constexpr int SIG = 32 * SPL;
   extern __shared__ __align__(16) unsigned char smraw[];
   double2* A = reinterpret_cast<double2*>(smraw);                              // [cap][SIG] swizzled
@@ -136,11 +143,23 @@ __global__ void __launch_bounds__(256, 2) k_spread_b(const double* __restrict__ 
     __syncthreads();
     // phase 1: amplitudes, transposed to [node][signal] with async copies
     // (one signal row per warp pass: lanes read consecutive nodes)
-    for (int sig = warp; sig < SIG; sig += kSpreadWarps) {
-      const int64_t b = b0 + sig;
-      const bool ok = b < batch;
-      const double2* row = amp + (ok ? b : 0) * Q;
-      for (int e = lane; e < cnt; e += 32) cp_async16(&A[e * SIG + swz(sig, e)], row + Pi[e], ok);
+    if (amp_ld == 0) {
+      for (int sig = warp; sig < SIG; sig += kSpreadWarps) {
+        const int64_t b = b0 + sig;
+        const bool ok = b < batch;
+        const double2* row = amp + (ok ? b : 0) * Q;
+        for (int e = lane; e < cnt; e += 32) cp_async16(&A[e * SIG + swz(sig, e)], row + Pi[e], ok);
+      }
+    } else {
+      for (int e = warp; e < cnt; e += kSpreadWarps) {
+        const double2* row = amp + (int64_t)Pi[e] * amp_ld + b0;
+#pragma unroll
+        for (int s2 = 0; s2 < SPL; s2++) {
+          const int sig = lane + 32 * s2;
+          const bool ok = b0 + sig < batch;
+          cp_async16(&A[e * SIG + swz(sig, e)], row + (ok ? sig : 0), ok);
+        }
+      }
     }
     // phase 2 (overlaps the copies): geometry, padded weight rows, factors
     for (int e = tid; e < cnt; e += blockDim.x) {
@@ -190,6 +209,17 @@ __global__ void __launch_bounds__(256, 2) k_spread_b(const double* __restrict__ 
       }
     }
   }
+  if (H_ld != 0) {  // batch-minor grid: each cell row is contiguous over the lanes
+    const int ncell_w = (int)min((int64_t)kCPW, n - jw);
+#pragma unroll
+    for (int c = 0; c < kCPW; c++)
+#pragma unroll
+      for (int s2 = 0; s2 < SPL; s2++) {
+        const int64_t b = b0 + lane + 32 * s2;
+        if (c < ncell_w && b < H_ld) H[(int64_t)(jw + c) * H_ld + b] = acc[c][s2];
+      }
+    return;
+  }
   // write: stage [cell][signal] then coalesced rows per signal
   __syncthreads();
   double2* O = A;  // reuse (kSpreadCap * SIG >= kSpreadTile * SIG)
@@ -209,8 +239,250 @@ __global__ void __launch_bounds__(256, 2) k_spread_b(const double* __restrict__ 
   }
 }
 
+
+// Pipelined spreading onto a batch-minor grid H[j * H_ld + b]: one CTA per
+// 64-cell tile walks signal groups g = blockIdx.y, blockIdx.y + gridDim.y, ...
+// (64 signals each).  Node geometry and the padded weight rows are computed
+// once per tile; the amplitudes of group g+1 are fetched with cp.async into
+// the second buffer while the FMAs of group g run.  Tiles reached by more
+// than kPipeCap nodes (strongly clustered grids) fall back to batching nodes
+// per group (weights recomputed), same arithmetic order.
+constexpr int kPipeCap = 64;
+
+template <int SPL>
+__global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double* __restrict__ ts, const int* __restrict__ perm,
+                                                    int64_t Q, int64_t n, double alpha, GaussTab G,
+                                                    const double2* __restrict__ amp, int64_t batch, NodeFactor nf,
+                                                    double2* __restrict__ H, const int2* __restrict__ ranges, int NS,
+                                                    int64_t amp_ld, int64_t H_ld, int ngroups) {
+  constexpr int SIG = 32 * SPL;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double2* A0 = reinterpret_cast<double2*>(smraw);                        // [cap][SIG]
+  double2* A1 = A0 + kPipeCap * SIG;                                      // [cap][SIG]
+  double* W = reinterpret_cast<double*>(A1 + kPipeCap * SIG);             // [cap][kWRow]
+  double2* F = reinterpret_cast<double2*>(W + kPipeCap * kWRow);          // [cap]
+  int* Cc2 = reinterpret_cast<int*>(F + kPipeCap);                        // [cap]
+  int* Pi = Cc2 + kPipeCap;                                               // [cap]
+  int* Qs = Pi + kPipeCap;                                                // [cap]
+  int* Si = Qs + kPipeCap;                                                // [cap]
+  __shared__ int s_cnt[8];
+  __shared__ int s_off[8];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t j0 = (int64_t)blockIdx.x * kSpreadTile;
+  const int jw = (int)j0 + warp * kCPW;
+  const int64_t s_lo = floordiv_b(-kM - (min(j0 + kSpreadTile, n) - 1) + n - 1, n);
+  if (tid == 0) {
+    int acc = 0;
+    for (int si = 0; si < NS && si < 8; si++) {
+      int2 r = ranges[blockIdx.x * (int64_t)NS + si];
+      s_off[si] = acc;
+      s_cnt[si] = r.y - r.x;
+      acc += r.y - r.x;
+    }
+  }
+  __syncthreads();
+  int total = 0;
+  for (int si = 0; si < NS && si < 8; si++) total += s_cnt[si];
+  const bool pipelined = total <= kPipeCap;
+
+  // node list (first batch) -> Qs, Pi, Si
+  auto node_at = [&](int g, int& si) -> int64_t {
+    si = 0;
+    while (si + 1 < NS && si + 1 < 8 && g >= s_off[si + 1]) si++;
+    return ranges[blockIdx.x * (int64_t)NS + si].x + (g - s_off[si]);
+  };
+  // geometry + padded weight rows + factors of nodes [base, base+cnt)
+  auto prep_nodes = [&](int base, int cnt) {
+    for (int e = tid; e < cnt; e += blockDim.x) {
+      int si;
+      const int64_t q = node_at(base + e, si);
+      Qs[e] = (int)q;
+      Pi[e] = perm[q];
+      const double t = ts[q];
+      const NodeGeo geo = node_geo(t, (double)n);
+      const int ce = (int)((int64_t)geo.i0 - (s_lo + si) * n);
+      Cc2[e] = ce;
+      F[e] = factor_at(nf, q, t);
+      double w[2 * kM + 1];
+      taps29(geo.f, alpha, G, w);
+      double* row = W + e * kWRow;
+      if ((ce + 1) & 1) {
+#pragma unroll
+        for (int x = 0; x < kWRow; x++) {
+          const int k = x - 1 - kM - 7;
+          row[x] = (k >= -kM && k <= kM) ? w[(k >= -kM && k <= kM) ? k + kM : 0] : 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int x = 0; x < kWRow; x++) {
+          const int k = x - kM - 7;
+          row[x] = (k >= -kM && k <= kM) ? w[(k >= -kM && k <= kM) ? k + kM : 0] : 0.0;
+        }
+      }
+    }
+  };
+  // async staging of the amplitudes of group g for staged nodes [0, cnt)
+  auto stage = [&](double2* A, int64_t g, int cnt) {
+    const int64_t b0 = g * SIG;
+    if (amp_ld == 0) {
+      for (int sig = warp; sig < SIG; sig += kSpreadWarps) {
+        const int64_t b = b0 + sig;
+        const bool ok = b < batch;
+        const double2* row = amp + (ok ? b : 0) * Q;
+        for (int e = lane; e < cnt; e += 32) cp_async16(&A[e * SIG + swz(sig, e)], row + Pi[e], ok);
+      }
+    } else {
+      for (int e = warp; e < cnt; e += kSpreadWarps) {
+        const double2* row = amp + (int64_t)Pi[e] * amp_ld + b0;
+#pragma unroll
+        for (int s2 = 0; s2 < SPL; s2++) {
+          const int sig = lane + 32 * s2;
+          const bool ok = b0 + sig < batch;
+          cp_async16(&A[e * SIG + swz(sig, e)], row + (ok ? sig : 0), ok);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  // this warp's active nodes (window meets its 8 cells), compacted once per
+  // staged node set so the FMA loop is branch-free and software-pipelined
+  __shared__ int s_act[kSpreadWarps][kPipeCap];
+  __shared__ int s_nact[kSpreadWarps];
+  auto compact = [&](int cnt) {
+    int na = 0;
+    for (int e0 = 0; e0 < cnt; e0 += 32) {
+      const int e = e0 + lane;
+      bool act = false;
+      if (e < cnt) {
+        const int o = jw - Cc2[e];
+        act = (o >= -kM - 7 && o <= kM);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, act);
+      if (act) s_act[warp][na + __popc(m & ((1u << lane) - 1u))] = e;
+      na += __popc(m);
+    }
+    if (lane == 0) s_nact[warp] = na;
+    __syncwarp();
+  };
+  struct Op {
+    double2 w01, w23, w45, w67, fe, a[SPL];
+  };
+  auto fetch = [&](const double2* A, int e, Op& op) {
+    const int ce = Cc2[e];
+    const int x = jw - ce + kM + 7 + ((ce + 1) & 1);
+    const double2* wr = reinterpret_cast<const double2*>(W + e * kWRow + x);
+    op.w01 = wr[0];
+    op.w23 = wr[1];
+    op.w45 = wr[2];
+    op.w67 = wr[3];
+    op.fe = F[e];
+#pragma unroll
+    for (int s2 = 0; s2 < SPL; s2++) op.a[s2] = A[e * SIG + swz(lane + 32 * s2, e)];
+  };
+  auto fma_node = [&](const Op& op, double2 (&acc)[kCPW][SPL]) {
+    const double wc[8] = {op.w01.x, op.w01.y, op.w23.x, op.w23.y, op.w45.x, op.w45.y, op.w67.x, op.w67.y};
+#pragma unroll
+    for (int s2 = 0; s2 < SPL; s2++) {
+      const double2 a = cmul(op.a[s2], op.fe);
+#pragma unroll
+      for (int c = 0; c < kCPW; c++) caxpy(acc[c][s2], wc[c], a);
+    }
+  };
+  auto accumulate = [&](const double2* A, int /*cnt*/, double2 (&acc)[kCPW][SPL]) {
+    const int na = s_nact[warp];
+    if (na == 0) return;
+    Op cur, nxt;
+    fetch(A, s_act[warp][0], cur);
+    for (int k = 0; k < na; k++) {
+      if (k + 1 < na) fetch(A, s_act[warp][k + 1], nxt);
+      fma_node(cur, acc);
+      cur = nxt;
+    }
+  };
+  auto store = [&](int64_t g, double2 (&acc)[kCPW][SPL]) {
+    const int ncell_w = (int)min((int64_t)kCPW, n - jw);
+#pragma unroll
+    for (int c = 0; c < kCPW; c++)
+#pragma unroll
+      for (int s2 = 0; s2 < SPL; s2++) {
+        const int64_t b = g * SIG + lane + 32 * s2;
+        if (c < ncell_w && b < H_ld) H[(int64_t)(jw + c) * H_ld + b] = acc[c][s2];
+      }
+  };
+
+  if (pipelined) {
+    prep_nodes(0, total);
+    __syncthreads();
+    compact(total);
+    int64_t g = blockIdx.y;
+    if (g < ngroups) stage(A0, g, total);
+    for (int it = 0; g < ngroups; it++, g += gridDim.y) {
+      double2* cur = (it & 1) ? A1 : A0;
+      double2* nxt = (it & 1) ? A0 : A1;
+      if (g + gridDim.y < ngroups) {
+        stage(nxt, g + gridDim.y, total);
+        cp_async_wait_group<1>();
+      } else {
+        cp_async_wait_group<0>();
+      }
+      __syncthreads();
+      double2 acc[kCPW][SPL];
+#pragma unroll
+      for (int c = 0; c < kCPW; c++)
+#pragma unroll
+        for (int s2 = 0; s2 < SPL; s2++) acc[c][s2] = make_double2(0.0, 0.0);
+      accumulate(cur, total, acc);
+      store(g, acc);
+      __syncthreads();  // `cur` is refilled two iterations later
+    }
+  } else {
+    for (int64_t g = blockIdx.y; g < ngroups; g += gridDim.y) {
+      double2 acc[kCPW][SPL];
+#pragma unroll
+      for (int c = 0; c < kCPW; c++)
+#pragma unroll
+        for (int s2 = 0; s2 < SPL; s2++) acc[c][s2] = make_double2(0.0, 0.0);
+      for (int base = 0; base < total; base += kPipeCap) {
+        const int cnt = min(kPipeCap, total - base);
+        __syncthreads();
+        prep_nodes(base, cnt);
+        __syncthreads();
+        compact(cnt);
+        stage(A0, g, cnt);
+        cp_async_wait_group<0>();
+        __syncthreads();
+        accumulate(A0, cnt, acc);
+      }
+      store(g, acc);
+    }
+  }
+}
+
+int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch,
+                     int64_t amp_ld, NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st) {
+  const int64_t ntiles = ceil_div(n, kSpreadTile);
+  const int NS = (int)((2 * win.m + kSpreadTile - 1) / n + 3);
+  if (NS > 8) return NFFT45_ERR_INVALID_ARGUMENT;
+  int2* ranges = nullptr;
+  NFFT_CUDA(cudaMallocAsync(&ranges, sizeof(int2) * ntiles * NS, st));
+  LAUNCH(k_tile_ranges, (unsigned)ceil_div(ntiles * NS, 128), 128, 0, st, g.ts, g.Q, n, win.m, kSpreadTile, ntiles,
+         NS, ranges);
+  constexpr int SIG = 32;
+  const int ngroups = (int)ceil_div(H_ld, SIG);
+  // enough CTAs for ~2 waves of 148 SMs, each walking several signal groups
+  int slices = (int)std::min<int64_t>(ngroups, std::max<int64_t>(1, ceil_div(4 * 148, ntiles)));
+  size_t smem = (size_t)2 * kPipeCap * SIG * 16 + (size_t)kPipeCap * kWRow * 8 + kPipeCap * 16 + kPipeCap * 16;
+  auto spread_p = k_spread_p<1>;
+  NFFT_CUDA(cudaFuncSetAttribute(spread_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  LAUNCH(spread_p, dim3((unsigned)ntiles, (unsigned)slices), 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha,
+         gauss_tab(win), amp, batch, f, H, ranges, NS, amp_ld, H_ld, ngroups);
+  NFFT_CUDA(cudaFreeAsync(ranges, st));
+  return NFFT45_OK;
+}
+
 int spread_batched(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch, NodeFactor f,
-                   double2* H, cudaStream_t st, int spl) {
+                   double2* H, cudaStream_t st, int spl, int64_t amp_ld, int64_t H_ld) {
   const int64_t ntiles = ceil_div(n, kSpreadTile);
   const int NS = (int)((2 * win.m + kSpreadTile - 1) / n + 3);
   if (NS > 8) return NFFT45_ERR_INVALID_ARGUMENT;  // tiny grids use the generic kernel
@@ -225,14 +497,16 @@ int spread_batched(const GridDev& g, int64_t n, const Window& win, const double2
     auto spread_b = k_spread_b<2>;
     NFFT_CUDA(cudaFuncSetAttribute(spread_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid((unsigned)ntiles, (unsigned)ceil_div(batch, SIG));
-    LAUNCH(spread_b, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, amp, batch, f, H, ranges, NS);
+    LAUNCH(spread_b, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, amp, batch, f, H, ranges, NS, amp_ld,
+           H_ld);
   } else {
     constexpr int SIG = 32;
     size_t smem = (size_t)kSpreadCap * SIG * 16 + (size_t)kSpreadCap * kWRow * 8 + kSpreadCap * 16 + kSpreadCap * 16;
     auto spread_b = k_spread_b<1>;
     NFFT_CUDA(cudaFuncSetAttribute(spread_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid((unsigned)ntiles, (unsigned)ceil_div(batch, SIG));
-    LAUNCH(spread_b, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, amp, batch, f, H, ranges, NS);
+    LAUNCH(spread_b, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, amp, batch, f, H, ranges, NS, amp_ld,
+           H_ld);
   }
   NFFT_CUDA(cudaFreeAsync(ranges, st));
   return NFFT45_OK;
@@ -245,15 +519,18 @@ int spread_batched(const GridDev& g, int64_t n, const Window& win, const double2
 // [cell][signal] in chunks of kGatherSpan; each warp builds a dense weight
 // table WT[cell][8 nodes] for its own cells (zeros outside windows) so one
 // staged cell value feeds 8 FMAs with one 64-byte broadcast of weights.
-__global__ void __launch_bounds__(128, 3) k_gather_b(const double* __restrict__ ts, const int* __restrict__ perm,
+__global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_b(const double* __restrict__ ts, const int* __restrict__ perm,
                                                     int64_t Q, int64_t n, double alpha, GaussTab G,
                                                     const double2* __restrict__ H, int64_t batch, NodeFactor nf,
                                                     const double2* __restrict__ sub, int mode,
-                                                    double2* __restrict__ out) {
+                                                    double2* __restrict__ out, int64_t H_ld, int64_t sub_ld,
+                                                    int64_t out_ld) {
+  // *_ld == 0: signal-major operand ([batch][len]); else batch-minor x[i * ld + b]
   constexpr int SIG = 32;
   extern __shared__ __align__(16) unsigned char smraw[];
   double2* Y = reinterpret_cast<double2*>(smraw);                                // [span][SIG]
   double* WT = reinterpret_cast<double*>(Y + kGatherSpan * SIG);                 // [warps][kWTSpan][8]
+  double2* Sb = reinterpret_cast<double2*>(WT + kGatherWarps * kWTSpan * kNPW);  // [nodes][SIG] subtrahend
   __shared__ int s_c0[kGatherNodes];
   __shared__ double s_f[kGatherNodes];
   __shared__ double2 s_fac[kGatherNodes];
@@ -282,6 +559,21 @@ __global__ void __launch_bounds__(128, 3) k_gather_b(const double* __restrict__ 
     s_f[tid] = f;
   }
   __syncthreads();
+  // subtrahend tile, read in the order that is coalesced for its layout
+  if (mode != 0) {
+    if (sub_ld == 0) {
+      for (int sig = warp; sig < SIG; sig += kGatherWarps) {
+        const int64_t b = b0 + sig;
+        const bool ok = b < batch;
+        if (lane < nq) cp_async16(&Sb[lane * SIG + swz(sig, lane)], sub + (ok ? b : 0) * Q + s_pq[lane], ok);
+      }
+    } else {
+      for (int e = warp; e < nq; e += kGatherWarps) {
+        const bool ok = b0 + lane < batch;
+        cp_async16(&Sb[e * SIG + swz(lane, e)], sub + (int64_t)s_pq[e] * sub_ld + b0 + (ok ? lane : 0), ok);
+      }
+    }
+  }
   // unwrapped cell span of the CTA and of this warp (centres ascend)
   const int cta_lo = s_c0[0] - kM, cta_hi = s_c0[kGatherNodes - 1] + kM;
   const int w_lo = s_c0[warp * kNPW] - kM, w_hi = s_c0[warp * kNPW + kNPW - 1] + kM;
@@ -296,20 +588,26 @@ __global__ void __launch_bounds__(128, 3) k_gather_b(const double* __restrict__ 
     const int len = ce - cs + 1;
     __syncthreads();  // previous chunk fully consumed
     // stage cells [cs, ce] (mod n) for the CTA's signals
-    for (int sig = warp; sig < SIG; sig += kGatherWarps) {
-      const int64_t b = b0 + sig;
-      const bool ok = b < batch;
-      const double2* row = H + (ok ? b : 0) * n;
-      for (int c = lane; c < len; c += 32) {
-        int64_t cell = (int64_t)(cs + c);
+    auto wrap = [&](int64_t cell) -> int64_t {
+      if (cell < 0) cell += n;
+      if (cell >= n) cell -= n;
+      if (cell < 0 || cell >= n) {  // tiny grids: full reduction
+        cell %= n;
         if (cell < 0) cell += n;
-        if (cell >= n) cell -= n;
-        if (cell < 0 || cell >= n) {  // tiny grids: full reduction
-          cell %= n;
-          if (cell < 0) cell += n;
-        }
-        cp_async16(&Y[c * SIG + swz(sig, c)], row + cell, ok);
       }
+      return cell;
+    };
+    if (H_ld == 0) {
+      for (int sig = warp; sig < SIG; sig += kGatherWarps) {
+        const int64_t b = b0 + sig;
+        const bool ok = b < batch;
+        const double2* row = H + (ok ? b : 0) * n;
+        for (int c = lane; c < len; c += 32) cp_async16(&Y[c * SIG + swz(sig, c)], row + wrap(cs + c), ok);
+      }
+    } else {
+      const bool ok = b0 + lane < batch;
+      for (int c = warp; c < len; c += kGatherWarps)
+        cp_async16(&Y[c * SIG + swz(lane, c)], H + wrap(cs + c) * H_ld + b0 + (ok ? lane : 0), ok);
     }
     // this warp's cells inside the chunk, in sub-chunks of kWTSpan (warp-private
     // table); the first table is built while the copies are in flight
@@ -340,19 +638,16 @@ __global__ void __launch_bounds__(128, 3) k_gather_b(const double* __restrict__ 
       for (int c = ws; c <= we; c++) {
         const double2 y = Y[(c - cs) * SIG + swz(lane, c - cs)];
         const double2* wr = reinterpret_cast<const double2*>(wt + (c - ws) * kNPW);
-        const double2 w01 = wr[0], w23 = wr[1], w45 = wr[2], w67 = wr[3];
-        caxpy(acc[0], w01.x, y);
-        caxpy(acc[1], w01.y, y);
-        caxpy(acc[2], w23.x, y);
-        caxpy(acc[3], w23.y, y);
-        caxpy(acc[4], w45.x, y);
-        caxpy(acc[5], w45.y, y);
-        caxpy(acc[6], w67.x, y);
-        caxpy(acc[7], w67.y, y);
+#pragma unroll
+        for (int i2 = 0; i2 < kNPW / 2; i2++) {
+          const double2 w = wr[i2];
+          caxpy(acc[2 * i2], w.x, y);
+          caxpy(acc[2 * i2 + 1], w.y, y);
+        }
       }
     }
   }
-  // epilogue: factor, optional subtraction, transposed coalesced store
+  // epilogue: factor, optional subtraction, store in the output's coalesced order
   __syncthreads();
   double2* O = Y;  // [node][SIG]
 #pragma unroll
@@ -361,27 +656,38 @@ __global__ void __launch_bounds__(128, 3) k_gather_b(const double* __restrict__ 
     O[e * SIG + swz(lane, e)] = acc[i];
   }
   __syncthreads();
-  for (int idx = tid; idx < kGatherNodes * SIG; idx += blockDim.x) {
-    const int e = idx & (kGatherNodes - 1), sig = idx / kGatherNodes;
-    const int64_t b = b0 + sig;
-    if (b >= batch || e >= nq) continue;
-    const double2 fq = s_fac[e];
-    double2 v = cmul(O[e * SIG + swz(sig, e)], fq);
-    const int64_t pq = s_pq[e];
-    if (mode == 1) v = csub(v, sub[b * Q + pq]);
-    else if (mode == 2) v = csub(sub[b * Q + pq], v);
-    out[b * Q + pq] = v;
+  auto value = [&](int e, int sig) -> double2 {
+    double2 v = cmul(O[e * SIG + swz(sig, e)], s_fac[e]);
+    if (mode == 1) v = csub(v, Sb[e * SIG + swz(sig, e)]);
+    else if (mode == 2) v = csub(Sb[e * SIG + swz(sig, e)], v);
+    return v;
+  };
+  if (out_ld == 0) {
+    for (int idx = tid; idx < kGatherNodes * SIG; idx += blockDim.x) {
+      const int e = idx & (kGatherNodes - 1), sig = idx / kGatherNodes;
+      const int64_t b = b0 + sig;
+      if (b >= batch || e >= nq) continue;
+      out[b * Q + s_pq[e]] = value(e, sig);
+    }
+  } else {
+    for (int e = warp; e < nq; e += kGatherWarps) {
+      const int64_t b = b0 + lane;
+      if (b < out_ld) out[(int64_t)s_pq[e] * out_ld + b] = b < batch ? value(e, lane) : make_double2(0.0, 0.0);
+    }
   }
 }
 
 int gather_batched(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch, NodeFactor f,
-                   const double2* sub, int mode, double2* out, cudaStream_t st) {
-  size_t smem = (size_t)kGatherSpan * 32 * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8;
+                   const double2* sub, int mode, double2* out, cudaStream_t st, int64_t H_ld, int64_t sub_ld,
+                   int64_t out_ld) {
+  if (!sub) mode = 0;
+  size_t smem = (size_t)kGatherSpan * 32 * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8 +
+                (mode ? (size_t)kGatherNodes * 32 * 16 : 0);
   auto gather_b = k_gather_b;
   NFFT_CUDA(cudaFuncSetAttribute(gather_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)ceil_div(g.Q, kGatherNodes), (unsigned)ceil_div(batch, 32));
+  dim3 grid((unsigned)ceil_div(g.Q, kGatherNodes), (unsigned)ceil_div(out_ld ? out_ld : batch, 32));
   LAUNCH(gather_b, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), H, batch, f, sub,
-         mode, out);
+         mode, out, H_ld, sub_ld, out_ld);
   return NFFT45_OK;
 }
 

@@ -125,6 +125,7 @@ struct nfft45_plan {
   double2 *c5, *c4;  // ascending-node fused factors nw * cis(-/+ K t)
   double* rtab;      // real copies: decay, coef_scale, deconvolution (length P each)
   double *rdecay, *rcoef, *rdeconv;
+  double *rdd, *rcd;  // deconv*decay, coef*deconv
 };
 
 // ------------------------------------------------------------- kernels
@@ -233,12 +234,15 @@ __global__ void k_plan_tables(const double* __restrict__ t, const double* __rest
 // real solve tables for the fused chains
 __global__ void k_real_tables(const double2* __restrict__ decay, const double2* __restrict__ coef, int64_t P,
                               double b, double* __restrict__ rdecay, double* __restrict__ rcoef,
-                              double* __restrict__ rdeconv) {
+                              double* __restrict__ rdeconv, double* __restrict__ rdd, double* __restrict__ rcd) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= P) return;
-  rdecay[p] = decay[p].x;
-  rcoef[p] = coef[p].x;
-  rdeconv[p] = deconv_weight(p, P / 2, 2 * P, b);
+  const double dec = decay[p].x, cf = coef[p].x, dc = deconv_weight(p, P / 2, 2 * P, b);
+  rdecay[p] = dec;
+  rcoef[p] = cf;
+  rdeconv[p] = dc;
+  rdd[p] = dc * dec;
+  rcd[p] = cf * dc;
 }
 
 __global__ void k_fused_factors(const double* __restrict__ ts, const int* __restrict__ perm,
@@ -381,6 +385,8 @@ static ChainPlanView chain_view(const nfft45_plan* p) {
   v.decay = p->rdecay;
   v.coef = p->rcoef;
   v.deconv = p->rdeconv;
+  v.dd = p->rdd;
+  v.cd = p->rcd;
   return v;
 }
 
@@ -749,7 +755,7 @@ int nfft45_plan_create(const nfft45_grid* g, double a, int eta, int m, void* st,
   p->a = a;
   p->eta = eta;
   p->m = m;
-  cudaError_t e = cudaMalloc(&p->tables, sizeof(double2) * 9 * P + sizeof(double) * 3 * P);
+  cudaError_t e = cudaMalloc(&p->tables, sizeof(double2) * 9 * P + sizeof(double) * 5 * P);
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "cudaMalloc(plan)");
@@ -758,6 +764,8 @@ int nfft45_plan_create(const nfft45_grid* g, double a, int eta, int m, void* st,
   p->rdecay = p->rtab;
   p->rcoef = p->rtab + P;
   p->rdeconv = p->rtab + 2 * P;
+  p->rdd = p->rtab + 3 * P;
+  p->rcd = p->rtab + 4 * P;
   double2* t = p->tables;
   p->v = t;
   p->ks = t + P;
@@ -784,7 +792,7 @@ int nfft45_plan_create(const nfft45_grid* g, double a, int eta, int m, void* st,
                                                                 p->c5, p->c4);
       g_launches++;
       k_real_tables<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(p->decay, p->coef, P, Window::make(m).b, p->rdecay,
-                                                              p->rcoef, p->rdeconv);
+                                                              p->rcoef, p->rdeconv, p->rdd, p->rcd);
       g_launches++;
       cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) status = cuda_fail(le, "plan tables");

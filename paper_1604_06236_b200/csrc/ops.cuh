@@ -51,6 +51,7 @@ struct ChainPlanView {
   int64_t P;
   const double2 *ks, *c5, *c4;         // complex tables (c5/c4 in ascending-node order)
   const double *decay, *coef, *deconv;  // real tables of length P
+  const double *dd, *cd;                // deconv*decay, coef*deconv
 };
 bool chain_supported(int64_t P, int m);
 // kind 5: type-5 (+ passes refinements); kind 4: type-4.  norms (may be
@@ -88,9 +89,21 @@ __global__ void k_tile_ranges(const double* __restrict__ ts, int64_t Q, int64_t 
 // Batched m = 14 kernels (gridding_b.cu): lanes over signals.  spl = signals
 // per lane (1 or 2) for the spread.
 int spread_batched(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch, NodeFactor f,
-                   double2* H, cudaStream_t st, int spl);
+                   double2* H, cudaStream_t st, int spl, int64_t amp_ld = 0, int64_t H_ld = 0);
 int gather_batched(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch, NodeFactor f,
-                   const double2* sub, int mode, double2* out, cudaStream_t st);
+                   const double2* sub, int mode, double2* out, cudaStream_t st, int64_t H_ld = 0, int64_t sub_ld = 0,
+                   int64_t out_ld = 0);
+int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch,
+                     int64_t amp_ld, NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st);
+// Layout-aware wrappers for the batch-minor chains (ld == 0: signal-major).
+int spread_layout(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch, int64_t amp_ld,
+                  NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st);
+int gather_layout(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t H_ld, int64_t batch,
+                  NodeFactor f, const double2* sub, int64_t sub_ld, int mode, double2* out, int64_t out_ld,
+                  cudaStream_t st);
+int norms_bm(const double2* r, int64_t len, int64_t batch, int64_t ld, double* norms, cudaStream_t st);
+int chain_run_bm(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes, double2* out,
+                 double* norms, cudaStream_t st);
 
 // Device deconvolution weight 1/(n Psi(nu)) of gridding.py:90.
 __device__ __forceinline__ double deconv_weight(int64_t p, int64_t K, int64_t n, double b) {

@@ -1,0 +1,96 @@
+"""Summarise a round's profiling artefacts into profiles/ (run here, no GPU).
+
+usage: python scripts/profile_summary.py <launches.csv> <full.ncu-rep> <tag> <steps-in-launch-list>
+Writes profiles/<tag>_launches.md (per-kernel share of device time from the
+ncu launch list) and profiles/<tag>_kernels.md + profiles/traffic_c4.json
+(DRAM bytes per launch from the --set full capture, used by bench.py as
+roofline.traffic)."""
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hi]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = collections.OrderedDict()
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "").strip()
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += float(r[vi].replace(",", ""))
+    return agg
+
+
+def full(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h = rows[0]
+    res = []
+    for r in rows[2:]:
+        d = dict(zip(h, r))
+        g = lambda k: float(d[k].replace(",", "")) if k in d and d[k] not in ("", "n/a") else None
+        res.append({
+            "kernel": d["Kernel Name"].split("(")[0].replace("void ", "").strip(),
+            "grid": d.get("Grid Size"), "block": d.get("Block Size"),
+            "time_ms": g("gpu__time_duration.sum"),
+            "dram_read_GB": (g("dram__bytes_read.sum") or 0) / 1e9 * (1e3 if d.get("dram__bytes_read.sum", "").count(".") == 0 else 1),
+            "dram_bytes_read": g("dram__bytes_read.sum"), "dram_bytes_write": g("dram__bytes_write.sum"),
+            "dram_pct": g("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+            "fp64_pct": g("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+            "l1_pct": g("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+            "issue_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "warps_active_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
+            "regs": g("launch__registers_per_thread"),
+        })
+    units = dict(zip(rows[0], rows[1]))
+    return res, units
+
+
+def main(lpath, fpath, tag, steps):
+    os.makedirs(os.path.join(REPO, "profiles"), exist_ok=True)
+    agg = launches(lpath)
+    tot = sum(v[1] for v in agg.values())
+    with open(os.path.join(REPO, "profiles", f"{tag}_launches.md"), "w") as f:
+        f.write(f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised)\n\n")
+        f.write(f"Command: `python bench.py --steps {steps} --warmup 3 --e2e-steps 1 --no-cpu-baseline` (C4). "
+                "Shares include warm-up/e2e launches; compare SHARES with bench.py's live kernels_ms_per_step.\n\n")
+        f.write("| kernel | launches | total ms | share |\n|---|---|---|---|\n")
+        for k, (n, ns) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+            f.write(f"| `{k}` | {n} | {ns / 1e6:.3f} | {ns / tot * 100:.1f}% |\n")
+    res, units = full(fpath)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    ur, uw = scale.get(units.get("dram__bytes_read.sum", "byte"), 1), scale.get(units.get("dram__bytes_write.sum", "byte"), 1)
+    traffic = collections.defaultdict(list)
+    with open(os.path.join(REPO, "profiles", f"{tag}_kernels.md"), "w") as f:
+        f.write(f"# {tag}: ncu --set full captures (C4, batched 1024 x 2^16)\n\n")
+        f.write("| kernel | grid | ms | DRAM read GB | DRAM write GB | DRAM % peak | fp64 pipe % | L1 % | issue % | warps active % | regs |\n")
+        f.write("|---|---|---|---|---|---|---|---|---|---|---|\n")
+        for r in res:
+            rb, wb = (r["dram_bytes_read"] or 0) * ur, (r["dram_bytes_write"] or 0) * uw
+            traffic[r["kernel"]].append(rb + wb)
+            f.write(f"| `{r['kernel']}` | {r['grid']} | {r['time_ms']:.3f} | {rb / 1e9:.3f} | {wb / 1e9:.3f} | "
+                    f"{r['dram_pct']:.1f} | {r['fp64_pct']:.1f} | {r['l1_pct']:.1f} | {r['issue_pct']:.1f} | "
+                    f"{r['warps_active_pct']:.1f} | {r['regs']:.0f} |\n")
+    short = {}
+    for k, v in traffic.items():
+        key = {"kbm_pad": "bm_pad", "kbm_band": "bm_band", "kbm_mid": "bm_mid", "kbm_col": "bm_col", "kbm_row": "bm_row",
+               "k_spread_p": "spread_p", "k_gather_b": "gather_b", "kbm_colin": "bm_colin",
+               "kbm_rowout": "bm_rowout"}.get(k.split("<")[0], k.split("<")[0])
+        short[key] = sum(v) / len(v)
+    json.dump(short, open(os.path.join(REPO, "profiles", "traffic_c4.json"), "w"), indent=1)
+    print(json.dumps(short, indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]))
