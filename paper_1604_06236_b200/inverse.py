@@ -169,7 +169,61 @@ def _charge_type4(f, P, taps):
     f.complex_mul(P)
 
 
+# Host-resident batches are streamed through the device in chunks of this many
+# signals: H2D of chunk i+1 and D2H of chunk i-1 (two copy streams, PCIe is
+# full duplex) overlap the solve of chunk i.
+STREAM_CHUNK = 128
+
+
+def _solve_streamed(name: str, plan: InversePlan, host, passes, dest):
+    """Pipelined host -> device -> host solve of a [batch, P] CPU tensor."""
+    torch = _device.torch
+    dev = plan.device
+    B, P = host.shape
+    if dest is None:
+        dest = torch.empty((B, P), dtype=torch.complex128, pin_memory=True)
+    src = host if host.dtype == torch.complex128 else host.to(torch.complex128)
+    main = torch.cuda.current_stream(dev)
+    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    chunk = STREAM_CHUNK
+    bufs_in = [torch.empty((chunk, P), dtype=torch.complex128, device=f"cuda:{dev}") for _ in range(2)]
+    bufs_out = [torch.empty((chunk, P), dtype=torch.complex128, device=f"cuda:{dev}") for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]      # solve of the chunk in slot k finished
+    drained = [torch.cuda.Event() for _ in range(2)]   # D2H of slot k finished
+    loaded = [torch.cuda.Event() for _ in range(2)]
+    for e in done + drained:
+        e.record(main)
+    st = main.cuda_stream
+    for i, lo in enumerate(range(0, B, chunk)):
+        hi = min(lo + chunk, B)
+        k, m = i % 2, hi - lo
+        with torch.cuda.stream(h2d):
+            h2d.wait_event(done[k])
+            bufs_in[k][:m].copy_(src[lo:hi], non_blocking=True)
+            loaded[k].record(h2d)
+        main.wait_event(loaded[k])
+        main.wait_event(drained[k])
+        if passes is None:
+            _lib.call(f"nfft45_{name}", plan.handle, bufs_in[k].data_ptr(), m, bufs_out[k].data_ptr(), st)
+        else:
+            _lib.call(f"nfft45_refine_{name}", plan.handle, bufs_in[k].data_ptr(), m, int(passes),
+                      bufs_out[k].data_ptr(), st)
+        done[k].record(main)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(done[k])
+            dest[lo:hi].copy_(bufs_out[k][:m], non_blocking=True)
+            drained[k].record(d2h)
+    d2h.synchronize()
+    main.wait_stream(d2h)
+    return dest
+
+
 def _solve(name: str, plan: InversePlan, data, label: str, passes: int | None, dest=None):
+    torch = _device.torch
+    if (isinstance(data, torch.Tensor) and not data.is_cuda and data.dim() == 2
+            and data.shape[0] > STREAM_CHUNK and data.shape[-1] == plan.size
+            and (dest is None or not dest.is_cuda)):
+        return _solve_streamed(name, plan, data, passes, dest)
     a = _device.operand(data, plan.device, length=plan.size, name=label)
     if dest is not None and dest.is_cuda and dest.dtype == _device.torch.complex128 and dest.is_contiguous():
         out = dest.reshape(a.tensor.shape)
