@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 2) kbm_pad(
     const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
     const double* __restrict__ cd, const double2* __restrict__ xsub, double2* __restrict__ xout) {
   constexpr int NC = 2 * M;
+  constexpr bool kLead2 = FastTraits<NC>::radix(0) == 2;
   extern __shared__ double2 sm[];
   const int r = blockIdx.x;
   const int64_t b0 = (int64_t)blockIdx.y * kSig;
@@ -126,15 +127,34 @@ __global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 2) kbm_pad(
       v = rsc(v, __ldg(&cd[p]));
     }
     const int n1 = (k2 - M / 2) & (NC - 1);
-    sm[sidx<NC, kSig, true>(n1, c)] = v;
-    sm[sidx<NC, kSig, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
+    if constexpr (kLead2) {
+      // The IFFT_2P column is zero outside the band, so its first Stockham
+      // pass (radix 2, pairs n1 and n1 + M) is a copy: write its outputs
+      // directly.  n1 in [0, M/2): partner zero -> (v, v); n1 in
+      // [3M/2, 2M): partner zero on the other side -> (v, -v).
+      if (n1 < M) {
+        sm[sidx<NC, kSig, true>(2 * n1, c)] = v;
+        sm[sidx<NC, kSig, true>(2 * n1 + 1, c)] = v;
+      } else {
+        const int j = n1 - M;
+        sm[sidx<NC, kSig, true>(2 * j, c)] = v;
+        sm[sidx<NC, kSig, true>(2 * j + 1, c)] = make_double2(-v.x, -v.y);
+      }
+    } else {
+      sm[sidx<NC, kSig, true>(n1, c)] = v;
+      sm[sidx<NC, kSig, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
+    }
   };
   fast_tile_fft<M, kSig, -1, true>(sm, ld1, st1, twR);
   __syncthreads();
-  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, kSig, true>(i, c)]; };
   auto st2 = [&](int k, int c, double2 v) { Y[((int64_t)k * M + r) * Bp + b0 + c] = v; };
   const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r, 0};
-  fast_tile_fft_smem<NC, kSig, +1, true>(sm, ld2, st2, twC, pt);
+  if constexpr (kLead2) {
+    fast_tile_fft_from<NC, kSig, +1, true, 1, 2>(sm, st2, twC, pt);
+  } else {
+    auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, kSig, true>(i, c)]; };
+    fast_tile_fft_smem<NC, kSig, +1, true>(sm, ld2, st2, twC, pt);
+  }
 }
 
 // row pass: row r = blockIdx.x (length L), output index r + R1 k.

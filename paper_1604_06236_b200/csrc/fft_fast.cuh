@@ -248,6 +248,15 @@ __device__ __forceinline__ void fast_tile_fft_smem(double2* sm, const Ld& ld, co
   fast_passes<N, C, S, CF, true, 0, 1>(sm, ld, st, tw, pt);
 }
 
+// Run passes P0.. of a tile FFT whose earlier passes were produced directly
+// in shared memory (Stockham layout after pass P0-1, Ns = NS0).
+template <int N, int C, int S, bool CF, int P0, int NS0, class St, class PT = NoPostTw>
+__device__ __forceinline__ void fast_tile_fft_from(double2* sm, const St& st, const double2* __restrict__ tw,
+                                                   const PT& pt = PT()) {
+  auto no_ld = [](int, int) -> double2 { return make_double2(0.0, 0.0); };
+  fast_passes<N, C, S, CF, false, P0, NS0>(sm, no_ld, st, tw, pt);
+}
+
 // the last-pass stride (= N / radix of the last pass) of a fast tile FFT
 template <int N>
 constexpr int last_stride() { return N / FastTraits<N>::radix(FastTraits<N>::np - 1); }

@@ -22,8 +22,8 @@ constexpr int kCPW = 8;          // spread: cells per warp
 constexpr int kSpreadWarps = 8;  // spread: warps per CTA -> 64 cells
 constexpr int kSpreadTile = kCPW * kSpreadWarps;
 constexpr int kSpreadCap = 72;   // nodes staged per batch
-constexpr int kNPW = 4;          // gather: nodes per warp
-constexpr int kGatherWarps = 8;  // gather: warps per CTA -> 32 nodes
+constexpr int kNPW = 8;          // gather: nodes per warp
+constexpr int kGatherWarps = 4;  // gather: warps per CTA -> 32 nodes
 constexpr int kGatherNodes = kNPW * kGatherWarps;
 constexpr int kGatherSpan = 112; // cells staged per chunk
 constexpr int kWTSpan = 64;      // per-warp weight-table cells per chunk
@@ -346,58 +346,73 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
     cp_async_commit();
   };
   // this warp's active nodes (window meets its 8 cells), compacted once per
-  // staged node set so the FMA loop is branch-free and software-pipelined
-  __shared__ int s_act[kSpreadWarps][kPipeCap];
+  // staged node set as (node, weight-row offset) pairs so the FMA loop is
+  // branch-free and address arithmetic is hoisted out of it
+  __shared__ int2 s_act[kSpreadWarps][kPipeCap];
   __shared__ int s_nact[kSpreadWarps];
   auto compact = [&](int cnt) {
     int na = 0;
     for (int e0 = 0; e0 < cnt; e0 += 32) {
       const int e = e0 + lane;
       bool act = false;
+      int woff = 0;
       if (e < cnt) {
-        const int o = jw - Cc2[e];
+        const int ce = Cc2[e];
+        const int o = jw - ce;
         act = (o >= -kM - 7 && o <= kM);
+        woff = e * kWRow + o + kM + 7 + ((ce + 1) & 1);
       }
       const unsigned m = __ballot_sync(0xffffffffu, act);
-      if (act) s_act[warp][na + __popc(m & ((1u << lane) - 1u))] = e;
+      if (act) s_act[warp][na + __popc(m & ((1u << lane) - 1u))] = make_int2(e, woff);
       na += __popc(m);
     }
     if (lane == 0) s_nact[warp] = na;
     __syncwarp();
   };
-  struct Op {
-    double2 w01, w23, w45, w67, fe, a[SPL];
-  };
-  auto fetch = [&](const double2* A, int e, Op& op) {
-    const int ce = Cc2[e];
-    const int x = jw - ce + kM + 7 + ((ce + 1) & 1);
-    const double2* wr = reinterpret_cast<const double2*>(W + e * kWRow + x);
-    op.w01 = wr[0];
-    op.w23 = wr[1];
-    op.w45 = wr[2];
-    op.w67 = wr[3];
-    op.fe = F[e];
-#pragma unroll
-    for (int s2 = 0; s2 < SPL; s2++) op.a[s2] = A[e * SIG + swz(lane + 32 * s2, e)];
-  };
-  auto fma_node = [&](const Op& op, double2 (&acc)[kCPW][SPL]) {
-    const double wc[8] = {op.w01.x, op.w01.y, op.w23.x, op.w23.y, op.w45.x, op.w45.y, op.w67.x, op.w67.y};
-#pragma unroll
-    for (int s2 = 0; s2 < SPL; s2++) {
-      const double2 a = cmul(op.a[s2], op.fe);
-#pragma unroll
-      for (int c = 0; c < kCPW; c++) caxpy(acc[c][s2], wc[c], a);
-    }
-  };
-  auto accumulate = [&](const double2* A, int /*cnt*/, double2 (&acc)[kCPW][SPL]) {
+  auto accumulate = [&](const double2* __restrict__ A, int /*cnt*/, double2 (&acc)[kCPW][SPL]) {
     const int na = s_nact[warp];
-    if (na == 0) return;
-    Op cur, nxt;
-    fetch(A, s_act[warp][0], cur);
-    for (int k = 0; k < na; k++) {
-      if (k + 1 < na) fetch(A, s_act[warp][k + 1], nxt);
-      fma_node(cur, acc);
-      cur = nxt;
+    const int2* __restrict__ act = s_act[warp];
+    int sw[SPL];
+#pragma unroll
+    for (int s2 = 0; s2 < SPL; s2++) sw[s2] = lane + 32 * s2;
+    int k = 0;
+    for (; k + 1 < na; k += 2) {
+      const int2 n0 = act[k], n1 = act[k + 1];
+      const double2* w0 = reinterpret_cast<const double2*>(W + n0.y);
+      const double2* w1 = reinterpret_cast<const double2*>(W + n1.y);
+      const double2 a01 = w0[0], a23 = w0[1], a45 = w0[2], a67 = w0[3];
+      const double2 b01 = w1[0], b23 = w1[1], b45 = w1[2], b67 = w1[3];
+      const double2 f0 = F[n0.x], f1 = F[n1.x];
+      double2 x0[SPL], x1[SPL];
+#pragma unroll
+      for (int s2 = 0; s2 < SPL; s2++) {
+        x0[s2] = A[n0.x * SIG + (sw[s2] ^ (n0.x & 7))];
+        x1[s2] = A[n1.x * SIG + (sw[s2] ^ (n1.x & 7))];
+      }
+      const double c0[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
+      const double c1[8] = {b01.x, b01.y, b23.x, b23.y, b45.x, b45.y, b67.x, b67.y};
+#pragma unroll
+      for (int s2 = 0; s2 < SPL; s2++) {
+        const double2 y0 = cmul(x0[s2], f0), y1 = cmul(x1[s2], f1);
+#pragma unroll
+        for (int c = 0; c < kCPW; c++) {
+          caxpy(acc[c][s2], c0[c], y0);
+          caxpy(acc[c][s2], c1[c], y1);
+        }
+      }
+    }
+    if (k < na) {
+      const int2 n0 = act[k];
+      const double2* w0 = reinterpret_cast<const double2*>(W + n0.y);
+      const double2 a01 = w0[0], a23 = w0[1], a45 = w0[2], a67 = w0[3];
+      const double2 f0 = F[n0.x];
+      const double c0[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
+#pragma unroll
+      for (int s2 = 0; s2 < SPL; s2++) {
+        const double2 y0 = cmul(A[n0.x * SIG + (sw[s2] ^ (n0.x & 7))], f0);
+#pragma unroll
+        for (int c = 0; c < kCPW; c++) caxpy(acc[c][s2], c0[c], y0);
+      }
     }
   };
   auto store = [&](int64_t g, double2 (&acc)[kCPW][SPL]) {
@@ -519,6 +534,7 @@ int spread_batched(const GridDev& g, int64_t n, const Window& win, const double2
 // [cell][signal] in chunks of kGatherSpan; each warp builds a dense weight
 // table WT[cell][8 nodes] for its own cells (zeros outside windows) so one
 // staged cell value feeds 8 FMAs with one 64-byte broadcast of weights.
+template <bool BM>
 __global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_b(const double* __restrict__ ts, const int* __restrict__ perm,
                                                     int64_t Q, int64_t n, double alpha, GaussTab G,
                                                     const double2* __restrict__ H, int64_t batch, NodeFactor nf,
@@ -565,7 +581,8 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_b(const double*
       for (int sig = warp; sig < SIG; sig += kGatherWarps) {
         const int64_t b = b0 + sig;
         const bool ok = b < batch;
-        if (lane < nq) cp_async16(&Sb[lane * SIG + swz(sig, lane)], sub + (ok ? b : 0) * Q + s_pq[lane], ok);
+        for (int e = lane; e < nq; e += 32)
+          cp_async16(&Sb[e * SIG + swz(sig, e)], sub + (ok ? b : 0) * Q + s_pq[e], ok);
       }
     } else {
       for (int e = warp; e < nq; e += kGatherWarps) {
@@ -588,16 +605,18 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_b(const double*
     const int len = ce - cs + 1;
     __syncthreads();  // previous chunk fully consumed
     // stage cells [cs, ce] (mod n) for the CTA's signals
-    auto wrap = [&](int64_t cell) -> int64_t {
-      if (cell < 0) cell += n;
-      if (cell >= n) cell -= n;
-      if (cell < 0 || cell >= n) {  // tiny grids: full reduction
-        cell %= n;
-        if (cell < 0) cell += n;
+    // cell index mod n: one conditional add/sub when the chunk spans less
+    // than a period (always, except tiny grids which take the full reduction)
+    const int ni = (int)n;
+    const bool small = n < (int64_t)kGatherSpan + 2 * kM + 2;
+    auto wrap = [&](int cell) -> int {
+      if (small) {
+        cell %= ni;
+        return cell < 0 ? cell + ni : cell;
       }
-      return cell;
+      return cell < 0 ? cell + ni : (cell >= ni ? cell - ni : cell);
     };
-    if (H_ld == 0) {
+    if constexpr (!BM) {
       for (int sig = warp; sig < SIG; sig += kGatherWarps) {
         const int64_t b = b0 + sig;
         const bool ok = b < batch;
@@ -606,8 +625,9 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_b(const double*
       }
     } else {
       const bool ok = b0 + lane < batch;
+      const double2* col = H + b0 + (ok ? lane : 0);
       for (int c = warp; c < len; c += kGatherWarps)
-        cp_async16(&Y[c * SIG + swz(lane, c)], H + wrap(cs + c) * H_ld + b0 + (ok ? lane : 0), ok);
+        cp_async16(&Y[c * SIG + lane], col + (int64_t)wrap(cs + c) * H_ld, ok);
     }
     // this warp's cells inside the chunk, in sub-chunks of kWTSpan (warp-private
     // table); the first table is built while the copies are in flight
@@ -635,9 +655,14 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_b(const double*
     for (int ws = a_lo; ws <= a_hi; ws += kWTSpan) {
       const int we = min(ws + kWTSpan - 1, a_hi);
       if (ws != a_lo) build(ws, we);
-      for (int c = ws; c <= we; c++) {
-        const double2 y = Y[(c - cs) * SIG + swz(lane, c - cs)];
-        const double2* wr = reinterpret_cast<const double2*>(wt + (c - ws) * kNPW);
+      const double2* __restrict__ yrow = Y + (ws - cs) * SIG;
+      const double2* __restrict__ wrow = reinterpret_cast<const double2*>(wt);
+      const int nc = we - ws + 1;
+#pragma unroll 4
+      for (int i = 0; i < nc; i++) {
+        const int r = ws - cs + i;
+        const double2 y = BM ? yrow[i * SIG + lane] : Y[r * SIG + swz(lane, r)];
+        const double2* wr = wrow + i * (kNPW / 2);
 #pragma unroll
         for (int i2 = 0; i2 < kNPW / 2; i2++) {
           const double2 w = wr[i2];
@@ -683,11 +708,18 @@ int gather_batched(const GridDev& g, int64_t n, const Window& win, const double2
   if (!sub) mode = 0;
   size_t smem = (size_t)kGatherSpan * 32 * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8 +
                 (mode ? (size_t)kGatherNodes * 32 * 16 : 0);
-  auto gather_b = k_gather_b;
-  NFFT_CUDA(cudaFuncSetAttribute(gather_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)ceil_div(g.Q, kGatherNodes), (unsigned)ceil_div(out_ld ? out_ld : batch, 32));
-  LAUNCH(gather_b, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), H, batch, f, sub,
-         mode, out, H_ld, sub_ld, out_ld);
+  if (H_ld) {
+    auto gather_b = k_gather_b<true>;
+    NFFT_CUDA(cudaFuncSetAttribute(gather_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LAUNCH(gather_b, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), H, batch, f,
+           sub, mode, out, H_ld, sub_ld, out_ld);
+  } else {
+    auto gather_b = k_gather_b<false>;
+    NFFT_CUDA(cudaFuncSetAttribute(gather_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LAUNCH(gather_b, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), H, batch, f,
+           sub, mode, out, H_ld, sub_ld, out_ld);
+  }
   return NFFT45_OK;
 }
 
