@@ -13,6 +13,9 @@
 // kernels transpose through shared memory (gridding_b.cu).
 //
 // Stage semantics are those of chain.cu (inverse.py:101-143, forward.py:26-102).
+#include <algorithm>
+#include <cstdlib>
+
 #include "fft_fast.cuh"
 #include "ops.cuh"
 
@@ -22,6 +25,41 @@ namespace {
 constexpr int kSig = 8;  // signals per tile (batch-minor kernels)
 
 __device__ __forceinline__ double2 rsc(double2 v, double s) { return make_double2(v.x * s, v.y * s); }
+
+__device__ __forceinline__ void cpa16(void* sdst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Persistent tile loop with a double-buffered cp.async prefetch of each
+// tile's input (L rows x 8 signals, row-contiguous in the batch-minor
+// layout): while tile t computes, tile t + gridDim.x is already in flight.
+template <int L, class Src, class Body>
+__device__ __forceinline__ void persistent_tiles(int ntiles, double2* buf0, double2* buf1, const Src& src,
+                                                 const Body& body) {
+  auto prefetch = [&](int t, double2* buf) {
+    for (int e = threadIdx.x; e < L * kSig; e += blockDim.x) cpa16(&buf[e], src(t, e >> 3, e & 7));
+    cpa_commit();
+  };
+  int t = blockIdx.x;
+  if (t < ntiles) prefetch(t, buf0);
+  for (int it = 0; t < ntiles; t += gridDim.x, it++) {
+    double2* cur = (it & 1) ? buf1 : buf0;
+    double2* nxt = (it & 1) ? buf0 : buf1;
+    if (t + (int)gridDim.x < ntiles) {
+      prefetch(t + gridDim.x, nxt);
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
+    }
+    __syncthreads();
+    body(t, cur);
+    __syncthreads();
+  }
+}
 }  // namespace
 
 // column pass: columns n2 = blockIdx.x of x[i * L2 + n2] (length L), optional
@@ -48,8 +86,8 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), 4) kbm_col(
 // row FFT_2P (row k1 = blockIdx.x, length 2M) -> band p = k1 + M m1 with
 // deconv*decay (or (X deconv - sub) decay) -> column IFFT_P (length M) ->
 // W_P^{+k1 k1'} -> U[(k1' M + k1)][b].
-template <int M>
-__global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 2) kbm_band(
+template <int M, int SG>
+__global__ void __launch_bounds__(fast_threads<2 * M, SG>(), (SG < 8 ? 3 : 2)) kbm_band(
     const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
@@ -57,7 +95,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 2) kbm_band(
   constexpr int NR = 2 * M;
   extern __shared__ double2 sm[];
   const int k1 = blockIdx.x;
-  const int64_t b0 = (int64_t)blockIdx.y * kSig;
+  const int64_t b0 = (int64_t)blockIdx.y * SG;
   auto ld1 = [&](int i, int c) -> double2 { return T[((int64_t)k1 * NR + i) * Bp + b0 + c]; };
   auto st1 = [&](int k2, int c, double2 v) {
     const int m1 = (k2 + M / 2) & (NR - 1);
@@ -70,15 +108,15 @@ __global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 2) kbm_band(
       } else {
         v = rsc(v, __ldg(&dd[p]));
       }
-      sm[sidx<M, kSig, true>(m1, c)] = v;
+      sm[sidx<M, SG, true>(m1, c)] = v;
     }
   };
-  fast_tile_fft<NR, kSig, -1, true>(sm, ld1, st1, twR);
+  fast_tile_fft<NR, SG, -1, true>(sm, ld1, st1, twR);
   __syncthreads();
-  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, kSig, true>(i, c)]; };
+  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, SG, true>(i, c)]; };
   auto st2 = [&](int k1p, int c, double2 v) { U[((int64_t)k1p * M + k1) * Bp + b0 + c] = v; };
   const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, k1, 0};
-  fast_tile_fft_smem<M, kSig, +1, true>(sm, ld2, st2, twC, pt);
+  fast_tile_fft_smem<M, SG, +1, true>(sm, ld2, st2, twC, pt);
 }
 
 // row IFFT_P (row r) -> * ks -> column FFT_P (column r) -> W_P^{-r k} -> Z.
@@ -104,8 +142,8 @@ __global__ void __launch_bounds__(fast_threads<M, kSig>(), 4) kbm_mid(
 
 // row FFT_P (row r) -> * coef (x = [xsub -] S coef stored when xout) *
 // deconv -> zero-padded column IFFT_2P (length 2M, column r) -> W_n^{+r k} -> Y.
-template <int M>
-__global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 2) kbm_pad(
+template <int M, int SG>
+__global__ void __launch_bounds__(fast_threads<2 * M, SG>(), (SG < 8 ? 3 : 2)) kbm_pad(
     const double2* __restrict__ Z, double2* __restrict__ Y, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
@@ -114,7 +152,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 2) kbm_pad(
   constexpr bool kLead2 = FastTraits<NC>::radix(0) == 2;
   extern __shared__ double2 sm[];
   const int r = blockIdx.x;
-  const int64_t b0 = (int64_t)blockIdx.y * kSig;
+  const int64_t b0 = (int64_t)blockIdx.y * SG;
   auto ld1 = [&](int i, int c) -> double2 { return Z[((int64_t)r * M + i) * Bp + b0 + c]; };
   auto st1 = [&](int k2, int c, double2 v) {
     const int64_t p = (int64_t)r + (int64_t)M * k2;
@@ -133,28 +171,133 @@ __global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 2) kbm_pad(
       // directly.  n1 in [0, M/2): partner zero -> (v, v); n1 in
       // [3M/2, 2M): partner zero on the other side -> (v, -v).
       if (n1 < M) {
-        sm[sidx<NC, kSig, true>(2 * n1, c)] = v;
-        sm[sidx<NC, kSig, true>(2 * n1 + 1, c)] = v;
+        sm[sidx<NC, SG, true>(2 * n1, c)] = v;
+        sm[sidx<NC, SG, true>(2 * n1 + 1, c)] = v;
       } else {
         const int j = n1 - M;
-        sm[sidx<NC, kSig, true>(2 * j, c)] = v;
-        sm[sidx<NC, kSig, true>(2 * j + 1, c)] = make_double2(-v.x, -v.y);
+        sm[sidx<NC, SG, true>(2 * j, c)] = v;
+        sm[sidx<NC, SG, true>(2 * j + 1, c)] = make_double2(-v.x, -v.y);
       }
     } else {
-      sm[sidx<NC, kSig, true>(n1, c)] = v;
-      sm[sidx<NC, kSig, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
+      sm[sidx<NC, SG, true>(n1, c)] = v;
+      sm[sidx<NC, SG, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
     }
   };
-  fast_tile_fft<M, kSig, -1, true>(sm, ld1, st1, twR);
+  fast_tile_fft<M, SG, -1, true>(sm, ld1, st1, twR);
   __syncthreads();
   auto st2 = [&](int k, int c, double2 v) { Y[((int64_t)k * M + r) * Bp + b0 + c] = v; };
   const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r, 0};
   if constexpr (kLead2) {
-    fast_tile_fft_from<NC, kSig, +1, true, 1, 2>(sm, st2, twC, pt);
+    fast_tile_fft_from<NC, SG, +1, true, 1, 2>(sm, st2, twC, pt);
   } else {
-    auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, kSig, true>(i, c)]; };
-    fast_tile_fft_smem<NC, kSig, +1, true>(sm, ld2, st2, twC, pt);
+    auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, SG, true>(i, c)]; };
+    fast_tile_fft_smem<NC, SG, +1, true>(sm, ld2, st2, twC, pt);
   }
+}
+
+// Persistent variant of kbm_pad (one CTA per SM walks all (row, group)
+// tiles; the next tile's Z row block is prefetched during compute).
+template <int M>
+__global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 1) kbm_pad_p(
+    const double2* __restrict__ Z, double2* __restrict__ Y, int64_t Bp, int groups, const double2* __restrict__ twR,
+    const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
+    const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
+    const double* __restrict__ cd, const double2* __restrict__ xsub, double2* __restrict__ xout) {
+  constexpr int NC = 2 * M;
+  constexpr bool kLead2 = FastTraits<NC>::radix(0) == 2;
+  extern __shared__ double2 sm[];
+  double2* buf0 = sm + (fast_smem<NC, kSig>() / sizeof(double2) + 1);
+  double2* buf1 = buf0 + M * kSig;
+  auto src = [&](int t, int i, int c) -> const double2* {
+    const int r = t % M;
+    const int64_t b0 = (int64_t)(t / M) * kSig;
+    return Z + ((int64_t)r * M + i) * Bp + b0 + c;
+  };
+  auto body = [&](int t, const double2* in) {
+    const int r = t % M;
+    const int64_t b0 = (int64_t)(t / M) * kSig;
+    auto ld1 = [&](int i, int c) -> double2 { return in[i * kSig + c]; };
+    auto st1 = [&](int k2, int c, double2 v) {
+      const int64_t p = (int64_t)r + (int64_t)M * k2;
+      if (xout) {
+        v = rsc(v, __ldg(&coef[p]));
+        if (xsub) v = csub(xsub[p * Bp + b0 + c], v);
+        xout[p * Bp + b0 + c] = v;
+        v = rsc(v, __ldg(&deconv[p]));
+      } else {
+        v = rsc(v, __ldg(&cd[p]));
+      }
+      const int n1 = (k2 - M / 2) & (NC - 1);
+      if constexpr (kLead2) {
+        if (n1 < M) {
+          sm[sidx<NC, kSig, true>(2 * n1, c)] = v;
+          sm[sidx<NC, kSig, true>(2 * n1 + 1, c)] = v;
+        } else {
+          const int j = n1 - M;
+          sm[sidx<NC, kSig, true>(2 * j, c)] = v;
+          sm[sidx<NC, kSig, true>(2 * j + 1, c)] = make_double2(-v.x, -v.y);
+        }
+      } else {
+        sm[sidx<NC, kSig, true>(n1, c)] = v;
+        sm[sidx<NC, kSig, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
+      }
+    };
+    fast_tile_fft<M, kSig, -1, true>(sm, ld1, st1, twR);
+    __syncthreads();
+    auto st2 = [&](int k, int c, double2 v) { Y[((int64_t)k * M + r) * Bp + b0 + c] = v; };
+    const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r, 0};
+    if constexpr (kLead2) {
+      fast_tile_fft_from<NC, kSig, +1, true, 1, 2>(sm, st2, twC, pt);
+    } else {
+      auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, kSig, true>(i, c)]; };
+      fast_tile_fft_smem<NC, kSig, +1, true>(sm, ld2, st2, twC, pt);
+    }
+  };
+  persistent_tiles<M>(M * groups, buf0, buf1, src, body);
+}
+
+// Persistent variant of kbm_band.
+template <int M>
+__global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 1) kbm_band_p(
+    const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, int groups, const double2* __restrict__ twR,
+    const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
+    const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
+    const double* __restrict__ dd, const double2* __restrict__ sub) {
+  constexpr int NR = 2 * M;
+  extern __shared__ double2 sm[];
+  double2* buf0 = sm + (fast_smem<NR, kSig>() / sizeof(double2) + 1);
+  double2* buf1 = buf0 + NR * kSig;
+  auto src = [&](int t, int i, int c) -> const double2* {
+    const int k1 = t % M;
+    const int64_t b0 = (int64_t)(t / M) * kSig;
+    return T + ((int64_t)k1 * NR + i) * Bp + b0 + c;
+  };
+  auto body = [&](int t, const double2* in) {
+    const int k1 = t % M;
+    const int64_t b0 = (int64_t)(t / M) * kSig;
+    auto ld1 = [&](int i, int c) -> double2 { return in[i * kSig + c]; };
+    auto st1 = [&](int k2, int c, double2 v) {
+      const int m1 = (k2 + M / 2) & (NR - 1);
+      if (m1 < M) {
+        const int64_t p = (int64_t)k1 + (int64_t)M * m1;
+        if (sub) {
+          v = rsc(v, __ldg(&deconv[p]));
+          v = csub(v, sub[p * Bp + b0 + c]);
+          v = rsc(v, __ldg(&decay[p]));
+        } else {
+          v = rsc(v, __ldg(&dd[p]));
+        }
+        sm[sidx<M, kSig, true>(m1, c)] = v;
+      }
+    };
+    fast_tile_fft<NR, kSig, -1, true>(sm, ld1, st1, twR);
+    __syncthreads();
+    auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, kSig, true>(i, c)]; };
+    auto st2 = [&](int k1p, int c, double2 v) { U[((int64_t)k1p * M + k1) * Bp + b0 + c] = v; };
+    const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, k1, 0};
+    fast_tile_fft_smem<M, kSig, +1, true>(sm, ld2, st2, twC, pt);
+  };
+  persistent_tiles<NR>(M * groups, buf0, buf1, src, body);
 }
 
 // row pass: row r = blockIdx.x (length L), output index r + R1 k.
@@ -239,6 +382,9 @@ struct ChainBM {
   int64_t Bp, batch;
   unsigned groups;  // Bp / 8
   cudaStream_t st;
+  int sms = 148;           // persistent grid size (set from the device)
+  bool persistent = true;
+  bool small_tiles = false;  // 4-signal tiles for the two-FFT kernels
 
   int qtab(int64_t Q, const double2** out) {
     int status = NFFT45_OK;
@@ -264,13 +410,31 @@ struct ChainBM {
   }
 
   int band(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub) {
-    auto bm_band = kbm_band<M>;
-    constexpr size_t smem = fast_smem<2 * M, kSig>();
-    NFFT_CHECK(bm_attr(bm_band, smem));
     constexpr int T = fast_threads<2 * M, kSig>();
     const int64_t Q = P / last_stride<M>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
+    constexpr size_t smem_p = fast_smem<2 * M, kSig>() + 16 + 2 * sizeof(double2) * 2 * M * kSig;
+    if (persistent && smem_p <= 227 * 1024) {
+      auto bm_band_p = kbm_band_p<M>;
+      NFFT_CHECK(bm_attr(bm_band_p, smem_p));
+      const int ntiles = M * (int)groups;
+      LAUNCH(bm_band_p, (unsigned)std::min(ntiles, sms), T, smem_p, st, T_, U, Bp, (int)groups, t.tw2M, t.twM,
+             t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
+      return NFFT45_OK;
+    }
+    if (small_tiles) {
+      auto bm_band4 = kbm_band<M, 4>;
+      constexpr size_t smem4 = fast_smem<2 * M, 4>();
+      NFFT_CHECK(bm_attr(bm_band4, smem4));
+      constexpr int T4 = fast_threads<2 * M, 4>();
+      LAUNCH(bm_band4, dim3((unsigned)M, groups * 2), T4, smem4, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi,
+             t.tP->s, twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
+      return NFFT45_OK;
+    }
+    auto bm_band = kbm_band<M, kSig>;
+    constexpr size_t smem = fast_smem<2 * M, kSig>();
+    NFFT_CHECK(bm_attr(bm_band, smem));
     LAUNCH(bm_band, dim3((unsigned)M, groups), T, smem, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s,
            twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
     return NFFT45_OK;
@@ -290,13 +454,31 @@ struct ChainBM {
   }
 
   int pad(const double2* Z, double2* Y, const ChainPlanView& pv, const double2* xsub, double2* xout) {
-    auto bm_pad = kbm_pad<M>;
-    constexpr size_t smem = fast_smem<2 * M, kSig>();
-    NFFT_CHECK(bm_attr(bm_pad, smem));
     constexpr int T = fast_threads<2 * M, kSig>();
     const int64_t Q = n / last_stride<2 * M>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
+    constexpr size_t smem_p = fast_smem<2 * M, kSig>() + 16 + 2 * sizeof(double2) * M * kSig;
+    if (persistent && smem_p <= 227 * 1024) {
+      auto bm_pad_p = kbm_pad_p<M>;
+      NFFT_CHECK(bm_attr(bm_pad_p, smem_p));
+      const int ntiles = M * (int)groups;
+      LAUNCH(bm_pad_p, (unsigned)std::min(ntiles, sms), T, smem_p, st, Z, Y, Bp, (int)groups, t.twM, t.tw2M, t.tN->lo,
+             t.tN->hi, t.tN->s, twQ, (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout);
+      return NFFT45_OK;
+    }
+    if (small_tiles) {
+      auto bm_pad4 = kbm_pad<M, 4>;
+      constexpr size_t smem4 = fast_smem<2 * M, 4>();
+      NFFT_CHECK(bm_attr(bm_pad4, smem4));
+      constexpr int T4 = fast_threads<2 * M, 4>();
+      LAUNCH(bm_pad4, dim3((unsigned)M, groups * 2), T4, smem4, st, Z, Y, Bp, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s,
+             twQ, (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout);
+      return NFFT45_OK;
+    }
+    auto bm_pad = kbm_pad<M, kSig>;
+    constexpr size_t smem = fast_smem<2 * M, kSig>();
+    NFFT_CHECK(bm_attr(bm_pad, smem));
     LAUNCH(bm_pad, dim3((unsigned)M, groups), T, smem, st, Z, Y, Bp, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s, twQ,
            (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout);
     return NFFT45_OK;
@@ -346,6 +528,17 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
   ch.batch = batch;
   ch.Bp = ceil_div(batch, kSig) * kSig;
   ch.groups = (unsigned)(ch.Bp / kSig);
+  {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) ch.sms = nsm;
+    // persistent prefetching variants measured slower on B200 (one CTA/SM
+    // serialises the FFT compute of consecutive tiles); opt-in for experiments
+    static const bool persist = getenv("NFFT45_PERSIST") != nullptr;
+    ch.persistent = persist;
+    static const bool small = getenv("NFFT45_TILE4") != nullptr;  // A/B experiment
+    ch.small_tiles = small;
+  }
   int status = NFFT45_OK;
   {
     const FftTables* a = fft_tables(M, st, &status);

@@ -259,13 +259,13 @@ __device__ __forceinline__ void fast_tile_fft_from(double2* sm, const St& st, co
 
 // the last-pass stride (= N / radix of the last pass) of a fast tile FFT
 template <int N>
-constexpr int last_stride() { return N / FastTraits<N>::radix(FastTraits<N>::np - 1); }
+__host__ __device__ constexpr int last_stride() { return N / FastTraits<N>::radix(FastTraits<N>::np - 1); }
 
 template <int N, int C>
-constexpr int fast_threads() { return N * C / FastTraits<N>::E; }
+__host__ __device__ constexpr int fast_threads() { return N * C / FastTraits<N>::E; }
 
 template <int N, int C>
-constexpr size_t fast_smem() {
+__host__ __device__ constexpr size_t fast_smem() {
   return FastTraits<N>::np > 1 ? ((size_t)N * C + (size_t)N * C / 8 + 1) * sizeof(double2) : 16;
 }
 

@@ -4,7 +4,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -114,7 +116,27 @@ struct nfft45_grid {
   GridDev d;
 };
 
+// CUDA-graph cache for launch-bound solves (small P x batch): the second call
+// with the same (kind, batch, passes, pointers) captures the launch sequence
+// on a library-owned stream; later calls replay it with one graph launch.
+struct GraphKey {
+  int kind, passes;
+  int64_t batch;
+  const void* in;
+  void* out;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(kind, passes, batch, in, out) < std::tie(o.kind, o.passes, o.batch, o.in, o.out);
+  }
+};
+struct GraphCache {
+  std::mutex mu;
+  std::map<GraphKey, cudaGraphExec_t> execs;
+  std::map<GraphKey, int64_t> kernels;  // kernel nodes per graph (for nfft45_launch_count)
+  std::map<GraphKey, int> seen;
+};
+
 struct nfft45_plan {
+  GraphCache* gc = nullptr;
   const nfft45_grid* g;
   int64_t P;
   double a;
@@ -498,6 +520,107 @@ static int refine_core(const nfft45_plan* p, const double2* data, int64_t batch,
 
 }  // namespace nfft45
 
+namespace nfft45 {
+
+// per-thread library stream used for capture / replay (forked from and joined
+// back to the caller's stream with events)
+static cudaStream_t lib_stream() {
+  static thread_local cudaStream_t s[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!s[dev]) cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking);
+  return s[dev];
+}
+
+static bool graph_eligible(const nfft45_plan* p, int64_t batch, int passes) {
+  static const bool off = getenv("NFFT45_NO_GRAPH") != nullptr;
+  return !off && passes <= 1 && p->P * batch <= (int64_t(1) << 22);
+}
+
+// run `fn(stream)` directly, or capture/replay it as a CUDA graph
+template <class Fn>
+static int run_graphed(const nfft45_plan* p, int kind, int64_t batch, int passes, const void* in, void* out,
+                       cudaStream_t user, const Fn& fn) {
+  if (!graph_eligible(p, batch, passes)) return fn(user);
+  nfft45_plan* mp = const_cast<nfft45_plan*>(p);
+  GraphKey key{kind, passes, batch, in, out};
+  cudaGraphExec_t exec = nullptr;
+  bool capture = false;
+  int64_t nkern = 0;
+  {
+    std::lock_guard<std::mutex> lk(mp->gc->mu);
+    auto it = mp->gc->execs.find(key);
+    if (it != mp->gc->execs.end()) {
+      exec = it->second;
+      nkern = mp->gc->kernels[key];
+    }
+    else if (++mp->gc->seen[key] >= 2 && mp->gc->execs.size() < 64) capture = true;
+  }
+  if (!exec && !capture) return fn(user);
+  cudaStream_t ls = lib_stream();
+  if (!ls) return fn(user);
+  cudaEvent_t e0, e1;
+  NFFT_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+  NFFT_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+  int status = NFFT45_OK;
+  NFFT_CUDA(cudaEventRecord(e0, user));
+  NFFT_CUDA(cudaStreamWaitEvent(ls, e0, 0));
+  if (!exec) {
+    cudaGraph_t graph = nullptr;
+    NFFT_CUDA(cudaStreamBeginCapture(ls, cudaStreamCaptureModeThreadLocal));
+    status = fn(ls);
+    cudaError_t ce = cudaStreamEndCapture(ls, &graph);
+    if (status == NFFT45_OK && ce == cudaSuccess) {
+      size_t nn = 0;
+      cudaGraphGetNodes(graph, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+      for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) nkern++;
+      }
+      // the captured launches were counted by LAUNCH already; replays add nkern each
+      ce = cudaGraphInstantiate(&exec, graph, 0);
+      if (ce == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(mp->gc->mu);
+        auto it = mp->gc->execs.find(key);
+        if (it == mp->gc->execs.end()) {
+          mp->gc->execs[key] = exec;
+          mp->gc->kernels[key] = nkern;
+        } else {
+          cudaGraphExecDestroy(exec);
+          exec = it->second;
+        }
+      }
+      NFFT_CUDA(cudaGraphLaunch(exec, ls));
+      NFFT_CUDA(cudaEventRecord(e1, ls));
+      NFFT_CUDA(cudaStreamWaitEvent(user, e1, 0));
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      if (graph) cudaGraphDestroy(graph);
+      return status;
+    }
+    if (graph) cudaGraphDestroy(graph);
+    if (status != NFFT45_OK || ce != cudaSuccess || !exec) {
+      cudaGetLastError();
+      // fall back to a direct run on the caller's stream
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      return status != NFFT45_OK ? status : fn(user);
+    }
+  }
+  NFFT_CUDA(cudaGraphLaunch(exec, ls));
+  g_launches.fetch_add(nkern, std::memory_order_relaxed);
+  NFFT_CUDA(cudaEventRecord(e1, ls));
+  NFFT_CUDA(cudaStreamWaitEvent(user, e1, 0));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return status;
+}
+
+}  // namespace nfft45
+
 // ================================================================== C ABI
 
 extern "C" {
@@ -750,6 +873,7 @@ int nfft45_plan_create(const nfft45_grid* g, double a, int eta, int m, void* st,
   if (dg.status) return dg.status;
   cudaStream_t s = S(st);
   nfft45_plan* p = new nfft45_plan();
+  p->gc = new GraphCache();
   p->g = g;
   p->P = P;
   p->a = a;
@@ -802,6 +926,7 @@ int nfft45_plan_create(const nfft45_grid* g, double a, int eta, int m, void* st,
   if (status) {
     cudaStreamSynchronize(s);
     cudaFree(p->tables);
+    delete p->gc;
     delete p;
     return status;
   }
@@ -812,6 +937,10 @@ int nfft45_plan_create(const nfft45_grid* g, double a, int eta, int m, void* st,
 void nfft45_plan_destroy(nfft45_plan* p) {
   if (!p) return;
   DeviceGuard dg(p->g->d.device);
+  if (p->gc) {
+    for (auto& kv : p->gc->execs) cudaGraphExecDestroy(kv.second);
+    delete p->gc;
+  }
   cudaFree(p->tables);
   delete p;
 }
@@ -829,28 +958,32 @@ int nfft45_type5(const nfft45_plan* p, const double* s, int64_t batch, double* o
   if (!p) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid plan");
   DeviceGuard dg(p->g->d.device);
   if (dg.status) return dg.status;
-  return type5_core(p, C2(s), batch, D2(out), S(st));
+  return run_graphed(p, 5, batch, -1, s, out, S(st),
+                     [&](cudaStream_t ss) { return type5_core(p, C2(s), batch, D2(out), ss); });
 }
 
 int nfft45_type4(const nfft45_plan* p, const double* A, int64_t batch, double* out, void* st) {
   if (!p) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid plan");
   DeviceGuard dg(p->g->d.device);
   if (dg.status) return dg.status;
-  return type4_core(p, C2(A), batch, D2(out), S(st));
+  return run_graphed(p, 4, batch, -1, A, out, S(st),
+                     [&](cudaStream_t ss) { return type4_core(p, C2(A), batch, D2(out), ss); });
 }
 
 int nfft45_refine_type5(const nfft45_plan* p, const double* s, int64_t batch, int passes, double* out, void* st) {
   if (!p || passes < 0) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid refine arguments");
   DeviceGuard dg(p->g->d.device);
   if (dg.status) return dg.status;
-  return refine_core(p, C2(s), batch, passes, D2(out), true, S(st));
+  return run_graphed(p, 15, batch, passes, s, out, S(st),
+                     [&](cudaStream_t ss) { return refine_core(p, C2(s), batch, passes, D2(out), true, ss); });
 }
 
 int nfft45_refine_type4(const nfft45_plan* p, const double* A, int64_t batch, int passes, double* out, void* st) {
   if (!p || passes < 0) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid refine arguments");
   DeviceGuard dg(p->g->d.device);
   if (dg.status) return dg.status;
-  return refine_core(p, C2(A), batch, passes, D2(out), false, S(st));
+  return run_graphed(p, 14, batch, passes, A, out, S(st),
+                     [&](cudaStream_t ss) { return refine_core(p, C2(A), batch, passes, D2(out), false, ss); });
 }
 
 }  // extern "C"

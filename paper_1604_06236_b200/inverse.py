@@ -172,7 +172,7 @@ def _charge_type4(f, P, taps):
 # Host-resident batches are streamed through the device in chunks of this many
 # signals: H2D of chunk i+1 and D2H of chunk i-1 (two copy streams, PCIe is
 # full duplex) overlap the solve of chunk i.
-STREAM_CHUNK = 128
+STREAM_CHUNK = 64
 
 
 def _solve_streamed(name: str, plan: InversePlan, host, passes, dest):
