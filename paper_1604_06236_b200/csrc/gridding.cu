@@ -328,6 +328,9 @@ int gather_layout(const GridDev& g, int64_t n, const Window& win, const double2*
                   NodeFactor f, const double2* sub, int64_t sub_ld, int mode, double2* out, int64_t out_ld,
                   cudaStream_t st) {
   if (!sub) mode = 0;
+  static const bool no_pipe = getenv("NFFT45_NO_GPIPE") != nullptr;  // A/B switch
+  if (!no_pipe && win.m == kFastM && n >= 256 && H_ld)
+    return gather_persistent(g, n, win, H, H_ld, batch, f, sub, sub_ld, mode, out, out_ld, st);
   if (win.m == kFastM && n >= 128 && (H_ld || sub_ld || out_ld || batch >= 32))
     return gather_batched(g, n, win, H, batch, f, sub, mode, out, st, H_ld, sub_ld, out_ld);
   if (H_ld || sub_ld || out_ld) {

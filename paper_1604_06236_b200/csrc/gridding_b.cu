@@ -535,12 +535,11 @@ int spread_batched(const GridDev& g, int64_t n, const Window& win, const double2
 // table WT[cell][8 nodes] for its own cells (zeros outside windows) so one
 // staged cell value feeds 8 FMAs with one 64-byte broadcast of weights.
 template <bool BM>
-__global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_b(const double* __restrict__ ts, const int* __restrict__ perm,
-                                                    int64_t Q, int64_t n, double alpha, GaussTab G,
-                                                    const double2* __restrict__ H, int64_t batch, NodeFactor nf,
-                                                    const double2* __restrict__ sub, int mode,
-                                                    double2* __restrict__ out, int64_t H_ld, int64_t sub_ld,
-                                                    int64_t out_ld) {
+__device__ __forceinline__ void gather_b_tile(const double* __restrict__ ts, const int* __restrict__ perm, int64_t Q,
+                                              int64_t n, double alpha, GaussTab G, const double2* __restrict__ H,
+                                              int64_t batch, NodeFactor nf, const double2* __restrict__ sub, int mode,
+                                              double2* __restrict__ out, int64_t H_ld, int64_t sub_ld, int64_t out_ld,
+                                              const int64_t b0) {
   // *_ld == 0: signal-major operand ([batch][len]); else batch-minor x[i * ld + b]
   constexpr int SIG = 32;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -554,7 +553,6 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_b(const double*
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t q0 = (int64_t)blockIdx.x * kGatherNodes;
-  const int64_t b0 = (int64_t)blockIdx.y * SIG;
   const int nq = (int)min((int64_t)kGatherNodes, Q - q0);
 
   if (tid < kGatherNodes) {
@@ -702,23 +700,245 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_b(const double*
   }
 }
 
+
+
+template <bool BM>
+__global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_b(const double* __restrict__ ts, const int* __restrict__ perm,
+                                                    int64_t Q, int64_t n, double alpha, GaussTab G,
+                                                    const double2* __restrict__ H, int64_t batch, NodeFactor nf,
+                                                    const double2* __restrict__ sub, int mode,
+                                                    double2* __restrict__ out, int64_t H_ld, int64_t sub_ld,
+                                                    int64_t out_ld, const int* __restrict__ only, int ny) {
+  // only != nullptr: process just the node blocks flagged there (fallback use;
+  // launched with one CTA row that walks all ny signal groups)
+  if (only && !only[blockIdx.x]) return;
+  for (int gy = blockIdx.y; gy < ny; gy += gridDim.y) {
+    if (gy != (int)blockIdx.y) __syncthreads();  // shared tiles are reused
+    gather_b_tile<BM>(ts, perm, Q, n, alpha, G, H, batch, nf, sub, mode, out, H_ld, sub_ld, out_ld, (int64_t)gy * 32);
+  }
+}
+
+int gather_fallback(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch, NodeFactor f,
+                    const double2* sub, int mode, double2* out, cudaStream_t st, int64_t H_ld, int64_t sub_ld,
+                    int64_t out_ld, const int* only);
+
+// Persistent interpolation from a batch-minor grid H[j * H_ld + b]: one CTA
+// per block of 32 ascending nodes (4 warps x 8) walks the signal groups
+// g = blockIdx.y, blockIdx.y + gridDim.y, ...  Node geometry and the
+// per-warp weight tables WT[cell][8 nodes] are built once per block; the
+// next group's cells are fetched with cp.async while the current group's
+// results are finished.  Batch-minor outputs / subtrahends go straight
+// between registers and global memory (lane = signal); signal-major ones are
+// transposed through shared memory.  Blocks whose cell span exceeds the
+// staging buffer (strongly clustered grids) return early and are handled by
+// k_gather_b (host passes `fallback` so those blocks are recomputed there).
+constexpr int kGPSpan = 112;
+
+template <bool OUT_BM, int SUBM>  // SUBM: 0 none, 1 batch-minor, 2 signal-major
+__global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_p(
+    const double* __restrict__ ts, const int* __restrict__ perm, int64_t Q, int64_t n, double alpha, GaussTab G,
+    const double2* __restrict__ H, int64_t H_ld, int64_t batch, NodeFactor nf, const double2* __restrict__ sub,
+    int64_t sub_ld, int mode, double2* __restrict__ out, int64_t out_ld, int ngroups, int* __restrict__ overflow) {
+  constexpr int SIG = 32;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double2* Y = reinterpret_cast<double2*>(smraw);                     // [kGPSpan][SIG]
+  double* WT = reinterpret_cast<double*>(Y + kGPSpan * SIG);           // [warps][kWTSpan][8]
+  double2* Sb = reinterpret_cast<double2*>(WT + kGatherWarps * kWTSpan * kNPW);  // [nodes][SIG] (SUBM == 2)
+  double2* O = Sb + (SUBM == 2 ? kGatherNodes * SIG : 0);              // [nodes][SIG] (!OUT_BM)
+  __shared__ int s_c0[kGatherNodes];
+  __shared__ double s_f[kGatherNodes];
+  __shared__ double2 s_fac[kGatherNodes];
+  __shared__ int s_pq[kGatherNodes];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t q0 = (int64_t)blockIdx.x * kGatherNodes;
+  const int nq = (int)min((int64_t)kGatherNodes, Q - q0);
+  if (tid < kGatherNodes) {
+    int c = 0;
+    double f = 0.0;
+    const int e = tid < nq ? tid : nq - 1;
+    const double t = ts[q0 + e];
+    const NodeGeo geo = node_geo(t, (double)n);
+    c = geo.i0;
+    f = tid < nq ? geo.f : 0.0;
+    s_c0[tid] = c;
+    s_f[tid] = f;
+    if (tid < nq) {
+      s_fac[tid] = factor_at(nf, q0 + tid, t);
+      s_pq[tid] = perm[q0 + tid];
+    }
+  }
+  __syncthreads();
+  const int cs = s_c0[0] - kM, ce = s_c0[kGatherNodes - 1] + kM;
+  const int len = ce - cs + 1;
+  const int w_lo = s_c0[warp * kNPW] - kM, w_hi = s_c0[warp * kNPW + kNPW - 1] + kM;
+  if (len > kGPSpan || w_hi - w_lo + 1 > kWTSpan || n < (int64_t)kGPSpan + 2 * kM + 2) {
+    if (tid == 0 && blockIdx.y == 0) overflow[blockIdx.x] = 1;  // handled by the fallback kernel
+    return;
+  }
+  // per-warp dense weight table over the warp's cells, built once
+  double* wt = WT + warp * kWTSpan * kNPW;
+  const int wl = w_hi - w_lo + 1;
+  for (int i = lane; i < wl * kNPW; i += 32) wt[i] = 0.0;
+  __syncwarp();
+  if (lane < kNPW && warp * kNPW + lane < nq) {
+    double w[2 * kM + 1];
+    taps29(s_f[warp * kNPW + lane], alpha, G, w);
+    const int c0 = s_c0[warp * kNPW + lane] - kM - w_lo;
+#pragma unroll
+    for (int k = 0; k < 2 * kM + 1; k++) wt[(c0 + k) * kNPW + lane] = w[k];
+  }
+  __syncwarp();
+  const int ni = (int)n;
+  auto stage = [&](int64_t g) {
+    const int64_t b0 = g * SIG;
+    const bool ok = b0 + lane < batch;
+    const double2* col = H + b0 + (ok ? lane : 0);
+    for (int c = warp; c < len; c += kGatherWarps) {
+      int cell = cs + c;
+      cell = cell < 0 ? cell + ni : (cell >= ni ? cell - ni : cell);
+      cp_async16(&Y[c * SIG + lane], col + (int64_t)cell * H_ld, ok);
+    }
+    if (SUBM == 2 && mode != 0) {
+      for (int sig = warp; sig < SIG; sig += kGatherWarps) {
+        const int64_t b = b0 + sig;
+        const bool okb = b < batch;
+        for (int e = lane; e < nq; e += 32)
+          cp_async16(&Sb[e * SIG + swz(sig, e)], sub + (okb ? b : 0) * Q + s_pq[e], okb);
+      }
+    }
+    cp_async_commit();
+  };
+  int64_t g = blockIdx.y;
+  if (g < ngroups) stage(g);
+  const double2* __restrict__ yw = Y + (w_lo - cs) * SIG + lane;
+  const double2* __restrict__ wr0 = reinterpret_cast<const double2*>(wt);
+  for (; g < ngroups; g += gridDim.y) {
+    const int64_t b0 = g * SIG;
+    cp_async_wait_group<0>();
+    __syncthreads();
+    double2 acc[kNPW];
+#pragma unroll
+    for (int i = 0; i < kNPW; i++) acc[i] = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (int i = 0; i < wl; i++) {
+      const double2 y = yw[i * SIG];
+      const double2* wr = wr0 + i * (kNPW / 2);
+#pragma unroll
+      for (int i2 = 0; i2 < kNPW / 2; i2++) {
+        const double2 w = wr[i2];
+        caxpy(acc[2 * i2], w.x, y);
+        caxpy(acc[2 * i2 + 1], w.y, y);
+      }
+    }
+    double2 sb_in[kNPW];
+    if (SUBM == 2 && mode != 0) {
+#pragma unroll
+      for (int i = 0; i < kNPW; i++) {
+        const int e = warp * kNPW + i;
+        sb_in[i] = e < nq ? Sb[e * SIG + swz(lane, e)] : make_double2(0.0, 0.0);
+      }
+    }
+    __syncthreads();  // Y (and Sb) consumed: prefetch the next group during the epilogue
+    if (g + gridDim.y < ngroups) stage(g + gridDim.y);
+    if constexpr (OUT_BM) {
+      const int64_t b = b0 + lane;
+#pragma unroll
+      for (int i = 0; i < kNPW; i++) {
+        const int e = warp * kNPW + i;
+        if (e >= nq || b >= out_ld) continue;
+        double2 v = cmul(acc[i], s_fac[e]);
+        const int64_t pq = s_pq[e];
+        if (b < batch && mode != 0) {
+          const double2 sv = SUBM == 1 ? sub[pq * sub_ld + b] : sb_in[i];
+          v = mode == 1 ? csub(v, sv) : csub(sv, v);
+        }
+        out[pq * out_ld + b] = b < batch ? v : make_double2(0.0, 0.0);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kNPW; i++) {
+        const int e = warp * kNPW + i;
+        double2 v = cmul(acc[i], e < nq ? s_fac[e] : make_double2(0.0, 0.0));
+        if (mode != 0 && e < nq && b0 + lane < batch) {
+          const double2 sv = SUBM == 1 ? sub[(int64_t)s_pq[e] * sub_ld + b0 + lane] : sb_in[i];
+          v = mode == 1 ? csub(v, sv) : csub(sv, v);
+        }
+        O[e * SIG + swz(lane, e)] = v;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < kGatherNodes * SIG; idx += blockDim.x) {
+        const int e = idx & (kGatherNodes - 1), sig = idx / kGatherNodes;
+        const int64_t b = b0 + sig;
+        if (b < batch && e < nq) out[b * Q + s_pq[e]] = O[e * SIG + swz(sig, e)];
+      }
+    }
+  }
+}
+
+__global__ void k_overflow_clear(int* f, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) f[i] = 0;
+}
+
+int gather_persistent(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t H_ld, int64_t batch,
+                      NodeFactor f, const double2* sub, int64_t sub_ld, int mode, double2* out, int64_t out_ld,
+                      cudaStream_t st) {
+  if (!sub) mode = 0;
+  const int64_t nblk = ceil_div(g.Q, kGatherNodes);
+  const int ngroups = (int)ceil_div(out_ld ? out_ld : batch, 32);
+  const int slices = (int)std::min<int64_t>(ngroups, std::max<int64_t>(1, ceil_div(4 * 148, nblk)));
+  int* overflow = nullptr;
+  NFFT_CUDA(cudaMallocAsync(&overflow, sizeof(int) * nblk, st));
+  LAUNCH(k_overflow_clear, (unsigned)ceil_div(nblk, 256), 256, 0, st, overflow, nblk);
+  const int subm = mode == 0 ? 0 : (sub_ld ? 1 : 2);
+  size_t smem = (size_t)kGPSpan * 32 * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8 +
+                (subm == 2 ? (size_t)kGatherNodes * 32 * 16 : 0) + (out_ld ? 0 : (size_t)kGatherNodes * 32 * 16);
+  dim3 grid((unsigned)nblk, (unsigned)slices);
+  GaussTab G = gauss_tab(win);
+#define NFFT_GP_LAUNCH(OBM, SM_)                                                                              \
+  {                                                                                                          \
+    auto gather_p = k_gather_p<OBM, SM_>;                                                                    \
+    NFFT_CUDA(cudaFuncSetAttribute(gather_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
+    LAUNCH(gather_p, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, H_ld, batch, f,  \
+           sub, sub_ld, mode, out, out_ld, ngroups, overflow);                                               \
+  }
+  if (out_ld) {
+    if (subm == 0) NFFT_GP_LAUNCH(true, 0) else if (subm == 1) NFFT_GP_LAUNCH(true, 1) else NFFT_GP_LAUNCH(true, 2)
+  } else {
+    if (subm == 0) NFFT_GP_LAUNCH(false, 0) else if (subm == 1) NFFT_GP_LAUNCH(false, 1) else NFFT_GP_LAUNCH(false, 2)
+  }
+#undef NFFT_GP_LAUNCH
+  // blocks that overflowed the staging buffers: recompute them with the chunked kernel
+  NFFT_CHECK(gather_fallback(g, n, win, H, batch, f, sub, mode, out, st, H_ld, sub_ld, out_ld, overflow));
+  NFFT_CUDA(cudaFreeAsync(overflow, st));
+  return NFFT45_OK;
+}
+
 int gather_batched(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch, NodeFactor f,
                    const double2* sub, int mode, double2* out, cudaStream_t st, int64_t H_ld, int64_t sub_ld,
                    int64_t out_ld) {
+  return gather_fallback(g, n, win, H, batch, f, sub, mode, out, st, H_ld, sub_ld, out_ld, nullptr);
+}
+
+int gather_fallback(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch, NodeFactor f,
+                    const double2* sub, int mode, double2* out, cudaStream_t st, int64_t H_ld, int64_t sub_ld,
+                    int64_t out_ld, const int* only) {
   if (!sub) mode = 0;
   size_t smem = (size_t)kGatherSpan * 32 * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8 +
                 (mode ? (size_t)kGatherNodes * 32 * 16 : 0);
-  dim3 grid((unsigned)ceil_div(g.Q, kGatherNodes), (unsigned)ceil_div(out_ld ? out_ld : batch, 32));
+  const int ny = (int)ceil_div(out_ld ? out_ld : batch, 32);
+  dim3 grid((unsigned)ceil_div(g.Q, kGatherNodes), only ? 1u : (unsigned)ny);
   if (H_ld) {
     auto gather_b = k_gather_b<true>;
     NFFT_CUDA(cudaFuncSetAttribute(gather_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     LAUNCH(gather_b, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), H, batch, f,
-           sub, mode, out, H_ld, sub_ld, out_ld);
+           sub, mode, out, H_ld, sub_ld, out_ld, only, ny);
   } else {
     auto gather_b = k_gather_b<false>;
     NFFT_CUDA(cudaFuncSetAttribute(gather_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     LAUNCH(gather_b, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), H, batch, f,
-           sub, mode, out, H_ld, sub_ld, out_ld);
+           sub, mode, out, H_ld, sub_ld, out_ld, only, ny);
   }
   return NFFT45_OK;
 }

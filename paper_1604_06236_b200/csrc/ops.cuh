@@ -93,6 +93,9 @@ int spread_batched(const GridDev& g, int64_t n, const Window& win, const double2
 int gather_batched(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch, NodeFactor f,
                    const double2* sub, int mode, double2* out, cudaStream_t st, int64_t H_ld = 0, int64_t sub_ld = 0,
                    int64_t out_ld = 0);
+int gather_persistent(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t H_ld, int64_t batch,
+                      NodeFactor f, const double2* sub, int64_t sub_ld, int mode, double2* out, int64_t out_ld,
+                      cudaStream_t st);
 int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch,
                      int64_t amp_ld, NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st);
 // Layout-aware wrappers for the batch-minor chains (ld == 0: signal-major).
