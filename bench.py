@@ -55,14 +55,15 @@ PASSES = 1
 # fused kernels each implement parts of that budget; per step (one refined
 # type-5 + one refined type-4) the launches of each kernel carry:
 ALGO_BYTES_PER_POINT_STEP = {
-    "spread_b": 3 * 48,          # 3 spreads
-    "gather_b": 3 * 48,          # 3 gathers
+    "spread": 3 * 48,            # 3 spreads (spread_p; spread_b for other layouts)
+    "gather": 3 * 48,            # 3 gathers (gather_p; gather_b = its fallback for wide node blocks)
     "chain_col": 3 * 32 + 16,    # 3 x (FFT_2P column pass) + 1 x (IFFT_P column pass)
     "chain_band": 3 * 48,        # 3 x (FFT_2P row pass + IFFT_P column pass)
     "chain_mid": 4 * 32,         # 4 x (IFFT_P row pass + FFT_P column pass)
     "chain_pad": 3 * 48,         # 3 x (FFT_P row pass + IFFT_2P column pass)
     "chain_row": 3 * 32 + 16,    # 3 x (IFFT_2P row pass) + 1 x (FFT_P row pass)
     # batch-minor chains (batches >= 16): same stages, plus the two layout-boundary kernels
+    # (only one of the chain_* / bm_* families runs for a given batch)
     "bm_col": 3 * 32,            # 3 x FFT_2P column pass
     "bm_colin": 16,              # 1 x IFFT_P column pass (type-4 input, signal-major -> batch-minor)
     "bm_band": 3 * 48,
@@ -347,6 +348,13 @@ def main():
     _lib.profile_enable(False)
     launches = _lib.load().nfft45_launch_count() - l0
     kprof = _lib.profile_read()
+    kernels_raw = dict(kprof)
+    fam = {}  # spread_p/spread_b -> spread, gather_p/gather_b -> gather
+    for name, (cnt, kms) in kprof.items():
+        key = name.split("_")[0] if name.split("_")[0] in ("spread", "gather") else name
+        c0, m0 = fam.get(key, (0, 0.0))
+        fam[key] = (max(c0, cnt), m0 + kms)
+    kprof = fam
     barrier(world)
     ms = max_over_ranks(ev0.elapsed_time(ev1), world)
     pts_per_step = 2 * B * P * world
@@ -397,7 +405,8 @@ def main():
         traffic = None
         tfile = os.path.join(REPO, "profiles", f"traffic_{args.config}.json")
         if os.path.exists(tfile):
-            traffic = json.load(open(tfile)).get(tname)
+            tj = json.load(open(tfile))
+            traffic = tj.get(tname, next((v for k, v in tj.items() if k.startswith(tname + "_")), None))
         roof = {"kernel": tname, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes_per_launch": algo,
                 "avg_launch_ms": avg_ms, "launches": tcount, "share_of_kernel_time": tms / step_kernel_ms,
@@ -408,7 +417,7 @@ def main():
         if name in ALGO_BYTES_PER_POINT_STEP and kms > 0:
             gbs = ALGO_BYTES_PER_POINT_STEP[name] * B * P * args.steps / (kms / 1e3) / 1e9
             per_kernel_roofline[name] = {"achieved_GBps": gbs, "frac": gbs / peak}
-    total_algo = sum(ALGO_BYTES_PER_POINT_STEP.values()) * B * P
+    total_algo = sum(ALGO_BYTES_PER_POINT_STEP[k] for k in kprof if k in ALGO_BYTES_PER_POINT_STEP) * B * P
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -425,7 +434,7 @@ def main():
         "clocks": clocks.summary(),
         "plan_ms": plan_ms,
         "parity": {"forward_residual_type5": resid5, "forward_residual_type4": resid4},
-        "kernels_ms_per_step": {k: v[1] / args.steps for k, v in sorted(kprof.items(), key=lambda kv: -kv[1][1])},
+        "kernels_ms_per_step": {k: v[1] / args.steps for k, v in sorted(kernels_raw.items(), key=lambda kv: -kv[1][1])},
         "kernel_roofline": per_kernel_roofline,
         "step_roofline": {"algorithmic_bytes_per_step": total_algo,
                           "achieved_GBps": total_algo / (ms / args.steps / 1e3) / 1e9 / world,

@@ -734,12 +734,16 @@ int gather_fallback(const GridDev& g, int64_t n, const Window& win, const double
 // k_gather_b (host passes `fallback` so those blocks are recomputed there).
 constexpr int kGPSpan = 112;
 
-template <bool OUT_BM, int SUBM>  // SUBM: 0 none, 1 batch-minor, 2 signal-major
-__global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_p(
+// SIG signals per group (16 or 32).  With SIG = 16 the two half-warps take
+// 4 nodes each of the warp's 8 (same cells, broadcast reads), which halves
+// the staging tile so 4 CTAs fit per SM.
+template <bool OUT_BM, int SUBM, int SIG>  // SUBM: 0 none, 1 batch-minor, 2 signal-major
+__global__ void __launch_bounds__(kGatherWarps * 32, SIG == 16 ? 4 : 2) k_gather_p(
     const double* __restrict__ ts, const int* __restrict__ perm, int64_t Q, int64_t n, double alpha, GaussTab G,
     const double2* __restrict__ H, int64_t H_ld, int64_t batch, NodeFactor nf, const double2* __restrict__ sub,
     int64_t sub_ld, int mode, double2* __restrict__ out, int64_t out_ld, int ngroups, int* __restrict__ overflow) {
-  constexpr int SIG = 32;
+  constexpr int HALVES = 32 / SIG, NPL = kNPW / HALVES;
+  static_assert(kGatherNodes == 32, "one node per lane in the signal-major staging");
   extern __shared__ __align__(16) unsigned char smraw[];
   double2* Y = reinterpret_cast<double2*>(smraw);                     // [kGPSpan][SIG]
   double* WT = reinterpret_cast<double*>(Y + kGPSpan * SIG);           // [warps][kWTSpan][8]
@@ -751,18 +755,15 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_p(
   __shared__ int s_pq[kGatherNodes];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sl = lane % SIG, hf = lane / SIG;
   const int64_t q0 = (int64_t)blockIdx.x * kGatherNodes;
   const int nq = (int)min((int64_t)kGatherNodes, Q - q0);
   if (tid < kGatherNodes) {
-    int c = 0;
-    double f = 0.0;
     const int e = tid < nq ? tid : nq - 1;
     const double t = ts[q0 + e];
     const NodeGeo geo = node_geo(t, (double)n);
-    c = geo.i0;
-    f = tid < nq ? geo.f : 0.0;
-    s_c0[tid] = c;
-    s_f[tid] = f;
+    s_c0[tid] = geo.i0;
+    s_f[tid] = tid < nq ? geo.f : 0.0;
     if (tid < nq) {
       s_fac[tid] = factor_at(nf, q0 + tid, t);
       s_pq[tid] = perm[q0 + tid];
@@ -790,62 +791,66 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_p(
   }
   __syncwarp();
   const int ni = (int)n;
+  // signal-major operands: this thread's node (lane) and first signal (warp)
+  const int64_t my_off = (int64_t)warp * Q + (lane < nq ? s_pq[lane] : 0);
+  const double2* sb_src = sub + my_off;
   auto stage = [&](int64_t g) {
     const int64_t b0 = g * SIG;
-    const bool ok = b0 + lane < batch;
-    const double2* col = H + b0 + (ok ? lane : 0);
-    for (int c = warp; c < len; c += kGatherWarps) {
+    const bool ok = b0 + sl < batch;
+    const double2* col = H + b0 + (ok ? sl : 0);
+    for (int c = warp * HALVES + hf; c < len; c += kGatherWarps * HALVES) {
       int cell = cs + c;
       cell = cell < 0 ? cell + ni : (cell >= ni ? cell - ni : cell);
-      cp_async16(&Y[c * SIG + lane], col + (int64_t)cell * H_ld, ok);
+      cp_async16(&Y[c * SIG + sl], col + (int64_t)cell * H_ld, ok);
     }
-    if (SUBM == 2 && mode != 0) {
-      for (int sig = warp; sig < SIG; sig += kGatherWarps) {
-        const int64_t b = b0 + sig;
-        const bool okb = b < batch;
-        for (int e = lane; e < nq; e += 32)
-          cp_async16(&Sb[e * SIG + swz(sig, e)], sub + (okb ? b : 0) * Q + s_pq[e], okb);
+    if (SUBM == 2 && mode != 0) {  // node = lane, signals warp + 4k: one base pointer, stride 4Q
+#pragma unroll
+      for (int k = 0; k < SIG / kGatherWarps; k++) {
+        const int sig = warp + kGatherWarps * k;
+        const bool okb = b0 + sig < batch && lane < nq;
+        cp_async16(&Sb[lane * SIG + swz(sig, lane)], sb_src + (okb ? (b0 + kGatherWarps * k) * Q : 0), okb);
       }
     }
     cp_async_commit();
   };
   int64_t g = blockIdx.y;
   if (g < ngroups) stage(g);
-  const double2* __restrict__ yw = Y + (w_lo - cs) * SIG + lane;
-  const double2* __restrict__ wr0 = reinterpret_cast<const double2*>(wt);
+  const double2* __restrict__ yw = Y + (w_lo - cs) * SIG + sl;
+  const double2* __restrict__ wr0 = reinterpret_cast<const double2*>(wt) + hf * (NPL / 2);
+  const int e0 = warp * kNPW + hf * NPL;  // node of acc[0]
   for (; g < ngroups; g += gridDim.y) {
     const int64_t b0 = g * SIG;
     cp_async_wait_group<0>();
     __syncthreads();
-    double2 acc[kNPW];
+    double2 acc[NPL];
 #pragma unroll
-    for (int i = 0; i < kNPW; i++) acc[i] = make_double2(0.0, 0.0);
+    for (int i = 0; i < NPL; i++) acc[i] = make_double2(0.0, 0.0);
 #pragma unroll 4
     for (int i = 0; i < wl; i++) {
       const double2 y = yw[i * SIG];
       const double2* wr = wr0 + i * (kNPW / 2);
 #pragma unroll
-      for (int i2 = 0; i2 < kNPW / 2; i2++) {
+      for (int i2 = 0; i2 < NPL / 2; i2++) {
         const double2 w = wr[i2];
         caxpy(acc[2 * i2], w.x, y);
         caxpy(acc[2 * i2 + 1], w.y, y);
       }
     }
-    double2 sb_in[kNPW];
+    double2 sb_in[NPL];
     if (SUBM == 2 && mode != 0) {
 #pragma unroll
-      for (int i = 0; i < kNPW; i++) {
-        const int e = warp * kNPW + i;
-        sb_in[i] = e < nq ? Sb[e * SIG + swz(lane, e)] : make_double2(0.0, 0.0);
+      for (int i = 0; i < NPL; i++) {
+        const int e = e0 + i;
+        sb_in[i] = e < nq ? Sb[e * SIG + swz(sl, e)] : make_double2(0.0, 0.0);
       }
     }
     __syncthreads();  // Y (and Sb) consumed: prefetch the next group during the epilogue
     if (g + gridDim.y < ngroups) stage(g + gridDim.y);
     if constexpr (OUT_BM) {
-      const int64_t b = b0 + lane;
+      const int64_t b = b0 + sl;
 #pragma unroll
-      for (int i = 0; i < kNPW; i++) {
-        const int e = warp * kNPW + i;
+      for (int i = 0; i < NPL; i++) {
+        const int e = e0 + i;
         if (e >= nq || b >= out_ld) continue;
         double2 v = cmul(acc[i], s_fac[e]);
         const int64_t pq = s_pq[e];
@@ -857,20 +862,21 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_p(
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < kNPW; i++) {
-        const int e = warp * kNPW + i;
+      for (int i = 0; i < NPL; i++) {
+        const int e = e0 + i;
         double2 v = cmul(acc[i], e < nq ? s_fac[e] : make_double2(0.0, 0.0));
-        if (mode != 0 && e < nq && b0 + lane < batch) {
-          const double2 sv = SUBM == 1 ? sub[(int64_t)s_pq[e] * sub_ld + b0 + lane] : sb_in[i];
+        if (mode != 0 && e < nq && b0 + sl < batch) {
+          const double2 sv = SUBM == 1 ? sub[(int64_t)s_pq[e] * sub_ld + b0 + sl] : sb_in[i];
           v = mode == 1 ? csub(v, sv) : csub(sv, v);
         }
-        O[e * SIG + swz(lane, e)] = v;
+        O[e * SIG + swz(sl, e)] = v;
       }
       __syncthreads();
-      for (int idx = tid; idx < kGatherNodes * SIG; idx += blockDim.x) {
-        const int e = idx & (kGatherNodes - 1), sig = idx / kGatherNodes;
-        const int64_t b = b0 + sig;
-        if (b < batch && e < nq) out[b * Q + s_pq[e]] = O[e * SIG + swz(sig, e)];
+      double2* dst = out + my_off + b0 * Q;
+#pragma unroll
+      for (int k = 0; k < SIG / kGatherWarps; k++) {
+        const int sig = warp + kGatherWarps * k;
+        if (b0 + sig < batch && lane < nq) dst[(int64_t)kGatherWarps * k * Q] = O[lane * SIG + swz(sig, lane)];
       }
     }
   }
@@ -885,29 +891,34 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
                       NodeFactor f, const double2* sub, int64_t sub_ld, int mode, double2* out, int64_t out_ld,
                       cudaStream_t st) {
   if (!sub) mode = 0;
+  static const bool wide = getenv("NFFT45_GATHER_SIG32") != nullptr;  // A/B switch
+  const int SIG = wide ? 32 : 16;
   const int64_t nblk = ceil_div(g.Q, kGatherNodes);
-  const int ngroups = (int)ceil_div(out_ld ? out_ld : batch, 32);
+  const int ngroups = (int)ceil_div(out_ld ? out_ld : batch, SIG);
   const int slices = (int)std::min<int64_t>(ngroups, std::max<int64_t>(1, ceil_div(4 * 148, nblk)));
   int* overflow = nullptr;
   NFFT_CUDA(cudaMallocAsync(&overflow, sizeof(int) * nblk, st));
   LAUNCH(k_overflow_clear, (unsigned)ceil_div(nblk, 256), 256, 0, st, overflow, nblk);
   const int subm = mode == 0 ? 0 : (sub_ld ? 1 : 2);
-  size_t smem = (size_t)kGPSpan * 32 * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8 +
-                (subm == 2 ? (size_t)kGatherNodes * 32 * 16 : 0) + (out_ld ? 0 : (size_t)kGatherNodes * 32 * 16);
+  size_t smem = (size_t)kGPSpan * SIG * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8 +
+                (subm == 2 ? (size_t)kGatherNodes * SIG * 16 : 0) + (out_ld ? 0 : (size_t)kGatherNodes * SIG * 16);
   dim3 grid((unsigned)nblk, (unsigned)slices);
   GaussTab G = gauss_tab(win);
-#define NFFT_GP_LAUNCH(OBM, SM_)                                                                              \
+#define NFFT_GP_LAUNCH(OBM, SM_, S_)                                                                           \
   {                                                                                                          \
-    auto gather_p = k_gather_p<OBM, SM_>;                                                                    \
+    auto gather_p = k_gather_p<OBM, SM_, S_>;                                                                \
     NFFT_CUDA(cudaFuncSetAttribute(gather_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
     LAUNCH(gather_p, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, H_ld, batch, f,  \
            sub, sub_ld, mode, out, out_ld, ngroups, overflow);                                               \
   }
-  if (out_ld) {
-    if (subm == 0) NFFT_GP_LAUNCH(true, 0) else if (subm == 1) NFFT_GP_LAUNCH(true, 1) else NFFT_GP_LAUNCH(true, 2)
+#define NFFT_GP_SUB(OBM, S_) \
+  if (subm == 0) NFFT_GP_LAUNCH(OBM, 0, S_) else if (subm == 1) NFFT_GP_LAUNCH(OBM, 1, S_) else NFFT_GP_LAUNCH(OBM, 2, S_)
+  if (SIG == 16) {
+    if (out_ld) NFFT_GP_SUB(true, 16) else NFFT_GP_SUB(false, 16)
   } else {
-    if (subm == 0) NFFT_GP_LAUNCH(false, 0) else if (subm == 1) NFFT_GP_LAUNCH(false, 1) else NFFT_GP_LAUNCH(false, 2)
+    if (out_ld) NFFT_GP_SUB(true, 32) else NFFT_GP_SUB(false, 32)
   }
+#undef NFFT_GP_SUB
 #undef NFFT_GP_LAUNCH
   // blocks that overflowed the staging buffers: recompute them with the chunked kernel
   NFFT_CHECK(gather_fallback(g, n, win, H, batch, f, sub, mode, out, st, H_ld, sub_ld, out_ld, overflow));
