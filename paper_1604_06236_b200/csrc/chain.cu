@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, C>(), 2) kc_band(
   auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, C, true>(i, c)]; };
   auto st2 = [&](int k1, int c, double2 v) { U[bi * P + (int64_t)k1 * M + r0 + c] = v; };
   const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, r0, -1};
-  fast_tile_fft_smem<M, C, +1, true>(sm, ld2, st2, twC, pt);
+  fast_tile_fft_smem<M, C, +1, true, HalfTr<M>>(sm, ld2, st2, twC, pt);
 }
 
 // K4 / K2': rows k1' of U (length M) -> row IFFT_P -> * ks[k1' + M k2'] ->
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, C>(), 2) kc_pad(
     sm[sidx<NC, C, true>(n1, c)] = v;
     sm[sidx<NC, C, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
   };
-  fast_tile_fft<M, C, -1, true>(sm, ld1, st1, twR);
+  fast_tile_fft<M, C, -1, true, HalfTr<M>>(sm, ld1, st1, twR);
   __syncthreads();
   auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, C, true>(i, c)]; };
   auto st2 = [&](int k1, int c, double2 v) { Y[bi * n + (int64_t)k1 * M + r0 + c] = v; };
@@ -244,7 +244,7 @@ struct Chain {
     constexpr size_t smem = fast_smem<2 * M, C>();
     NFFT_CHECK(chain_attr(chain_band, smem));
     constexpr int T = fast_threads<2 * M, C>();
-    const int64_t Q = P / last_stride<M>();
+    const int64_t Q = P / last_stride<M, HalfTr<M>>();
     int status = NFFT45_OK;
     const double2* twQ = q_table(Q, st, &status);
     if (!twQ) return status;

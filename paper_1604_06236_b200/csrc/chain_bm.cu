@@ -15,6 +15,7 @@
 // Stage semantics are those of chain.cu (inverse.py:101-143, forward.py:26-102).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "fft_fast.cuh"
 #include "ops.cuh"
@@ -23,6 +24,7 @@ namespace nfft45 {
 
 namespace {
 constexpr int kSig = 8;  // signals per tile (batch-minor kernels)
+
 
 __device__ __forceinline__ double2 rsc(double2 v, double s) { return make_double2(v.x * s, v.y * s); }
 
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, SG>(), (SG < 8 ? 3 : 2)) k
   auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, SG, true>(i, c)]; };
   auto st2 = [&](int k1p, int c, double2 v) { U[((int64_t)k1p * M + k1) * Bp + b0 + c] = v; };
   const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, k1, 0};
-  fast_tile_fft_smem<M, SG, +1, true>(sm, ld2, st2, twC, pt);
+  fast_tile_fft_smem<M, SG, +1, true, HalfTr<M>>(sm, ld2, st2, twC, pt);
 }
 
 // row IFFT_P (row r) -> * ks -> column FFT_P (column r) -> W_P^{-r k} -> Z.
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, SG>(), (SG < 8 ? 3 : 2)) k
       sm[sidx<NC, SG, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
     }
   };
-  fast_tile_fft<M, SG, -1, true>(sm, ld1, st1, twR);
+  fast_tile_fft<M, SG, -1, true, HalfTr<M>>(sm, ld1, st1, twR);
   __syncthreads();
   auto st2 = [&](int k, int c, double2 v) { Y[((int64_t)k * M + r) * Bp + b0 + c] = v; };
   const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r, 0};
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 1) kbm_pad_p(
         sm[sidx<NC, kSig, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
       }
     };
-    fast_tile_fft<M, kSig, -1, true>(sm, ld1, st1, twR);
+    fast_tile_fft<M, kSig, -1, true, HalfTr<M>>(sm, ld1, st1, twR);
     __syncthreads();
     auto st2 = [&](int k, int c, double2 v) { Y[((int64_t)k * M + r) * Bp + b0 + c] = v; };
     const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r, 0};
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 1) kbm_band_p(
     auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, kSig, true>(i, c)]; };
     auto st2 = [&](int k1p, int c, double2 v) { U[((int64_t)k1p * M + k1) * Bp + b0 + c] = v; };
     const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, k1, 0};
-    fast_tile_fft_smem<M, kSig, +1, true>(sm, ld2, st2, twC, pt);
+    fast_tile_fft_smem<M, kSig, +1, true, HalfTr<M>>(sm, ld2, st2, twC, pt);
   };
   persistent_tiles<NR>(M * groups, buf0, buf1, src, body);
 }
@@ -411,7 +413,7 @@ struct ChainBM {
 
   int band(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub) {
     constexpr int T = fast_threads<2 * M, kSig>();
-    const int64_t Q = P / last_stride<M>();
+    const int64_t Q = P / last_stride<M, HalfTr<M>>();  // the column IFFT_P runs the HalfTr schedule
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
     constexpr size_t smem_p = fast_smem<2 * M, kSig>() + 16 + 2 * sizeof(double2) * 2 * M * kSig;

@@ -13,6 +13,8 @@
 // and JF (butterfly-fast lanes, for row-contiguous layouts).
 #pragma once
 
+#include <type_traits>
+
 #include "fft.cuh"
 
 namespace nfft45 {
@@ -39,6 +41,29 @@ struct FastTraits {
     return (!pow2 && p == 0) ? 3 : ((rem && p == (pow2 ? 0 : 1)) ? (1 << rem) : big);
   }
 };
+
+// 8 elements per thread, radix-8 passes (power-of-two N only): twice the
+// threads of FastTraits<N> for the same tile, one more pass.  Used where a
+// chain kernel's CTA is sized for a 2N-point FFT and the N-point stage
+// would otherwise leave half the threads idle.
+template <int N>
+struct FastTraitsE8 {
+  static_assert(is_pow2_c(N), "radix-8 schedule is for powers of two");
+  static constexpr bool pow2 = true;
+  static constexpr int E = 8;
+  static constexpr int a = log2_c(N);
+  static constexpr int rem = a % 3;
+  static constexpr int nbig = a / 3;
+  static constexpr int np = (rem ? 1 : 0) + nbig;
+  __host__ __device__ static constexpr int radix(int p) { return (rem && p == 0) ? (1 << rem) : 8; }
+};
+
+// The M-point stage of a band / pad chain kernel runs in a CTA sized for the
+// 2M-point FFT: with 8 elements per thread (radix-8 schedule) it uses all of
+// its threads.  Signal-major and batch-minor chains use the same schedule,
+// so batched and per-signal results stay bitwise identical.
+template <int M>
+using HalfTr = std::conditional_t<is_pow2_c(M), FastTraitsE8<M>, FastTraits<M>>;
 
 template <int S>
 __device__ __forceinline__ void bfly16(double2* v) {
@@ -175,10 +200,9 @@ struct FourStepTw {
 // with threadIdx.x >= T (a CTA sized for a bigger FFT of a chain) idle but
 // still meet every barrier.  SYNC0: the first pass reads shared memory that
 // its own stores overwrite (chain kernels), so it needs a barrier too.
-template <int N, int C, int S, bool CF, bool SYNC0, int P, int Ns, class Ld, class St, class PT>
+template <int N, int C, int S, bool CF, bool SYNC0, int P, int Ns, class Tr, class Ld, class St, class PT>
 __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
                                             const PT& pt) {
-  using Tr = FastTraits<N>;
   constexpr int E = Tr::E;
   constexpr int R = Tr::radix(P);
   constexpr int T = N * C / E;
@@ -230,22 +254,22 @@ __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St&
   }
   if constexpr (!LAST) {
     __syncthreads();
-    fast_passes<N, C, S, CF, SYNC0, P + 1, Ns * R>(sm, ld, st, tw, pt);
+    fast_passes<N, C, S, CF, SYNC0, P + 1, Ns * R, Tr>(sm, ld, st, tw, pt);
   }
 }
 
-template <int N, int C, int S, bool CF, class Ld, class St, class PT = NoPostTw>
+template <int N, int C, int S, bool CF, class Tr = FastTraits<N>, class Ld, class St, class PT = NoPostTw>
 __device__ __forceinline__ void fast_tile_fft(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
                                               const PT& pt = PT()) {
-  fast_passes<N, C, S, CF, false, 0, 1>(sm, ld, st, tw, pt);
+  fast_passes<N, C, S, CF, false, 0, 1, Tr>(sm, ld, st, tw, pt);
 }
 
 // Variant whose first pass reads the tile from shared memory (via `ld`)
 // that later passes overwrite.
-template <int N, int C, int S, bool CF, class Ld, class St, class PT = NoPostTw>
+template <int N, int C, int S, bool CF, class Tr = FastTraits<N>, class Ld, class St, class PT = NoPostTw>
 __device__ __forceinline__ void fast_tile_fft_smem(double2* sm, const Ld& ld, const St& st,
                                                    const double2* __restrict__ tw, const PT& pt = PT()) {
-  fast_passes<N, C, S, CF, true, 0, 1>(sm, ld, st, tw, pt);
+  fast_passes<N, C, S, CF, true, 0, 1, Tr>(sm, ld, st, tw, pt);
 }
 
 // Run passes P0.. of a tile FFT whose earlier passes were produced directly
@@ -254,12 +278,12 @@ template <int N, int C, int S, bool CF, int P0, int NS0, class St, class PT = No
 __device__ __forceinline__ void fast_tile_fft_from(double2* sm, const St& st, const double2* __restrict__ tw,
                                                    const PT& pt = PT()) {
   auto no_ld = [](int, int) -> double2 { return make_double2(0.0, 0.0); };
-  fast_passes<N, C, S, CF, false, P0, NS0>(sm, no_ld, st, tw, pt);
+  fast_passes<N, C, S, CF, false, P0, NS0, FastTraits<N>>(sm, no_ld, st, tw, pt);
 }
 
 // the last-pass stride (= N / radix of the last pass) of a fast tile FFT
-template <int N>
-__host__ __device__ constexpr int last_stride() { return N / FastTraits<N>::radix(FastTraits<N>::np - 1); }
+template <int N, class Tr = FastTraits<N>>
+__host__ __device__ constexpr int last_stride() { return N / Tr::radix(Tr::np - 1); }
 
 template <int N, int C>
 __host__ __device__ constexpr int fast_threads() { return N * C / FastTraits<N>::E; }

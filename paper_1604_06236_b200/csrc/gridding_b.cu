@@ -738,7 +738,7 @@ constexpr int kGPSpan = 112;
 // 4 nodes each of the warp's 8 (same cells, broadcast reads), which halves
 // the staging tile so 4 CTAs fit per SM.
 template <bool OUT_BM, int SUBM, int SIG>  // SUBM: 0 none, 1 batch-minor, 2 signal-major
-__global__ void __launch_bounds__(kGatherWarps * 32, SIG == 16 ? 4 : 2) k_gather_p(
+__global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 ? 4 : 5)) k_gather_p(
     const double* __restrict__ ts, const int* __restrict__ perm, int64_t Q, int64_t n, double alpha, GaussTab G,
     const double2* __restrict__ H, int64_t H_ld, int64_t batch, NodeFactor nf, const double2* __restrict__ sub,
     int64_t sub_ld, int mode, double2* __restrict__ out, int64_t out_ld, int ngroups, int* __restrict__ overflow) {
@@ -891,8 +891,11 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
                       NodeFactor f, const double2* sub, int64_t sub_ld, int mode, double2* out, int64_t out_ld,
                       cudaStream_t st) {
   if (!sub) mode = 0;
-  static const bool wide = getenv("NFFT45_GATHER_SIG32") != nullptr;  // A/B switch
-  const int SIG = wide ? 32 : 16;
+  static const int SIG = [] {  // signals per group (A/B switch NFFT45_GATHER_SIG = 8 | 16 | 32)
+    const char* e = getenv("NFFT45_GATHER_SIG");
+    const int v = e ? atoi(e) : 16;
+    return v == 8 || v == 32 ? v : 16;
+  }();
   const int64_t nblk = ceil_div(g.Q, kGatherNodes);
   const int ngroups = (int)ceil_div(out_ld ? out_ld : batch, SIG);
   const int slices = (int)std::min<int64_t>(ngroups, std::max<int64_t>(1, ceil_div(4 * 148, nblk)));
@@ -915,6 +918,8 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
   if (subm == 0) NFFT_GP_LAUNCH(OBM, 0, S_) else if (subm == 1) NFFT_GP_LAUNCH(OBM, 1, S_) else NFFT_GP_LAUNCH(OBM, 2, S_)
   if (SIG == 16) {
     if (out_ld) NFFT_GP_SUB(true, 16) else NFFT_GP_SUB(false, 16)
+  } else if (SIG == 8) {
+    if (out_ld) NFFT_GP_SUB(true, 8) else NFFT_GP_SUB(false, 8)
   } else {
     if (out_ld) NFFT_GP_SUB(true, 32) else NFFT_GP_SUB(false, 32)
   }
