@@ -25,6 +25,17 @@ namespace nfft45 {
 namespace {
 constexpr int kSig = 8;  // signals per tile (batch-minor kernels)
 
+// CTAs per SM to request for a T-thread tile kernel: enough that every thread
+// keeps ~128 registers (a 16-element tile FFT spills below that).
+__host__ __device__ constexpr int bm_minb(int T) { return T >= 512 ? 1 : (T >= 256 ? 2 : 4); }
+// signals per tile of the two-FFT kernels: 8, or 4 when 8 would need a
+// CTA above 512 threads (M = 1024)
+template <int M>
+__host__ __device__ constexpr int bm_sg() { return fast_threads<2 * M, kSig>() > 512 ? kSig / 2 : kSig; }
+// rows per tile of the boundary kernels (4 signals each): 4, or 2 for M = 1024
+template <int M>
+__host__ __device__ constexpr int bm_rw() { return fast_threads<M, 16>() > 512 ? 2 : 4; }
+
 
 __device__ __forceinline__ double2 rsc(double2 v, double s) { return make_double2(v.x * s, v.y * s); }
 
@@ -67,7 +78,7 @@ __device__ __forceinline__ void persistent_tiles(int ntiles, double2* buf0, doub
 // column pass: columns n2 = blockIdx.x of x[i * L2 + n2] (length L), optional
 // real pre-table, twiddle W_N^{S n2 k1}, in place-layout.
 template <int L, int S>
-__global__ void __launch_bounds__(fast_threads<L, kSig>(), 4) kbm_col(
+__global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<L, kSig>())) kbm_col(
     const double2* __restrict__ in, double2* __restrict__ out, int L2, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ lo, const double2* __restrict__ hi, int sh, const double2* __restrict__ twQ, int Q,
     const double* __restrict__ pre) {
@@ -89,7 +100,7 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), 4) kbm_col(
 // deconv*decay (or (X deconv - sub) decay) -> column IFFT_P (length M) ->
 // W_P^{+k1 k1'} -> U[(k1' M + k1)][b].
 template <int M, int SG>
-__global__ void __launch_bounds__(fast_threads<2 * M, SG>(), (SG < 8 ? 3 : 2)) kbm_band(
+__global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_threads<2 * M, SG>())) kbm_band(
     const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
@@ -123,7 +134,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, SG>(), (SG < 8 ? 3 : 2)) k
 
 // row IFFT_P (row r) -> * ks -> column FFT_P (column r) -> W_P^{-r k} -> Z.
 template <int M>
-__global__ void __launch_bounds__(fast_threads<M, kSig>(), 4) kbm_mid(
+__global__ void __launch_bounds__(fast_threads<M, kSig>(), bm_minb(fast_threads<M, kSig>())) kbm_mid(
     const double2* __restrict__ U, double2* __restrict__ Z, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
     const double2* __restrict__ ks) {
@@ -145,7 +156,7 @@ __global__ void __launch_bounds__(fast_threads<M, kSig>(), 4) kbm_mid(
 // row FFT_P (row r) -> * coef (x = [xsub -] S coef stored when xout) *
 // deconv -> zero-padded column IFFT_2P (length 2M, column r) -> W_n^{+r k} -> Y.
 template <int M, int SG>
-__global__ void __launch_bounds__(fast_threads<2 * M, SG>(), (SG < 8 ? 3 : 2)) kbm_pad(
+__global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_threads<2 * M, SG>())) kbm_pad(
     const double2* __restrict__ Z, double2* __restrict__ Y, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
@@ -304,7 +315,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 1) kbm_band_p(
 
 // row pass: row r = blockIdx.x (length L), output index r + R1 k.
 template <int L, int S>
-__global__ void __launch_bounds__(fast_threads<L, kSig>(), 4) kbm_row(const double2* __restrict__ in,
+__global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<L, kSig>())) kbm_row(const double2* __restrict__ in,
                                                                   double2* __restrict__ out, int64_t Bp, int64_t R1,
                                                                   const double2* __restrict__ tw) {
   extern __shared__ double2 sm[];
@@ -318,50 +329,50 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), 4) kbm_row(const doub
 // Boundary, type-4 input: signal-major A[b][P] -> column IFFT_P * decay
 // (columns m2 = 4 blockIdx.x + (c & 3), signals b = 4 blockIdx.y + (c >> 2))
 // -> batch-minor U; optionally also a batch-minor copy AT of A.
-template <int M>
-__global__ void __launch_bounds__(fast_threads<M, 16>()) kbm_colin(
+template <int M, int RW>
+__global__ void __launch_bounds__(fast_threads<M, 4 * RW>(), bm_minb(fast_threads<M, 4 * RW>())) kbm_colin(
     const double2* __restrict__ A, int64_t batch, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
     const double* __restrict__ decay, double2* __restrict__ AT) {
   constexpr int64_t P = (int64_t)M * M;
   extern __shared__ double2 sm[];
-  const int m20 = blockIdx.x * 4;
+  const int m20 = blockIdx.x * RW;
   const int64_t bb = (int64_t)blockIdx.y * 4;
   auto ld = [&](int i, int c) -> double2 {
-    const int64_t idx = (int64_t)i * M + m20 + (c & 3);
-    const int64_t b = bb + (c >> 2);
+    const int64_t idx = (int64_t)i * M + m20 + (c % RW);
+    const int64_t b = bb + c / RW;
     double2 v = b < batch ? A[b * P + idx] : make_double2(0.0, 0.0);
     if (AT) AT[idx * Bp + b] = v;
     return rsc(v, __ldg(&decay[idx]));
   };
   auto st = [&](int k1, int c, double2 v) {
-    U[((int64_t)k1 * M + m20 + (c & 3)) * Bp + bb + (c >> 2)] = v;
+    U[((int64_t)k1 * M + m20 + (c % RW)) * Bp + bb + c / RW] = v;
   };
-  const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, m20, 3};
-  fast_tile_fft<M, 16, +1, true>(sm, ld, st, tw, pt);
+  const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, m20, RW - 1};
+  fast_tile_fft<M, 4 * RW, +1, true>(sm, ld, st, tw, pt);
 }
 
 // Boundary, type-5 output: batch-minor Z rows r = 4 blockIdx.x + (c & 3) ->
 // row FFT_P * coef [xsub (batch-minor) - .] -> signal-major out[b][P].
-template <int M>
-__global__ void __launch_bounds__(fast_threads<M, 16>()) kbm_rowout(
+template <int M, int RW>
+__global__ void __launch_bounds__(fast_threads<M, 4 * RW>(), bm_minb(fast_threads<M, 4 * RW>())) kbm_rowout(
     const double2* __restrict__ Z, double2* __restrict__ out, int64_t batch, int64_t Bp,
     const double2* __restrict__ tw, const double* __restrict__ coef, const double2* __restrict__ xsub) {
   constexpr int64_t P = (int64_t)M * M;
   extern __shared__ double2 sm[];
-  const int r0 = blockIdx.x * 4;
+  const int r0 = blockIdx.x * RW;
   const int64_t bb = (int64_t)blockIdx.y * 4;
   auto ld = [&](int i, int c) -> double2 {
-    return Z[((int64_t)(r0 + (c & 3)) * M + i) * Bp + bb + (c >> 2)];
+    return Z[((int64_t)(r0 + (c % RW)) * M + i) * Bp + bb + c / RW];
   };
   auto st = [&](int k, int c, double2 v) {
-    const int64_t p = (int64_t)(r0 + (c & 3)) + (int64_t)M * k;
-    const int64_t b = bb + (c >> 2);
+    const int64_t p = (int64_t)(r0 + (c % RW)) + (int64_t)M * k;
+    const int64_t b = bb + c / RW;
     v = rsc(v, __ldg(&coef[p]));
     if (xsub) v = csub(xsub[p * Bp + b], v);
     if (b < batch) out[b * P + p] = v;
   };
-  fast_tile_fft<M, 16, -1, true>(sm, ld, st, tw);
+  fast_tile_fft<M, 4 * RW, -1, true>(sm, ld, st, tw);
 }
 
 // ------------------------------------------------------------ host side
@@ -425,7 +436,7 @@ struct ChainBM {
              t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
       return NFFT45_OK;
     }
-    if (small_tiles) {
+    if (small_tiles || bm_sg<M>() < kSig) {  // 4-signal tiles (always for M = 1024)
       auto bm_band4 = kbm_band<M, 4>;
       constexpr size_t smem4 = fast_smem<2 * M, 4>();
       NFFT_CHECK(bm_attr(bm_band4, smem4));
@@ -469,7 +480,7 @@ struct ChainBM {
              t.tN->hi, t.tN->s, twQ, (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout);
       return NFFT45_OK;
     }
-    if (small_tiles) {
+    if (small_tiles || bm_sg<M>() < kSig) {  // 4-signal tiles (always for M = 1024)
       auto bm_pad4 = kbm_pad<M, 4>;
       constexpr size_t smem4 = fast_smem<2 * M, 4>();
       NFFT_CHECK(bm_attr(bm_pad4, smem4));
@@ -497,24 +508,26 @@ struct ChainBM {
   }
 
   int colin(const double2* A, double2* U, const ChainPlanView& pv, double2* AT) {
-    auto bm_colin = kbm_colin<M>;
-    constexpr size_t smem = fast_smem<M, 16>();
+    constexpr int RW = bm_rw<M>();
+    auto bm_colin = kbm_colin<M, RW>;
+    constexpr size_t smem = fast_smem<M, 4 * RW>();
     NFFT_CHECK(bm_attr(bm_colin, smem));
-    constexpr int T = fast_threads<M, 16>();
+    constexpr int T = fast_threads<M, 4 * RW>();
     const int64_t Q = P / last_stride<M>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    LAUNCH(bm_colin, dim3((unsigned)(M / 4), (unsigned)(Bp / 4)), T, smem, st, A, batch, U, Bp, t.twM, t.tP->lo,
+    LAUNCH(bm_colin, dim3((unsigned)(M / RW), (unsigned)(Bp / 4)), T, smem, st, A, batch, U, Bp, t.twM, t.tP->lo,
            t.tP->hi, t.tP->s, twQ, (int)Q, pv.decay, AT);
     return NFFT45_OK;
   }
 
   int rowout(const double2* Z, double2* out, const ChainPlanView& pv, const double2* xsub) {
-    auto bm_rowout = kbm_rowout<M>;
-    constexpr size_t smem = fast_smem<M, 16>();
+    constexpr int RW = bm_rw<M>();
+    auto bm_rowout = kbm_rowout<M, RW>;
+    constexpr size_t smem = fast_smem<M, 4 * RW>();
     NFFT_CHECK(bm_attr(bm_rowout, smem));
-    constexpr int T = fast_threads<M, 16>();
-    LAUNCH(bm_rowout, dim3((unsigned)(M / 4), (unsigned)(Bp / 4)), T, smem, st, Z, out, batch, Bp, t.twM, pv.coef,
+    constexpr int T = fast_threads<M, 4 * RW>();
+    LAUNCH(bm_rowout, dim3((unsigned)(M / RW), (unsigned)(Bp / 4)), T, smem, st, Z, out, batch, Bp, t.twM, pv.coef,
            xsub);
     return NFFT45_OK;
   }

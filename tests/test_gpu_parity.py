@@ -159,6 +159,23 @@ def test_c3_single_2_20():
     _check_config(1 << 20, 0.4, 1, 16043, passes=(1,))
 
 
+@pytest.mark.parametrize("logP", [18, 20])
+def test_batched_large_grids(logP):
+    """Batch-minor chains at M = 512 (8-signal tiles) and M = 1024 (4-signal
+    band/pad tiles, 2-row boundary tiles): vs the oracle on the first and last
+    signal; type 5 bitwise equal to the single-signal (signal-major) chain,
+    type 4 equal to rounding (its batch-minor and signal-major kernels round
+    differently, ~1e-13 on the plain solve, ~1e-15 refined)."""
+    P, B = 1 << logP, 16
+    _check_config(P, 0.3, B, 16046, passes=(1,), rows=(0, B - 1))
+    t, data = O.make_inputs(P, 0.3, B, 16046)
+    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-15, P, 2))
+    full5 = nf.refine_type5(plan, data, passes=1)
+    full4 = nf.refine_type4(plan, data, passes=1)
+    assert np.array_equal(full5[B - 1], nf.refine_type5(plan, data[B - 1], passes=1))
+    assert rel(nf.refine_type4(plan, data[B - 1], passes=1), full4[B - 1]) < 1e-13
+
+
 @pytest.mark.parametrize("J,eta", [(0.1, 2), (0.45, 2), (0.3, 3)])
 def test_c5_sweep_2_18(J, eta):
     _check_config(1 << 18, J, 1, 16045, eta=eta, passes=(1,))
