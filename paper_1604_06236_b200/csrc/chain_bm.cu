@@ -46,6 +46,10 @@ __device__ __forceinline__ void cpa16(void* sdst, const void* gsrc) {
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void cpa8(void* sdst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
+}
 
 // Persistent tile loop with a double-buffered cp.async prefetch of each
 // tile's input (L rows x 8 signals, row-contiguous in the batch-minor
@@ -99,6 +103,10 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<
 // row FFT_2P (row k1 = blockIdx.x, length 2M) -> band p = k1 + M m1 with
 // deconv*decay (or (X deconv - sub) decay) -> column IFFT_P (length M) ->
 // W_P^{+k1 k1'} -> U[(k1' M + k1)][b].
+// Per-tile tables (deconv*decay, or deconv and decay plus the subtrahend
+// tile) are staged into shared memory with cp.async at entry; the copies fly
+// during the first FFT pass (CpAsyncWaitHook) instead of stalling the band
+// epilogue on L2 latency.
 template <int M, int SG>
 __global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_threads<2 * M, SG>())) kbm_band(
     const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
@@ -107,24 +115,39 @@ __global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_thread
     const double* __restrict__ dd, const double2* __restrict__ sub) {
   constexpr int NR = 2 * M;
   extern __shared__ double2 sm[];
+  double* s_t0 = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + fast_smem<NR, SG>());
+  double* s_t1 = s_t0 + M;
+  double2* s_sb = reinterpret_cast<double2*>(s_t1 + M);
   const int k1 = blockIdx.x;
   const int64_t b0 = (int64_t)blockIdx.y * SG;
+  for (int m1 = threadIdx.x; m1 < M; m1 += blockDim.x) {
+    const int64_t p = (int64_t)k1 + (int64_t)M * m1;
+    if (sub) {
+      cpa8(&s_t0[m1], &deconv[p]);
+      cpa8(&s_t1[m1], &decay[p]);
+    } else {
+      cpa8(&s_t0[m1], &dd[p]);
+    }
+  }
+  if (sub)
+    for (int e = threadIdx.x; e < M * SG; e += blockDim.x)
+      cpa16(&s_sb[e], &sub[((int64_t)k1 + (int64_t)M * (e / SG)) * Bp + b0 + e % SG]);
+  cpa_commit();
   auto ld1 = [&](int i, int c) -> double2 { return T[((int64_t)k1 * NR + i) * Bp + b0 + c]; };
   auto st1 = [&](int k2, int c, double2 v) {
     const int m1 = (k2 + M / 2) & (NR - 1);
     if (m1 < M) {
-      const int64_t p = (int64_t)k1 + (int64_t)M * m1;
       if (sub) {
-        v = rsc(v, __ldg(&deconv[p]));
-        v = csub(v, sub[p * Bp + b0 + c]);
-        v = rsc(v, __ldg(&decay[p]));
+        v = rsc(v, s_t0[m1]);
+        v = csub(v, s_sb[m1 * SG + c]);
+        v = rsc(v, s_t1[m1]);
       } else {
-        v = rsc(v, __ldg(&dd[p]));
+        v = rsc(v, s_t0[m1]);
       }
       sm[sidx<M, SG, true>(m1, c)] = v;
     }
   };
-  fast_tile_fft<NR, SG, -1, true>(sm, ld1, st1, twR);
+  fast_tile_fft<NR, SG, -1, true>(sm, ld1, st1, twR, NoPostTw(), CpAsyncWaitHook());
   __syncthreads();
   auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, SG, true>(i, c)]; };
   auto st2 = [&](int k1p, int c, double2 v) { U[((int64_t)k1p * M + k1) * Bp + b0 + c] = v; };
@@ -139,13 +162,14 @@ __global__ void __launch_bounds__(fast_threads<M, kSig>(), bm_minb(fast_threads<
     const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
     const double2* __restrict__ ks) {
   extern __shared__ double2 sm[];
+  double2* s_ks = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + fast_smem<M, kSig>());
   const int r = blockIdx.x;
   const int64_t b0 = (int64_t)blockIdx.y * kSig;
+  for (int k2 = threadIdx.x; k2 < M; k2 += blockDim.x) cpa16(&s_ks[k2], &ks[(int64_t)r + (int64_t)M * k2]);
+  cpa_commit();
   auto ld1 = [&](int i, int c) -> double2 { return U[((int64_t)r * M + i) * Bp + b0 + c]; };
-  auto st1 = [&](int k2, int c, double2 v) {
-    sm[sidx<M, kSig, true>(k2, c)] = cmul(v, __ldg(&ks[(int64_t)r + (int64_t)M * k2]));
-  };
-  fast_tile_fft<M, kSig, +1, true>(sm, ld1, st1, tw);
+  auto st1 = [&](int k2, int c, double2 v) { sm[sidx<M, kSig, true>(k2, c)] = cmul(v, s_ks[k2]); };
+  fast_tile_fft<M, kSig, +1, true>(sm, ld1, st1, tw, NoPostTw(), CpAsyncWaitHook());
   __syncthreads();
   auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, kSig, true>(i, c)]; };
   auto st2 = [&](int k, int c, double2 v) { Z[((int64_t)k * M + r) * Bp + b0 + c] = v; };
@@ -164,18 +188,36 @@ __global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_thread
   constexpr int NC = 2 * M;
   constexpr bool kLead2 = FastTraits<NC>::radix(0) == 2;
   extern __shared__ double2 sm[];
+  double* s_t0 = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + fast_smem<NC, SG>());
+  double* s_t1 = s_t0 + M;
+  double2* s_xs = reinterpret_cast<double2*>(s_t1 + M);
   const int r = blockIdx.x;
   const int64_t b0 = (int64_t)blockIdx.y * SG;
+  // per-tile tables (and the xsub tile) staged with cp.async, waited for at
+  // the end of the first FFT pass
+  for (int k2 = threadIdx.x; k2 < M; k2 += blockDim.x) {
+    const int64_t p = (int64_t)r + (int64_t)M * k2;
+    if (xout) {
+      cpa8(&s_t0[k2], &coef[p]);
+      cpa8(&s_t1[k2], &deconv[p]);
+    } else {
+      cpa8(&s_t0[k2], &cd[p]);
+    }
+  }
+  if (xout && xsub)
+    for (int e = threadIdx.x; e < M * SG; e += blockDim.x)
+      cpa16(&s_xs[e], &xsub[((int64_t)r + (int64_t)M * (e / SG)) * Bp + b0 + e % SG]);
+  cpa_commit();
   auto ld1 = [&](int i, int c) -> double2 { return Z[((int64_t)r * M + i) * Bp + b0 + c]; };
   auto st1 = [&](int k2, int c, double2 v) {
     const int64_t p = (int64_t)r + (int64_t)M * k2;
     if (xout) {
-      v = rsc(v, __ldg(&coef[p]));
-      if (xsub) v = csub(xsub[p * Bp + b0 + c], v);
+      v = rsc(v, s_t0[k2]);
+      if (xsub) v = csub(s_xs[k2 * SG + c], v);
       xout[p * Bp + b0 + c] = v;
-      v = rsc(v, __ldg(&deconv[p]));
+      v = rsc(v, s_t1[k2]);
     } else {
-      v = rsc(v, __ldg(&cd[p]));
+      v = rsc(v, s_t0[k2]);
     }
     const int n1 = (k2 - M / 2) & (NC - 1);
     if constexpr (kLead2) {
@@ -196,7 +238,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_thread
       sm[sidx<NC, SG, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
     }
   };
-  fast_tile_fft<M, SG, -1, true, HalfTr<M>>(sm, ld1, st1, twR);
+  fast_tile_fft<M, SG, -1, true, HalfTr<M>>(sm, ld1, st1, twR, NoPostTw(), CpAsyncWaitHook());
   __syncthreads();
   auto st2 = [&](int k, int c, double2 v) { Y[((int64_t)k * M + r) * Bp + b0 + c] = v; };
   const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r, 0};
@@ -438,7 +480,7 @@ struct ChainBM {
     }
     if (small_tiles || bm_sg<M>() < kSig) {  // 4-signal tiles (always for M = 1024)
       auto bm_band4 = kbm_band<M, 4>;
-      constexpr size_t smem4 = fast_smem<2 * M, 4>();
+      const size_t smem4 = fast_smem<2 * M, 4>() + 2 * sizeof(double) * M + (sub ? sizeof(double2) * M * 4 : 0);
       NFFT_CHECK(bm_attr(bm_band4, smem4));
       constexpr int T4 = fast_threads<2 * M, 4>();
       LAUNCH(bm_band4, dim3((unsigned)M, groups * 2), T4, smem4, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi,
@@ -446,7 +488,7 @@ struct ChainBM {
       return NFFT45_OK;
     }
     auto bm_band = kbm_band<M, kSig>;
-    constexpr size_t smem = fast_smem<2 * M, kSig>();
+    const size_t smem = fast_smem<2 * M, kSig>() + 2 * sizeof(double) * M + (sub ? sizeof(double2) * M * kSig : 0);
     NFFT_CHECK(bm_attr(bm_band, smem));
     LAUNCH(bm_band, dim3((unsigned)M, groups), T, smem, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s,
            twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
@@ -455,7 +497,7 @@ struct ChainBM {
 
   int mid(const double2* U, double2* Z, const ChainPlanView& pv) {
     auto bm_mid = kbm_mid<M>;
-    constexpr size_t smem = fast_smem<M, kSig>();
+    constexpr size_t smem = fast_smem<M, kSig>() + sizeof(double2) * M;
     NFFT_CHECK(bm_attr(bm_mid, smem));
     constexpr int T = fast_threads<M, kSig>();
     const int64_t Q = P / last_stride<M>();
@@ -482,7 +524,7 @@ struct ChainBM {
     }
     if (small_tiles || bm_sg<M>() < kSig) {  // 4-signal tiles (always for M = 1024)
       auto bm_pad4 = kbm_pad<M, 4>;
-      constexpr size_t smem4 = fast_smem<2 * M, 4>();
+      const size_t smem4 = fast_smem<2 * M, 4>() + 2 * sizeof(double) * M + (xout && xsub ? sizeof(double2) * M * 4 : 0);
       NFFT_CHECK(bm_attr(bm_pad4, smem4));
       constexpr int T4 = fast_threads<2 * M, 4>();
       LAUNCH(bm_pad4, dim3((unsigned)M, groups * 2), T4, smem4, st, Z, Y, Bp, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s,
@@ -490,7 +532,7 @@ struct ChainBM {
       return NFFT45_OK;
     }
     auto bm_pad = kbm_pad<M, kSig>;
-    constexpr size_t smem = fast_smem<2 * M, kSig>();
+    const size_t smem = fast_smem<2 * M, kSig>() + 2 * sizeof(double) * M + (xout && xsub ? sizeof(double2) * M * kSig : 0);
     NFFT_CHECK(bm_attr(bm_pad, smem));
     LAUNCH(bm_pad, dim3((unsigned)M, groups), T, smem, st, Z, Y, Bp, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s, twQ,
            (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout);

@@ -196,13 +196,27 @@ struct FourStepTw {
   }
 };
 
+// Hook run by every thread at the end of the first pass, just before its
+// barrier: kernels that stage per-tile tables with cp.async at entry wait for
+// them here, so the copies overlap the first pass and are visible to the
+// last pass's storer.
+struct NoHook {
+  static constexpr bool kActive = false;
+  __device__ __forceinline__ void operator()() const {}
+};
+struct CpAsyncWaitHook {
+  static constexpr bool kActive = true;
+  __device__ __forceinline__ void operator()() const { asm volatile("cp.async.wait_all;\n" ::); }
+};
+
 // One pass; FIRST reads through `ld`, LAST writes through `st`.  Threads
 // with threadIdx.x >= T (a CTA sized for a bigger FFT of a chain) idle but
 // still meet every barrier.  SYNC0: the first pass reads shared memory that
 // its own stores overwrite (chain kernels), so it needs a barrier too.
-template <int N, int C, int S, bool CF, bool SYNC0, int P, int Ns, class Tr, class Ld, class St, class PT>
+template <int N, int C, int S, bool CF, bool SYNC0, int P, int Ns, class Tr, class Ld, class St, class PT,
+          class Hk = NoHook>
 __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
-                                            const PT& pt) {
+                                            const PT& pt, const Hk& hook = Hk()) {
   constexpr int E = Tr::E;
   constexpr int R = Tr::radix(P);
   constexpr int T = N * C / E;
@@ -227,7 +241,8 @@ __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St&
     }
   }
   }
-  if constexpr (!FIRST || SYNC0) __syncthreads();  // everyone has read before anyone overwrites
+  if constexpr (FIRST && LAST && Hk::kActive) hook();
+  if constexpr (!FIRST || SYNC0 || (LAST && Hk::kActive)) __syncthreads();  // everyone has read before anyone overwrites
   if (active) {
 #pragma unroll
   for (int u = 0; u < MB; u++) {
@@ -253,15 +268,17 @@ __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St&
   }
   }
   if constexpr (!LAST) {
+    if constexpr (FIRST && Hk::kActive) hook();
     __syncthreads();
     fast_passes<N, C, S, CF, SYNC0, P + 1, Ns * R, Tr>(sm, ld, st, tw, pt);
   }
 }
 
-template <int N, int C, int S, bool CF, class Tr = FastTraits<N>, class Ld, class St, class PT = NoPostTw>
+template <int N, int C, int S, bool CF, class Tr = FastTraits<N>, class Ld, class St, class PT = NoPostTw,
+          class Hk = NoHook>
 __device__ __forceinline__ void fast_tile_fft(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
-                                              const PT& pt = PT()) {
-  fast_passes<N, C, S, CF, false, 0, 1, Tr>(sm, ld, st, tw, pt);
+                                              const PT& pt = PT(), const Hk& hook = Hk()) {
+  fast_passes<N, C, S, CF, false, 0, 1, Tr>(sm, ld, st, tw, pt, hook);
 }
 
 // Variant whose first pass reads the tile from shared memory (via `ld`)
