@@ -120,6 +120,20 @@ int nfft45_type2_direct(const nfft45_grid* g, const double* S_dev, int64_t batch
 int nfft45_dft(const double* in_dev, double* out_dev, int64_t batch, int64_t N, int sign,
                void* stream);
 
+/* ------------------------------------------------------- CG baseline */
+
+/* cg_solve(grid, rhs, which, tol, max_iter, spread_width) — baselines.py:108-181.
+ * CGNR, unpreconditioned: each iteration applies the system matrix and its
+ * Hermitian transpose (one type-1 and one type-2 NFFT of width m).  kind 4:
+ * A = type1 (amplitudes -> spectrum), kind 5: A = type2 (coefficients ->
+ * samples).  rhs_dev, x_dev: [batch][P] device (P = grid size); every row runs
+ * its own recurrence.  Host outputs per row: iterations, converged (0/1),
+ * relres = ||r|| / ||b||, stalled (|A p| = 0 stop; may be NULL).  tol <= 0 or
+ * an unknown kind: INVALID_ARGUMENT. */
+int nfft45_cg_solve(const nfft45_grid* g, int kind, const double* rhs_dev, int64_t batch, double tol,
+                    int64_t max_iter, int m, double* x_dev, int64_t* iterations, int* converged,
+                    double* relres, int* stalled, void* stream);
+
 /* ------------------------------------------------- Lagrange quantities */
 
 /* compute_v_samples(grid, params) — lagrange.py:57-75. v_dev: complex [P]. */

@@ -195,6 +195,45 @@ def main(ref_root="/root/reference"):
     put("fixture_samples8", _read_vec(os.path.join(fx, "samples8.txt")))
     put("fixture_coeffs8", _read_vec(os.path.join(fx, "coeffs8_dense_solve.txt")))
 
+    # ---- baselines (baselines.py): CG runs with their iteration counts and
+    # flop reports, dense GE solutions.  Own generator: earlier arrays keep
+    # their values.
+    rng2 = np.random.default_rng(1604)
+
+    def randc2(n):
+        return rng2.standard_normal(n) + 1j * rng2.standard_normal(n)
+
+    cg_cases = [
+        ("cg4", 256, 17, "type4", 1e-14, None),
+        ("cg5", 64, 19, "type5", 1e-14, None),
+        ("cgcap", 128, 23, "type4", 1e-15, 2),
+        ("cgtol", 512, 29, "type4", 1e-10, None),
+    ]
+    for name, P, seed, which, tol, cap in cg_cases:
+        grid, a_true = R.generate_trial(P, seed)
+        b = R.nfft_type1_direct(grid, a_true, P) if which == "type4" else randc2(P)
+        fc = R.FlopCounter()
+        res = R.cg_solve(grid, b, which, tol=tol, max_iter=cap, flops=fc)
+        put(f"{name}_t", np.asarray(grid.instants))
+        put(f"{name}_b", b)
+        put(f"{name}_x", res.solution)
+        put(f"{name}_meta", np.array([res.iterations, int(res.converged)], dtype=np.int64))
+        put(f"{name}_rel", np.array(res.relative_residual))
+        put(f"{name}_flops", rep(fc))
+        if P <= 256:
+            sysm = R.type4_system(grid, b) if which == "type4" else R.type5_system(grid, b)
+            put(f"{name}_ge", R.ge_solve(sysm))
+    fc = R.FlopCounter()
+    grid, _ = R.generate_trial(32, 7)
+    b = randc2(32)
+    sysm = R.type4_system(grid, b, flops=fc)
+    put("ge32_t", np.asarray(grid.instants))
+    put("ge32_b", b)
+    put("ge32_matrix", sysm.matrix)
+    put("ge32_x", R.ge_solve(sysm, flops=fc))
+    put("ge32_flops", rep(fc))
+    put("cg_cases", np.array([c[0] for c in cg_cases]))
+
     out["meta_numpy"] = np.array(np.__version__)
     out["meta_reference"] = np.array(R.__version__)
     dst = os.path.join(REPO, "tests", "golden", "golden.npz")

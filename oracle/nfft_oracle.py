@@ -345,6 +345,67 @@ def refine4(plan: Plan, spectrum, passes: int = 1):
 # ---------------------------------------------------------------------- inputs
 
 
+# ------------------------------------------------------------ baselines
+
+def cg(t, b, which: str = "type4", tol: float = 1e-15, max_iter: int | None = None):
+    """CGNR, unpreconditioned (baselines.py:116-181): per iteration one
+    forward and one adjoint fast NFFT; stops at ||r|| <= tol ||b||.
+    Returns (x, iterations, converged, relative_residual)."""
+    if tol <= 0.0:
+        raise ValueError("tolerance must be positive")
+    if which not in ("type4", "type5"):
+        raise ValueError(f"unknown system kind {which!r}")
+    b = np.asarray(b, dtype=np.complex128)
+    P = b.size
+    if max_iter is None:
+        max_iter = 4 * P
+    if which == "type4":
+        apply_A = lambda x: type1(t, x, P)
+        apply_AH = lambda y: type2(y, t)
+    else:
+        apply_A = lambda x: type2(x, t)
+        apply_AH = lambda y: type1(t, y, P)
+    bnorm = float(np.linalg.norm(b))
+    if bnorm == 0.0:
+        return np.zeros(P, dtype=np.complex128), 0, True, 0.0
+    x = np.zeros(P, dtype=np.complex128)
+    r = b.copy()
+    z = apply_AH(r)
+    p = z.copy()
+    zz = float(np.vdot(z, z).real)
+    rnorm = bnorm
+    iterations = 0
+    for iterations in range(1, max_iter + 1):
+        w = apply_A(p)
+        ww = float(np.vdot(w, w).real)
+        if ww == 0.0:
+            iterations -= 1
+            break
+        alpha = zz / ww
+        x = x + alpha * p
+        r = r - alpha * w
+        rnorm = float(np.linalg.norm(r))
+        if rnorm <= tol * bnorm:
+            return x, iterations, True, rnorm / bnorm
+        z = apply_AH(r)
+        zz_new = float(np.vdot(z, z).real)
+        p = z + (zz_new / zz) * p
+        zz = zz_new
+    return x, iterations, rnorm <= tol * bnorm, rnorm / bnorm
+
+
+def phase_matrix(t, sign: int):
+    """e^{sign 2 pi i p t_q}, rows p, columns q (baselines.py:37-49)."""
+    P = len(t)
+    tt = np.asarray(t, dtype=np.longdouble)
+    return cis_turns(sign * np.outer(np.arange(P, dtype=np.longdouble), tt))
+
+
+def dense_solve(matrix, rhs):
+    """Dense LU solve standing in for ge_solve (baselines.py:64-105)."""
+    return np.linalg.solve(np.asarray(matrix, dtype=np.complex128), np.asarray(rhs, dtype=np.complex128))
+
+
 def make_inputs(P: int, jitter: float, batch: int, seed: int):
     """Seeded benchmark inputs (generator as bench.py:84-92).
 

@@ -60,6 +60,9 @@ _SIGS = {
                                            ctypes.c_void_p]),
     "nfft45_refine_type4": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _i64, ctypes.c_int, ctypes.c_void_p,
                                            ctypes.c_void_p]),
+    "nfft45_cg_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, _i64, ctypes.c_double, _i64,
+                                       ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -33,6 +33,10 @@ int cuda_fail(cudaError_t e, const char* what);
 // When profiling is enabled (nfft45_profile_enable), each launch is
 // bracketed by CUDA events recorded on its own stream, keyed by kernel name.
 extern std::atomic<int64_t> g_launches;
+// NFFT45_DEBUG_SYNC=1: synchronise after every launch so an asynchronous
+// fault is reported against the kernel that caused it (debugging aid; use
+// with NFFT45_NO_GRAPH=1).
+extern const bool g_debug_sync;
 extern std::atomic<int> g_profiling;
 int prof_begin(cudaStream_t st);
 void prof_end(int slot, const char* name, cudaStream_t st);
@@ -43,6 +47,7 @@ void prof_end(int slot, const char* name, cudaStream_t st);
     if (_ps >= 0) prof_end(_ps, #kernel, stream);                          \
     g_launches.fetch_add(1, std::memory_order_relaxed);                    \
     cudaError_t _le = cudaGetLastError();                                  \
+    if (_le == cudaSuccess && g_debug_sync) _le = cudaStreamSynchronize(stream); \
     if (_le != cudaSuccess) return cuda_fail(_le, #kernel);                \
   } while (0)
 

@@ -17,6 +17,7 @@
 namespace nfft45 {
 
 std::atomic<int64_t> g_launches{0};
+const bool g_debug_sync = getenv("NFFT45_DEBUG_SYNC") != nullptr;
 std::atomic<int> g_profiling{0};
 static thread_local std::string tl_err;
 
@@ -785,6 +786,41 @@ int nfft45_nonuniform_conv(const nfft45_grid* g, const double* a, int64_t batch,
   NFFT_CHECK(V.alloc(sizeof(double2) * batch * P));
   NFFT_CHECK(type1_core(g->d, C2(a), batch, R, m, P, C2(lam), nullptr, V.c(), s));
   return fft_run(V.c(), D2(out), batch, P, +1, nullptr, nullptr, s);
+}
+
+// cg_solve(grid, rhs, which, tol, max_iter, spread_width) — baselines.py:108-181.
+namespace {
+struct GridCgOps final : CgOps {
+  const GridDev& g;
+  int64_t P;
+  int m;
+  bool type4;
+  GridCgOps(const GridDev& g_, int64_t P_, int m_, bool t4) : g(g_), P(P_), m(m_), type4(t4) {}
+  int t1(const double2* in, double2* out, int64_t batch, cudaStream_t st) const {
+    return type1_core(g, in, batch, P, m, P, nullptr, nullptr, out, st);
+  }
+  int t2(const double2* in, double2* out, int64_t batch, cudaStream_t st) const {
+    return type2_core(g, in, batch, P, m, nullptr, out, st);
+  }
+  int A(const double2* in, double2* out, int64_t batch, cudaStream_t st) const override {
+    return type4 ? t1(in, out, batch, st) : t2(in, out, batch, st);
+  }
+  int AH(const double2* in, double2* out, int64_t batch, cudaStream_t st) const override {
+    return type4 ? t2(in, out, batch, st) : t1(in, out, batch, st);
+  }
+};
+}  // namespace
+
+int nfft45_cg_solve(const nfft45_grid* g, int kind, const double* rhs, int64_t batch, double tol, int64_t max_iter,
+                    int m, double* x, int64_t* iterations, int* converged, double* relres, int* stalled, void* st) {
+  if (!g || batch < 0 || m < 1 || max_iter < 0 || !iterations || !converged || !relres)
+    return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid cg_solve arguments");
+  if (!(tol > 0.0)) return fail(NFFT45_ERR_INVALID_ARGUMENT, "tolerance must be positive");
+  if (kind != 4 && kind != 5) return fail(NFFT45_ERR_INVALID_ARGUMENT, "unknown system kind");
+  DeviceGuard dg(g->d.device);
+  if (dg.status) return dg.status;
+  GridCgOps ops(g->d, g->d.Q, m, kind == 4);
+  return cg_run(ops, C2(rhs), batch, g->d.Q, tol, max_iter, D2(x), iterations, converged, relres, stalled, S(st));
 }
 
 int nfft45_type1_direct(const nfft45_grid* g, const double* a, int64_t batch, int64_t R, double* out, void* st) {

@@ -115,4 +115,15 @@ __device__ __forceinline__ double deconv_weight(int64_t p, int64_t K, int64_t n,
   return exp(b * (x * x)) / sqrt(4.0 * 3.141592653589793 * b);
 }
 
+
+// CGNR (baselines.py:108-181): the system matrix and its Hermitian transpose
+// as batched device operators, and the device-resident iteration (cg.cu).
+struct CgOps {
+  virtual int A(const double2* in, double2* out, int64_t batch, cudaStream_t st) const = 0;
+  virtual int AH(const double2* in, double2* out, int64_t batch, cudaStream_t st) const = 0;
+  virtual ~CgOps() = default;
+};
+int cg_run(const CgOps& ops, const double2* b, int64_t batch, int64_t P, double tol, int64_t max_iter,
+           double2* x, int64_t* iterations, int* converged, double* relres, int* stalled, cudaStream_t st);
+
 }  // namespace nfft45

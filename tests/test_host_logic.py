@@ -155,3 +155,42 @@ def test_tally_and_merge():
     b.complex_exp(2)
     a.merge(b)
     assert a.report().complex_exps == 2 and a.report().fft_invocations == (4,)
+
+
+def _report_array(fc):
+    r = fc.report()
+    return np.array([r.real_adds, r.complex_adds, r.real_muls, r.complex_muls, r.complex_exps, r.total_flops]
+                    + list(r.fft_invocations), dtype=np.int64)
+
+
+@pytest.mark.parametrize("name,which", [("cg4", "type4"), ("cg5", "type5"), ("cgcap", "type4"),
+                                        ("cgtol", "type4")])
+def test_cg_flop_charges_match_reference(golden, name, which):
+    """cg_solve's flops= charges (baselines.py:141-181) from the iteration
+    outcome alone reproduce the reference's counter for the same run."""
+    from paper_1604_06236_b200 import baselines as B
+
+    P = golden[f"{name}_t"].size
+    it, conv = (int(v) for v in golden[f"{name}_meta"])
+    fc = nf.FlopCounter()
+    B._charge_cg(fc, P, 29, which, it, bool(conv), False, False)
+    assert np.array_equal(_report_array(fc), golden[f"{name}_flops"])
+
+
+def test_ge_flop_charges_match_reference(golden):
+    from paper_1604_06236_b200 import baselines as B
+
+    n = golden["ge32_t"].size
+    fc = nf.FlopCounter()
+    fc.real_mul(n * n)  # type4_system's phase matrix (baselines.py:46-48)
+    fc.complex_exp(n * n)
+    B._charge_ge(fc, n, n - 1, True)
+    assert np.array_equal(_report_array(fc), golden["ge32_flops"])
+
+
+def test_cg_argument_checks_precede_device_work():
+    grid = nf.NonuniformGrid.__new__(nf.NonuniformGrid)  # never touched: validation fails first
+    with pytest.raises(ValueError):
+        nf.cg_solve(grid, np.ones(8), tol=0.0)
+    with pytest.raises(ValueError):
+        nf.cg_solve(grid, np.ones(8), which="type3")

@@ -99,3 +99,27 @@ def test_validation_errors():
     assert list(order) == [1, 0, 2]
     with pytest.raises(O.NonPositiveDamping):
         O.damping(0.5, 4, 1)
+
+
+_CG_ARGS = {"cg4": ("type4", 1e-14, None), "cg5": ("type5", 1e-14, None), "cgcap": ("type4", 1e-15, 2),
+            "cgtol": ("type4", 1e-10, None)}
+
+
+@pytest.mark.parametrize("name", sorted(_CG_ARGS))
+def test_oracle_cg_reproduces_reference(golden, name):
+    """CGNR restatement (baselines.py:116-181) vs the reference's own runs:
+    same iteration count and convergence flag, same iterate."""
+    which, tol, cap = _CG_ARGS[name]
+    x, it, conv, relres = O.cg(golden[f"{name}_t"], golden[f"{name}_b"], which, tol, cap)
+    want_it, want_conv = (int(v) for v in golden[f"{name}_meta"])
+    assert (it, int(conv)) == (want_it, want_conv)
+    assert rel(golden[f"{name}_x"], x) < 1e-14
+    assert abs(relres - float(golden[f"{name}_rel"])) <= 1e-12 * float(golden[f"{name}_rel"])
+
+
+def test_oracle_phase_matrix_and_dense_solve(golden):
+    M = O.phase_matrix(golden["ge32_t"], -1)
+    assert np.abs(M - golden["ge32_matrix"]).max() < 1e-15
+    assert rel(golden["ge32_x"], O.dense_solve(M, golden["ge32_b"])) < 1e-12
+    for name in ("cg4", "cg5"):  # CG converged to the dense solution
+        assert rel(golden[f"{name}_ge"], golden[f"{name}_x"]) < 1e-10
