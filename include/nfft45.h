@@ -45,7 +45,8 @@ typedef enum {
   NFFT45_ERR_NON_CONVERGENCE = 8,       /* NonConvergenceError      errors.py:40  */
   NFFT45_ERR_INVALID_ARGUMENT = 9,      /* ValueError (grid.py:143-150)           */
   NFFT45_ERR_CUDA = 10,                 /* CUDA runtime failure                   */
-  NFFT45_ERR_NO_DEVICE = 11             /* no usable sm_100 device                */
+  NFFT45_ERR_NO_DEVICE = 11,            /* no usable sm_100 device                */
+  NFFT45_ERR_SINGULAR_MATRIX = 12       /* SingularMatrixError      errors.py     */
 } nfft45_status;
 
 typedef struct nfft45_grid nfft45_grid;  /* device-resident node set */
@@ -133,6 +134,17 @@ int nfft45_dft(const double* in_dev, double* out_dev, int64_t batch, int64_t N, 
 int nfft45_cg_solve(const nfft45_grid* g, int kind, const double* rhs_dev, int64_t batch, double tol,
                     int64_t max_iter, int m, double* x_dev, int64_t* iterations, int* converged,
                     double* relres, int* stalled, void* stream);
+
+/* ge_solve(DenseSystem) — baselines.py:64-105.  Dense right-looking
+ * Gaussian elimination with partial pivoting on the device, in the
+ * reference's operation order.  A_dev: complex [n][n] row-major and b_dev:
+ * complex [n], both device and OVERWRITTEN (U and the eliminated rhs);
+ * x_dev: complex [n].  A pivot magnitude below pivot_floor (1e-300) at
+ * elimination step k < n-1, or on the last diagonal entry (k = n-1), returns
+ * SINGULAR_MATRIX; *bad_step (host) is that k, or n on success, and
+ * *bad_pivot its magnitude. */
+int nfft45_ge_solve(double* A_dev, double* b_dev, int64_t n, double* x_dev, double pivot_floor,
+                    int64_t* bad_step, double* bad_pivot, void* stream);
 
 /* ------------------------------------------------- Lagrange quantities */
 

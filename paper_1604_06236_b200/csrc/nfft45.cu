@@ -823,6 +823,26 @@ int nfft45_cg_solve(const nfft45_grid* g, int kind, const double* rhs, int64_t b
   return cg_run(ops, C2(rhs), batch, g->d.Q, tol, max_iter, D2(x), iterations, converged, relres, stalled, S(st));
 }
 
+int nfft45_ge_solve(double* A, double* b, int64_t n, double* x, double pivot_floor, int64_t* bad_step,
+                    double* bad_pivot, void* st) {
+  if (!A || !b || !x || n < 1 || !bad_step || !bad_pivot)
+    return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid ge_solve arguments");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DeviceGuard dg(dev);
+  if (dg.status) return dg.status;
+  NFFT_CHECK(ge_run(D2(A), D2(b), n, D2(x), pivot_floor, bad_step, bad_pivot, S(st)));
+  if (*bad_step < n) {
+    char buf[96];
+    if (*bad_step < n - 1)
+      snprintf(buf, sizeof buf, "pivot %.3e below %.0e", *bad_pivot, pivot_floor);
+    else
+      snprintf(buf, sizeof buf, "matrix is numerically singular");
+    return fail(NFFT45_ERR_SINGULAR_MATRIX, buf);
+  }
+  return NFFT45_OK;
+}
+
 int nfft45_type1_direct(const nfft45_grid* g, const double* a, int64_t batch, int64_t R, double* out, void* st) {
   if (!g || R < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid direct type-1 arguments");
   DeviceGuard dg(g->d.device);

@@ -126,4 +126,8 @@ struct CgOps {
 int cg_run(const CgOps& ops, const double2* b, int64_t batch, int64_t P, double tol, int64_t max_iter,
            double2* x, int64_t* iterations, int* converged, double* relres, int* stalled, cudaStream_t st);
 
+// Dense GE with partial pivoting (baselines.py:64-105), dense.cu.
+int ge_run(double2* A, double2* b, int64_t n, double2* x, double floor, int64_t* bad_step_host,
+           double* bad_val_host, cudaStream_t st);
+
 }  // namespace nfft45

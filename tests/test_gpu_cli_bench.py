@@ -1,0 +1,181 @@
+"""The file-in/file-out CLI, the GPU self-check suite and the Monte-Carlo
+figure harness on the GPU (reference tests/test_cli.py, test_bench.py)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1604_06236_b200 as nf
+from paper_1604_06236_b200 import bench as B
+from paper_1604_06236_b200.cli import main
+from paper_1604_06236_b200.vecio import read_results_csv, read_vector_file, write_grid_file, write_vector_file
+
+pytestmark = pytest.mark.gpu
+
+
+def _trial_files(tmp_path, P=8, seed=3):
+    grid, amps = nf.generate_trial(P, seed)
+    write_grid_file(tmp_path / "grid.txt", grid.instants)
+    return grid, amps, str(tmp_path / "grid.txt")
+
+
+def _rel(want, got):
+    return np.linalg.norm(got - want) / np.linalg.norm(want)
+
+
+# ------------------------------------------------------------------ transform
+
+def test_transform_type2_constant(tmp_path):
+    _, _, g = _trial_files(tmp_path)
+    S = np.zeros(8, complex)
+    S[0] = 2.0 - 0.5j
+    write_vector_file(tmp_path / "coef.txt", S)
+    assert main(["transform", "--type", "2", "--grid", g, "--data", str(tmp_path / "coef.txt"),
+                 "--out", str(tmp_path / "out.txt")]) == 0
+    assert np.abs(read_vector_file(tmp_path / "out.txt") - (2.0 - 0.5j)).max() < 1e-12
+
+
+def test_transform_type1_output_length(tmp_path):
+    grid, amps, g = _trial_files(tmp_path)
+    write_vector_file(tmp_path / "amps.txt", amps)
+    assert main(["transform", "--type", "1", "--grid", g, "--data", str(tmp_path / "amps.txt"),
+                 "--out", str(tmp_path / "spec.txt"), "--p", "16"]) == 0
+    got = read_vector_file(tmp_path / "spec.txt")
+    assert got.size == 16 and _rel(nf.nfft_type1_direct(grid, amps, 16), got) < 1e-12
+
+
+def test_transform_type4_roundtrip_flag(tmp_path, capsys):
+    grid, amps, g = _trial_files(tmp_path, P=16, seed=5)
+    write_vector_file(tmp_path / "spec.txt", nf.nfft_type1_direct(grid, amps, 16))
+    assert main(["transform", "--type", "4", "--grid", g, "--data", str(tmp_path / "spec.txt"),
+                 "--out", str(tmp_path / "amps.txt"), "--mu", "1e-11", "--eta", "2", "--check-roundtrip"]) == 0
+    line = [x for x in capsys.readouterr().out.splitlines() if x.startswith("roundtrip-residual")][0]
+    assert float(line.split()[1]) < 1e-9
+    assert _rel(amps, read_vector_file(tmp_path / "amps.txt")) < 1e-9
+
+
+def test_transform_type5_matches_dense_solve(tmp_path):
+    grid, _, g = _trial_files(tmp_path, P=8, seed=9)
+    rng = np.random.default_rng(1)
+    s = rng.standard_normal(8) + 1j * rng.standard_normal(8)
+    write_vector_file(tmp_path / "s.txt", s)
+    assert main(["transform", "--type", "5", "--grid", g, "--data", str(tmp_path / "s.txt"),
+                 "--out", str(tmp_path / "c.txt"), "--mu", "1e-11", "--eta", "2"]) == 0
+    assert _rel(nf.ge_solve(nf.type5_system(grid, s)), read_vector_file(tmp_path / "c.txt")) < 1e-10
+
+
+def test_transform_refined_pass(tmp_path):
+    grid, amps, g = _trial_files(tmp_path, P=64, seed=13)
+    write_vector_file(tmp_path / "spec.txt", nf.nfft_type1_direct(grid, amps, 64))
+    common = ["transform", "--type", "4", "--grid", g, "--data", str(tmp_path / "spec.txt"), "--mu", "1e-6",
+              "--eta", "1"]
+    assert main(common + ["--out", str(tmp_path / "plain.txt")]) == 0
+    assert main(common + ["--out", str(tmp_path / "ref.txt"), "--passes", "1"]) == 0
+    assert (np.linalg.norm(read_vector_file(tmp_path / "ref.txt") - amps)
+            < np.linalg.norm(read_vector_file(tmp_path / "plain.txt") - amps))
+
+
+def test_transform_type5_against_frozen_fixture(tmp_path, golden):
+    """The reference's checked-in dense-elimination fixture, through files."""
+    write_grid_file(tmp_path / "grid8.txt", golden["fixture_grid8"])
+    write_vector_file(tmp_path / "samples8.txt", golden["fixture_samples8"])
+    assert main(["transform", "--type", "5", "--grid", str(tmp_path / "grid8.txt"), "--data",
+                 str(tmp_path / "samples8.txt"), "--out", str(tmp_path / "c.txt"), "--mu", "1e-11",
+                 "--eta", "2"]) == 0
+    assert _rel(golden["fixture_coeffs8"], read_vector_file(tmp_path / "c.txt")) < 1e-10
+
+
+# ------------------------------------------------------------------ verify
+
+def test_verify_quick_and_full(capsys):
+    assert main(["verify", "--level", "quick"]) == 0
+    assert "kernel-coefficient-recovery" in capsys.readouterr().out
+    assert main(["verify", "--level", "full"]) == 0
+    assert "flop-duality" in capsys.readouterr().out
+
+
+def test_verify_fault_injection(capsys):
+    assert main(["verify", "--level", "quick", "--inject-fault", "kernel-coefficient-recovery"]) == 1
+    assert "kernel-coefficient-recovery" in capsys.readouterr().err
+
+
+# ------------------------------------------------------------ bench / harness
+
+def test_bench_smoke(tmp_path):
+    out = tmp_path / "fig1.csv"
+    assert main(["bench", "--figure", "fig1", "--out", str(out), "--p", "32", "--trials", "2", "--eta", "1",
+                 "--mu", "1e-10", "1e-8", "--method", "NFFT", "GE", "--seed", "19"]) == 0
+    rows, meta = read_results_csv(out)
+    assert meta["figure"] == "fig1" and len(rows) == 2 + 2 * 2
+
+
+def test_bench_out_dir_env(tmp_path, monkeypatch):
+    monkeypatch.setenv("NUFFT1D_OUT_DIR", str(tmp_path))
+    assert main(["bench", "--figure", "fig7", "--p", "16", "--trials", "1", "--eta", "1", "2", "--method", "NFFT",
+                 "--seed", "3"]) == 0
+    assert (tmp_path / "fig7.csv").exists()
+
+
+SMALL = B.TrialConfig(p=(32,), eta=(1, 2), mu=(1e-10, 1e-8), trials=2, seed=7,
+                      methods=(B.METHOD_GE, B.METHOD_CG, B.METHOD_NFFT, B.METHOD_RNFFT))
+
+
+def test_run_sweep_structure_and_determinism():
+    rows1, rows2 = B.run_sweep(SMALL), B.run_sweep(SMALL)
+    assert rows1 == rows2  # bitwise-deterministic device path
+    assert {r.method for r in rows1} == set(B.ALL_METHODS)
+    assert sum(r.method == B.METHOD_GE for r in rows1) == 2
+    assert sum(r.method == B.METHOD_NFFT for r in rows1) == 2 * 2 * 2
+    for r in rows1:
+        if r.method == B.METHOD_CG:
+            assert r.cg_iterations and r.cg_iterations > 0
+        assert r.total_flops > 0
+        assert abs(r.error_db - 20.0 * math.log10(r.error_linear)) < 1e-9
+
+
+def test_error_consistent_with_reconstruction():
+    rows = B.run_sweep(B.TrialConfig(p=(16,), eta=(2,), mu=(1e-11,), trials=1, seed=3, methods=(B.METHOD_NFFT,)))
+    assert len(rows) == 1
+    grid, a_true = nf.generate_trial(16, 3)
+    plan = nf.build_plan(grid, nf.MethodParams.from_mu(1e-11, 16, 2))
+    err = nf.relative_error(a_true, nf.type4(plan, nf.nfft_type1_direct(grid, a_true, 16)))
+    assert abs(err - rows[0].error_linear) / err < 1e-12
+
+
+def test_infeasible_mu_skipped():
+    rows = B.run_sweep(B.TrialConfig(p=(32,), eta=(1,), mu=(0.5, 1e-10), trials=1, seed=1,
+                                     methods=(B.METHOD_NFFT,)))
+    assert len(rows) == 1 and rows[0].mu == 1e-10
+
+
+def test_ge_cg_error_agreement():
+    rows = B.run_sweep(B.TrialConfig(p=(512,), trials=3, seed=5, methods=(B.METHOD_GE, B.METHOD_CG)))
+    ge = {r.trial: r.error_db for r in rows if r.method == B.METHOD_GE}
+    cg = {r.trial: r.error_db for r in rows if r.method == B.METHOD_CG}
+    assert ge.keys() == cg.keys() and all(abs(ge[t] - cg[t]) <= 5.0 for t in ge)
+
+
+def test_best_mu_and_figures():
+    rows = B.run_sweep(B.TrialConfig(p=(64,), eta=(1,), mu=(1e-13, 1e-9, 1e-5), trials=2, seed=11,
+                                     methods=(B.METHOD_RNFFT,)))
+    winners = B.best_mu(rows, B.METHOD_RNFFT)
+    assert {r.mu for r in B.filter_best_mu(rows, B.METHOD_RNFFT)} == {winners[(64, 1)]}
+    rows, meta = B.run_figure("fig2", B.TrialConfig(p=(32,), eta=(1,), mu=(1e-10, 1e-7), trials=2, seed=2,
+                                                    methods=(B.METHOD_GE, B.METHOD_RNFFT)))
+    assert meta["figure"] == "fig2" and len({r.mu for r in rows if r.method == B.METHOD_RNFFT}) == 1
+    rows, _ = B.run_figure("fig1", B.TrialConfig(p=(32, 64), eta=(1,), mu=(1e-9,), trials=1, seed=4,
+                                                 methods=(B.METHOD_GE, B.METHOD_NFFT)), dense_cap=32)
+    assert any(r.method == B.METHOD_GE and r.p == 32 for r in rows)
+    assert not any(r.method == B.METHOD_GE and r.p == 64 for r in rows)
+    assert any(r.method == B.METHOD_NFFT and r.p == 64 for r in rows)
+
+
+def test_multi_pass_sweep_skips_diverging_cells():
+    """Cells whose two-pass refinement raises NonConvergence are skipped.
+    The reference's plain error already reaches 1 at mu = 1e-18 (P = 64,
+    eta = 1); this path's more accurate phases keep that cell contracting
+    (error ~6e-3), so the diverging corner is taken further out."""
+    rows = B.run_sweep(B.TrialConfig(p=(64,), eta=(1,), mu=(1e-22, 1e-18, 1e-9), trials=1, seed=21,
+                                     methods=(B.METHOD_RNFFT,), refine_passes=2))
+    assert {r.mu for r in rows} == {1e-18, 1e-9}
