@@ -85,7 +85,7 @@ def main(lpath, fpath, tag, steps):
     short = {}
     for k, v in traffic.items():
         key = {"kbm_pad": "bm_pad", "kbm_band": "bm_band", "kbm_mid": "bm_mid", "kbm_col": "bm_col", "kbm_row": "bm_row",
-               "k_spread_p": "spread_p", "k_gather_b": "gather_b", "kbm_colin": "bm_colin",
+               "k_spread_p": "spread_p", "k_gather_b": "gather_b", "k_gather_p": "gather_p", "kbm_colin": "bm_colin",
                "kbm_rowout": "bm_rowout"}.get(k.split("<")[0], k.split("<")[0])
         short[key] = sum(v) / len(v)
     json.dump(short, open(os.path.join(REPO, "profiles", "traffic_c4.json"), "w"), indent=1)
