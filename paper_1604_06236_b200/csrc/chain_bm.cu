@@ -38,6 +38,14 @@ __host__ __device__ constexpr int bm_rw() { return fast_threads<M, 16>() > 512 ?
 
 
 __device__ __forceinline__ double2 rsc(double2 v, double s) { return make_double2(v.x * s, v.y * s); }
+// 0 that the compiler cannot prove constant: offsetting the tables by it inside
+// a persistent tile loop keeps loop-invariant twiddles from being hoisted into
+// (and spilled from) registers across tiles.
+__device__ __forceinline__ int opaque0() {
+  int z;
+  asm volatile("mov.u32 %0, 0;" : "=r"(z));
+  return z;
+}
 
 __device__ __forceinline__ void cpa16(void* sdst, const void* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
@@ -63,6 +71,7 @@ __device__ __forceinline__ void persistent_tiles(int ntiles, double2* buf0, doub
   };
   int t = blockIdx.x;
   if (t < ntiles) prefetch(t, buf0);
+#pragma unroll 1
   for (int it = 0; t < ntiles; t += gridDim.x, it++) {
     double2* cur = (it & 1) ? buf1 : buf0;
     double2* nxt = (it & 1) ? buf0 : buf1;
@@ -107,8 +116,8 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<
 // tile) are staged into shared memory with cp.async at entry; the copies fly
 // during the first FFT pass (CpAsyncWaitHook) instead of stalling the band
 // epilogue on L2 latency.
-template <int M, int SG>
-__global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_threads<2 * M, SG>())) kbm_band(
+template <int M, int SG, class Tr1 = FastTraits<2 * M>>
+__global__ void __launch_bounds__(2 * M * SG / Tr1::E, Tr1::E == 8 ? 2 : bm_minb(2 * M * SG / Tr1::E)) kbm_band(
     const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
@@ -147,7 +156,7 @@ __global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_thread
       sm[sidx<M, SG, true>(m1, c)] = v;
     }
   };
-  fast_tile_fft<NR, SG, -1, true>(sm, ld1, st1, twR, NoPostTw(), CpAsyncWaitHook());
+  fast_tile_fft<NR, SG, -1, true, Tr1>(sm, ld1, st1, twR, NoPostTw(), CpAsyncWaitHook());
   __syncthreads();
   auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, SG, true>(i, c)]; };
   auto st2 = [&](int k1p, int c, double2 v) { U[((int64_t)k1p * M + k1) * Bp + b0 + c] = v; };
@@ -312,8 +321,8 @@ __global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 1) kbm_pad_p(
 }
 
 // Persistent variant of kbm_band.
-template <int M>
-__global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 1) kbm_band_p(
+template <int M, class Tr1 = FastTraits<2 * M>>
+__global__ void __launch_bounds__(2 * M * kSig / Tr1::E, 1) kbm_band_p(
     const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, int groups, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
@@ -345,12 +354,13 @@ __global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 1) kbm_band_p(
         sm[sidx<M, kSig, true>(m1, c)] = v;
       }
     };
-    fast_tile_fft<NR, kSig, -1, true>(sm, ld1, st1, twR);
+    const int z = opaque0();
+    fast_tile_fft<NR, kSig, -1, true, Tr1>(sm, ld1, st1, twR + z);
     __syncthreads();
     auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, kSig, true>(i, c)]; };
     auto st2 = [&](int k1p, int c, double2 v) { U[((int64_t)k1p * M + k1) * Bp + b0 + c] = v; };
-    const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, k1, 0};
-    fast_tile_fft_smem<M, kSig, +1, true, HalfTr<M>>(sm, ld2, st2, twC, pt);
+    const FourStepTw<+1> pt{loP + z, hiP + z, sP, twQ + z, Q, k1, 0};
+    fast_tile_fft_smem<M, kSig, +1, true, HalfTr<M>>(sm, ld2, st2, twC + z, pt);
   };
   persistent_tiles<NR>(M * groups, buf0, buf1, src, body);
 }
@@ -440,6 +450,7 @@ struct ChainBM {
   int sms = 148;           // persistent grid size (set from the device)
   bool persistent = true;
   bool small_tiles = false;  // 4-signal tiles for the two-FFT kernels
+  bool e8 = false;           // experiment: radix-8 / 8-element schedule for the 2M-point stage
 
   int qtab(int64_t Q, const double2** out) {
     int status = NFFT45_OK;
@@ -471,9 +482,16 @@ struct ChainBM {
     NFFT_CHECK(qtab(Q, &twQ));
     constexpr size_t smem_p = fast_smem<2 * M, kSig>() + 16 + 2 * sizeof(double2) * 2 * M * kSig;
     if (persistent && smem_p <= 227 * 1024) {
+      const int ntiles = M * (int)groups;
+      if (e8) {
+        auto bm_band_p8 = kbm_band_p<M, FastTraitsE8<2 * M>>;
+        NFFT_CHECK(bm_attr(bm_band_p8, smem_p));
+        LAUNCH(bm_band_p8, (unsigned)std::min(ntiles, sms), 2 * M * kSig / 8, smem_p, st, T_, U, Bp, (int)groups,
+               t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
+        return NFFT45_OK;
+      }
       auto bm_band_p = kbm_band_p<M>;
       NFFT_CHECK(bm_attr(bm_band_p, smem_p));
-      const int ntiles = M * (int)groups;
       LAUNCH(bm_band_p, (unsigned)std::min(ntiles, sms), T, smem_p, st, T_, U, Bp, (int)groups, t.tw2M, t.twM,
              t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
       return NFFT45_OK;
@@ -487,8 +505,15 @@ struct ChainBM {
              t.tP->s, twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
       return NFFT45_OK;
     }
-    auto bm_band = kbm_band<M, kSig>;
     const size_t smem = fast_smem<2 * M, kSig>() + 2 * sizeof(double) * M + (sub ? sizeof(double2) * M * kSig : 0);
+    if (e8) {
+      auto bm_band8 = kbm_band<M, kSig, FastTraitsE8<2 * M>>;
+      NFFT_CHECK(bm_attr(bm_band8, smem));
+      LAUNCH(bm_band8, dim3((unsigned)M, groups), 2 * M * kSig / 8, smem, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo,
+             t.tP->hi, t.tP->s, twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
+      return NFFT45_OK;
+    }
+    auto bm_band = kbm_band<M, kSig>;
     NFFT_CHECK(bm_attr(bm_band, smem));
     LAUNCH(bm_band, dim3((unsigned)M, groups), T, smem, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s,
            twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
@@ -595,6 +620,8 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
     ch.persistent = persist;
     static const bool small = getenv("NFFT45_TILE4") != nullptr;  // A/B experiment
     ch.small_tiles = small;
+    static const bool e8 = getenv("NFFT45_E8") != nullptr;
+    ch.e8 = e8;
   }
   int status = NFFT45_OK;
   {

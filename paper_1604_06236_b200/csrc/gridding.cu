@@ -1,7 +1,9 @@
 // gridding.cu — Gaussian-window spreading / interpolation, band kernels,
 // direct sums.  fp64 throughout, deterministic (no floating-point atomics).
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "ops.cuh"
 
@@ -98,6 +100,63 @@ __global__ void k_tile_ranges(const double* __restrict__ ts, int64_t Q, int64_t 
 // image s of the tile, the contributing nodes (a contiguous range of the
 // ascending order) are staged in shared memory (centre, 2m+1 weights, SB
 // amplitudes) and every thread accumulates its own cell in node order.
+struct RangeCache {
+  struct Entry {
+    int64_t n;
+    int m, TC, NS;
+    int2* d;
+  };
+  std::mutex mu;
+  std::vector<Entry> v;
+};
+
+int tile_ranges(const GridDev& g, int64_t n, int m, int TC, int NS, cudaStream_t st, const int2** out, int2** own) {
+  *own = nullptr;
+  if (g.rc) {
+    std::lock_guard<std::mutex> lk(g.rc->mu);
+    for (const auto& e : g.rc->v)
+      if (e.n == n && e.m == m && e.TC == TC && e.NS == NS) {
+        *out = e.d;
+        return NFFT45_OK;
+      }
+  }
+  const int64_t ntiles = ceil_div(n, TC);
+  int2* r = nullptr;
+  NFFT_CUDA(cudaMallocAsync(&r, sizeof(int2) * ntiles * NS, st));
+  LAUNCH(k_tile_ranges, (unsigned)ceil_div(ntiles * NS, 128), 128, 0, st, g.ts, g.Q, n, m, TC, ntiles, NS, r);
+  *out = r;
+  *own = r;
+  return NFFT45_OK;
+}
+
+int tile_ranges_cache(const GridDev& g, int64_t n, int m, int TC, cudaStream_t st) {
+  if (!g.rc) return NFFT45_OK;
+  const int NS = tile_images(n, m, TC);
+  if (NS > 8) return NFFT45_OK;
+  {
+    std::lock_guard<std::mutex> lk(g.rc->mu);
+    for (const auto& e : g.rc->v)
+      if (e.n == n && e.m == m && e.TC == TC && e.NS == NS) return NFFT45_OK;
+  }
+  const int64_t ntiles = ceil_div(n, TC);
+  int2* r = nullptr;
+  NFFT_CUDA(cudaMalloc(&r, sizeof(int2) * ntiles * NS));
+  LAUNCH(k_tile_ranges, (unsigned)ceil_div(ntiles * NS, 128), 128, 0, st, g.ts, g.Q, n, m, TC, ntiles, NS, r);
+  NFFT_CUDA(cudaStreamSynchronize(st));
+  std::lock_guard<std::mutex> lk(g.rc->mu);
+  g.rc->v.push_back({n, m, TC, NS, r});
+  return NFFT45_OK;
+}
+
+RangeCache* range_cache_new() { return new RangeCache(); }
+
+void tile_ranges_free(GridDev& g) {
+  if (!g.rc) return;
+  for (auto& e : g.rc->v) cudaFree(e.d);
+  delete g.rc;
+  g.rc = nullptr;
+}
+
 template <int SB, int M>
 __global__ void __launch_bounds__(256) k_spread(const double* __restrict__ ts, const int* __restrict__ perm,
                                                 int64_t Q, int64_t n, int m, double alpha, GaussTab G,
@@ -199,15 +258,14 @@ static int spread_launch(const GridDev& g, int64_t n, const Window& win, const d
   size_t smem = (size_t)NB * taps * 8 + (size_t)SB * NB * 16 + (size_t)NB * 4;
   NFFT_CHECK(smem_attr(k_spread<SB, M>, smem));
   const int64_t ntiles = ceil_div(n, TC);
-  const int NS = (int)((2 * win.m + TC - 1) / n + 3);
-  int2* ranges = nullptr;
-  NFFT_CUDA(cudaMallocAsync(&ranges, sizeof(int2) * ntiles * NS, st));
-  LAUNCH(k_tile_ranges, (unsigned)ceil_div(ntiles * NS, 128), 128, 0, st, g.ts, g.Q, n, win.m, TC, ntiles, NS,
-         ranges);
+  const int NS = tile_images(n, win.m, TC);
+  const int2* ranges = nullptr;
+  int2* own = nullptr;
+  NFFT_CHECK(tile_ranges(g, n, win.m, TC, NS, st, &ranges, &own));
   dim3 grid((unsigned)ntiles, (unsigned)ceil_div(batch, SB));
   LAUNCH((k_spread<SB, M>), grid, TC, smem, st, g.ts, g.perm, g.Q, n, win.m, win.alpha, gauss_tab(win), amp,
          batch, f, H, NB, ranges, NS);
-  NFFT_CUDA(cudaFreeAsync(ranges, st));
+  if (own) NFFT_CUDA(cudaFreeAsync(own, st));
   return NFFT45_OK;
 }
 
@@ -216,6 +274,8 @@ int spread(const GridDev& g, int64_t n, const Window& win, const double2* amp, i
   if (batch <= 0) return NFFT45_OK;
   bool fast = (win.m == kFastM);
   if (fast && batch >= 32 && n >= 128) return spread_batched(g, n, win, amp, batch, f, H, st, batch >= 64 ? 2 : 1);
+  static const bool legacy = getenv("NFFT45_LEGACY_SMALL") != nullptr;  // A/B switch
+  if (fast && !legacy && tile_images(n, win.m, 256) <= 8) return spread_small(g, n, win, amp, batch, f, H, st);
   if (batch >= 4) return fast ? spread_launch<4, kFastM>(g, n, win, amp, batch, f, H, st)
                               : spread_launch<4, 0>(g, n, win, amp, batch, f, H, st);
   return fast ? spread_launch<1, kFastM>(g, n, win, amp, batch, f, H, st)
@@ -299,6 +359,8 @@ int gather_mode(const GridDev& g, int64_t n, const Window& win, const double2* H
   if (!sub) mode = 0;
   bool fast = (win.m == kFastM);
   if (fast && batch >= 32 && n >= 128) return gather_batched(g, n, win, H, batch, f, sub, mode, out, st);
+  static const bool legacy = getenv("NFFT45_LEGACY_SMALL") != nullptr;  // A/B switch
+  if (fast && !legacy) return gather_small(g, n, win, H, batch, f, sub, mode, out, st);
   if (batch >= 4) return fast ? gather_launch<4, kFastM>(g, n, win, H, batch, f, sub, mode, out, st)
                               : gather_launch<4, 0>(g, n, win, H, batch, f, sub, mode, out, st);
   return fast ? gather_launch<1, kFastM>(g, n, win, H, batch, f, sub, mode, out, st)

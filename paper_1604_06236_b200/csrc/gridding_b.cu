@@ -477,12 +477,11 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
 int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch,
                      int64_t amp_ld, NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st) {
   const int64_t ntiles = ceil_div(n, kSpreadTile);
-  const int NS = (int)((2 * win.m + kSpreadTile - 1) / n + 3);
+  const int NS = tile_images(n, win.m, kSpreadTile);
   if (NS > 8) return NFFT45_ERR_INVALID_ARGUMENT;
-  int2* ranges = nullptr;
-  NFFT_CUDA(cudaMallocAsync(&ranges, sizeof(int2) * ntiles * NS, st));
-  LAUNCH(k_tile_ranges, (unsigned)ceil_div(ntiles * NS, 128), 128, 0, st, g.ts, g.Q, n, win.m, kSpreadTile, ntiles,
-         NS, ranges);
+  const int2* ranges = nullptr;
+  int2* own = nullptr;
+  NFFT_CHECK(tile_ranges(g, n, win.m, kSpreadTile, NS, st, &ranges, &own));
   constexpr int SIG = 32;
   const int ngroups = (int)ceil_div(H_ld, SIG);
   // enough CTAs for ~2 waves of 148 SMs, each walking several signal groups
@@ -492,19 +491,18 @@ int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const doubl
   NFFT_CUDA(cudaFuncSetAttribute(spread_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   LAUNCH(spread_p, dim3((unsigned)ntiles, (unsigned)slices), 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha,
          gauss_tab(win), amp, batch, f, H, ranges, NS, amp_ld, H_ld, ngroups);
-  NFFT_CUDA(cudaFreeAsync(ranges, st));
+  if (own) NFFT_CUDA(cudaFreeAsync(own, st));
   return NFFT45_OK;
 }
 
 int spread_batched(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch, NodeFactor f,
                    double2* H, cudaStream_t st, int spl, int64_t amp_ld, int64_t H_ld) {
   const int64_t ntiles = ceil_div(n, kSpreadTile);
-  const int NS = (int)((2 * win.m + kSpreadTile - 1) / n + 3);
+  const int NS = tile_images(n, win.m, kSpreadTile);
   if (NS > 8) return NFFT45_ERR_INVALID_ARGUMENT;  // tiny grids use the generic kernel
-  int2* ranges = nullptr;
-  NFFT_CUDA(cudaMallocAsync(&ranges, sizeof(int2) * ntiles * NS, st));
-  LAUNCH(k_tile_ranges, (unsigned)ceil_div(ntiles * NS, 128), 128, 0, st, g.ts, g.Q, n, win.m, kSpreadTile, ntiles,
-         NS, ranges);
+  const int2* ranges = nullptr;
+  int2* own = nullptr;
+  NFFT_CHECK(tile_ranges(g, n, win.m, kSpreadTile, NS, st, &ranges, &own));
   GaussTab G = gauss_tab(win);
   if (spl == 2) {
     constexpr int SIG = 64;
@@ -523,7 +521,7 @@ int spread_batched(const GridDev& g, int64_t n, const Window& win, const double2
     LAUNCH(spread_b, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, amp, batch, f, H, ranges, NS, amp_ld,
            H_ld);
   }
-  NFFT_CUDA(cudaFreeAsync(ranges, st));
+  if (own) NFFT_CUDA(cudaFreeAsync(own, st));
   return NFFT45_OK;
 }
 

@@ -722,10 +722,12 @@ int nfft45_grid_create(const double* t, const int64_t* order, int64_t Q, int dev
   g->d.Q = Q;
   g->d.sum_hi = hi;
   g->d.sum_lo = lo;
+  g->d.rc = range_cache_new();
   size_t bytes = sizeof(double) * 2 * Q + sizeof(int) * Q;
   char* base = nullptr;
   cudaError_t e = cudaMalloc(&base, bytes);
   if (e != cudaSuccess) {
+    tile_ranges_free(g->d);
     delete g;
     return cuda_fail(e, "cudaMalloc(grid)");
   }
@@ -737,6 +739,7 @@ int nfft45_grid_create(const double* t, const int64_t* order, int64_t Q, int dev
   if (e == cudaSuccess) e = cudaMemcpy(g->d.perm, perm.data(), sizeof(int) * Q, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(base);
+    tile_ranges_free(g->d);
     delete g;
     return cuda_fail(e, "cudaMemcpy(grid)");
   }
@@ -747,6 +750,7 @@ int nfft45_grid_create(const double* t, const int64_t* order, int64_t Q, int dev
 void nfft45_grid_destroy(nfft45_grid* g) {
   if (!g) return;
   DeviceGuard dg(g->d.device);
+  tile_ranges_free(g->d);
   cudaFree(g->d.t);
   delete g;
 }
@@ -978,6 +982,10 @@ int nfft45_plan_create(const nfft45_grid* g, double a, int eta, int m, void* st,
       if (le != cudaSuccess) status = cuda_fail(le, "plan tables");
     }
     if (!status) status = check_guards(guard.d(), 1, 1, s);
+  }
+  if (!status && m == kFastM) {  // per-tile node ranges of the solve grid n = 2P (spread kernels)
+    status = tile_ranges_cache(g->d, 2 * P, m, 64, s);
+    if (!status) status = tile_ranges_cache(g->d, 2 * P, m, 256, s);
   }
   if (status) {
     cudaStreamSynchronize(s);

@@ -14,7 +14,18 @@ struct GridDev {
   int* perm;       // ts[i] = t[perm[i]]
   double sum_hi;   // sum of instants as a double-double (lagrange.py:92)
   double sum_lo;
+  struct RangeCache* rc;  // per-tile node ranges for the fine grids the plans use (may be null)
 };
+
+// Node range of every (tile of TC cells, periodic image) pair for a fine grid
+// of n cells: the cached device table when the node set holds one for
+// (n, m, TC), else computed on `st` into `*own` (caller frees it, stream-ordered).
+int tile_ranges(const GridDev& g, int64_t n, int m, int TC, int NS, cudaStream_t st, const int2** out, int2** own);
+// Compute and cache the table for (n, m, TC) (synchronous; outside stream capture).
+int tile_ranges_cache(const GridDev& g, int64_t n, int m, int TC, cudaStream_t st);
+void tile_ranges_free(GridDev& g);
+RangeCache* range_cache_new();
+inline int tile_images(int64_t n, int m, int TC) { return (int)((2 * m + TC - 1) / n + 3); }
 
 // Gaussian taps exp(-alpha k^2), k = 0..kFastM (for the factorised weights).
 struct GaussTab {
@@ -104,6 +115,11 @@ int spread_layout(const GridDev& g, int64_t n, const Window& win, const double2*
 int gather_layout(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t H_ld, int64_t batch,
                   NodeFactor f, const double2* sub, int64_t sub_ld, int mode, double2* out, int64_t out_ld,
                   cudaStream_t st);
+// Small-batch (batch < 32) m = 14 kernels (gridding_s.cu).
+int spread_small(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch, NodeFactor f,
+                 double2* H, cudaStream_t st);
+int gather_small(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch, NodeFactor f,
+                 const double2* sub, int mode, double2* out, cudaStream_t st);
 int norms_bm(const double2* r, int64_t len, int64_t batch, int64_t ld, double* norms, cudaStream_t st);
 int chain_run_bm(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes, double2* out,
                  double* norms, cudaStream_t st);
