@@ -152,6 +152,13 @@ int nfft45_ge_solve(double* A_dev, double* b_dev, int64_t n, double* x_dev, doub
 int nfft45_v_samples(const nfft45_grid* g, double damping_a, int eta, int m,
                      double* v_dev, void* stream);
 
+/* Extension (fractional oversampling, BASELINE config 5's eta = 1.5): the
+ * same with R = number of log-series terms given directly (the reference
+ * requires R = eta P with integer eta, grid.py:143-144, forward.py:149-154;
+ * here any R >= 2, the fold onto P summing a partial last slice). */
+int nfft45_v_samples_terms(const nfft45_grid* g, double damping_a, int64_t R, int m,
+                           double* v_dev, void* stream);
+
 /* kernel_samples_from_v(v, grid) — lagrange.py:78-97.  ks = exp(i pi P +
  * 2 pi i sum t + v).  Synchronizes to apply the KERNEL_OVERFLOW guard. */
 int nfft45_kernel_samples(const nfft45_grid* g, const double* v_dev, double* ks_dev,
@@ -184,6 +191,10 @@ int nfft45_derivative_samples(const nfft45_grid* g, const double* L_dev, int m,
  * NON_POSITIVE_DAMPING. */
 int nfft45_plan_create(const nfft45_grid* g, double damping_a, int eta, int m,
                        void* stream, nfft45_plan** out);
+/* Extension: build_plan with R = round(eta P) log-series terms for a
+ * fractional oversampling factor eta (see nfft45_v_samples_terms). */
+int nfft45_plan_create_terms(const nfft45_grid* g, double damping_a, int64_t R, int m,
+                             void* stream, nfft45_plan** out);
 void nfft45_plan_destroy(nfft45_plan* p);
 
 /* Plan tables (InversePlan fields, inverse.py:44-55; KernelData,

@@ -230,6 +230,21 @@ def v_samples(t, a: float, eta: int, m: int = SPREAD_HALF_WIDTH):
     return conv(t, np.ones(P, dtype=np.complex128), log_series(a, R), P, m)
 
 
+def v_samples_terms(t, a: float, R: int, m: int = SPREAD_HALF_WIDTH):
+    """EXTENSION, not in the reference (which requires R = eta P with integer
+    eta, grid.py:143-144, forward.py:149-154): v with R log-series terms for
+    any R >= 2.  Same steps as v_samples / conv (forward.py:133-162) except
+    that the fold onto P zero-pads the product to a whole number of slices
+    (a fractional oversampling factor eta = R / P, BASELINE config 5)."""
+    P = len(t)
+    lam = log_series(a, R)
+    prod = lam * type1(t, np.ones(P, dtype=np.complex128), R, m)
+    nsl = -(-R // P)
+    if nsl > 1 or R % P:
+        prod = np.concatenate([prod, np.zeros(nsl * P - R, dtype=prod.dtype)]).reshape(nsl, P).sum(axis=0)
+    return _idft_unscaled(prod.astype(np.complex128, copy=False))
+
+
 def kernel_samples(v, t):
     """exp(i pi P + 2 pi i sum t + v), with the overflow guard (lagrange.py:78-97)."""
     v = np.asarray(v, dtype=np.complex128)
@@ -287,9 +302,14 @@ class Plan:
 
     @classmethod
     def build(cls, t, a: float, eta: int = 2, m: int = SPREAD_HALF_WIDTH) -> "Plan":
+        """eta integer: the reference's build_plan.  eta fractional (eta * P an
+        integer): the extension of v_samples_terms."""
         t = np.asarray(t, dtype=np.float64)
         P = t.size
-        v = v_samples(t, a, eta, m)
+        if float(eta) == int(eta):
+            v = v_samples(t, a, int(eta), m)
+        else:
+            v = v_samples_terms(t, a, int(round(eta * P)), m)
         ks = kernel_samples(v, t)
         L = kernel_coeffs(ks, a)
         dL = derivative(L, t, m)

@@ -43,6 +43,8 @@ _SIGS = {
     "nfft45_dft": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _i64, _i64, ctypes.c_int, ctypes.c_void_p]),
     "nfft45_v_samples": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                         ctypes.c_void_p, ctypes.c_void_p]),
+    "nfft45_v_samples_terms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, _i64, ctypes.c_int,
+                                              ctypes.c_void_p, ctypes.c_void_p]),
     "nfft45_kernel_samples": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "nfft45_kernel_coefficients": (ctypes.c_int, [ctypes.c_void_p, _i64, ctypes.c_double, ctypes.c_void_p,
                                                   ctypes.c_void_p]),
@@ -52,6 +54,8 @@ _SIGS = {
                                                  ctypes.c_void_p]),
     "nfft45_plan_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "nfft45_plan_create_terms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, _i64, ctypes.c_int,
+                                                ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
     "nfft45_plan_destroy": (None, [ctypes.c_void_p]),
     "nfft45_plan_table": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
     "nfft45_type5": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _i64, ctypes.c_void_p, ctypes.c_void_p]),

@@ -327,9 +327,10 @@ static int type2_core(const GridDev& g, const double2* Sc, int64_t batch, int64_
   return NFFT45_OK;
 }
 
-static int v_core(const GridDev& g, double a, int eta, int m, double2* v, cudaStream_t st) {
+// R = number of log-series terms (eta P in the reference; any R >= 2 for the
+// fractional-oversampling extension: the fold then sums a partial last slice).
+static int v_core(const GridDev& g, double a, int64_t R, int m, double2* v, cudaStream_t st) {
   const int64_t P = g.Q;
-  const int64_t R = (int64_t)eta * P;
   Scratch lam(st), V(st);
   NFFT_CHECK(lam.alloc(sizeof(double2) * R));
   NFFT_CHECK(V.alloc(sizeof(double2) * P));
@@ -868,11 +869,15 @@ int nfft45_dft(const double* in, double* out, int64_t batch, int64_t N, int sign
 
 int nfft45_v_samples(const nfft45_grid* g, double a, int eta, int m, double* v, void* st) {
   if (!g || eta < 1 || m < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid v-samples arguments");
-  if ((int64_t)eta * g->d.Q < 2)
-    return fail(NFFT45_ERR_INVALID_ARGUMENT, "need eta * P >= 2 so the truncated series has at least one term");
+  return nfft45_v_samples_terms(g, a, (int64_t)eta * g->d.Q, m, v, st);
+}
+
+int nfft45_v_samples_terms(const nfft45_grid* g, double a, int64_t R, int m, double* v, void* st) {
+  if (!g || m < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid v-samples arguments");
+  if (R < 2) return fail(NFFT45_ERR_INVALID_ARGUMENT, "need eta * P >= 2 so the truncated series has at least one term");
   DeviceGuard dg(g->d.device);
   if (dg.status) return dg.status;
-  return v_core(g->d, a, eta, m, D2(v), S(st));
+  return v_core(g->d, a, R, m, D2(v), S(st));
 }
 
 int nfft45_kernel_samples(const nfft45_grid* g, const double* v, double* ks, void* st) {
@@ -924,11 +929,18 @@ int nfft45_derivative_samples(const nfft45_grid* g, const double* L, int m, doub
 
 int nfft45_plan_create(const nfft45_grid* g, double a, int eta, int m, void* st, nfft45_plan** out) {
   if (!g || !out) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid plan arguments");
-  if (!(a > 0.0)) return fail(NFFT45_ERR_NON_POSITIVE_DAMPING, "damping must be positive");
   if (eta < 1 || m < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "eta and m must be >= 1");
+  return nfft45_plan_create_terms(g, a, (int64_t)eta * g->d.Q, m, st, out);
+}
+
+int nfft45_plan_create_terms(const nfft45_grid* g, double a, int64_t R, int m, void* st, nfft45_plan** out) {
+  if (!g || !out) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid plan arguments");
+  if (!(a > 0.0)) return fail(NFFT45_ERR_NON_POSITIVE_DAMPING, "damping must be positive");
+  if (m < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "eta and m must be >= 1");
   const int64_t P = g->d.Q;
-  if ((int64_t)eta * P < 2)
+  if (R < 2)
     return fail(NFFT45_ERR_INVALID_ARGUMENT, "need eta * P >= 2 so the truncated series has at least one term");
+  const int eta = (int)((R + P - 1) / P);
   DeviceGuard dg(g->d.device);
   if (dg.status) return dg.status;
   cudaStream_t s = S(st);
@@ -964,7 +976,7 @@ int nfft45_plan_create(const nfft45_grid* g, double a, int eta, int m, void* st,
   {
     Scratch guard(s);
     status = guard.alloc(sizeof(double) * 2);
-    if (!status) status = v_core(g->d, a, eta, m, p->v, s);
+    if (!status) status = v_core(g->d, a, R, m, p->v, s);
     if (!status) status = ks_core(g->d, p->v, p->ks, guard.d(), s);
     if (!status) status = coeff_core(p->ks, P, a, p->L, s);
     if (!status) status = deriv_core(g->d, p->L, m, p->dL, guard.d() + 1, s);

@@ -8,6 +8,8 @@ stages); refine_type5/4 run the Section V residual passes inside the C call.
 
 from __future__ import annotations
 
+import os
+
 import ctypes
 import threading
 
@@ -106,7 +108,7 @@ def _charge_plan(f: FlopCounter | None, P: int, params: MethodParams):
     if f is None:
         return
     taps = 2 * params.spread_width + 1
-    R = params.eta * P
+    R = params.series_terms(P)
     f.complex_exp(R - 1)
     f.real_mul(R - 1)
     _fl.charge_type1(f, P, R, taps)
@@ -136,13 +138,18 @@ def build_plan(grid: NonuniformGrid, params: MethodParams, flops: FlopCounter | 
     """Precompute everything grid-dependent for type-4/type-5 solves (inverse.py:58-98)."""
     P = grid.size
     dev = _device.device_index(device)
-    kernel_fine = kernel_for_size(params.eta * P, params.spread_width)
+    R = params.series_terms(P)
+    kernel_fine = kernel_for_size(R, params.spread_width)
     kernel_base = kernel_for_size(P, params.spread_width)
     _amplification_check(P, params.damping_a)
     gptr = grid.device_handle(dev)
     out = ctypes.c_void_p()
-    _lib.call("nfft45_plan_create", gptr, float(params.damping_a), int(params.eta), int(params.spread_width),
-              _device.stream_handle(dev), ctypes.byref(out))
+    if params.fractional_eta:  # extension: R = eta P series terms, partial fold
+        _lib.call("nfft45_plan_create_terms", gptr, float(params.damping_a), R, int(params.spread_width),
+                  _device.stream_handle(dev), ctypes.byref(out))
+    else:
+        _lib.call("nfft45_plan_create", gptr, float(params.damping_a), int(params.eta), int(params.spread_width),
+                  _device.stream_handle(dev), ctypes.byref(out))
     _charge_plan(flops, P, params)
     return InversePlan(grid, params, _PlanHandle(out.value, grid), dev, kernel_fine, kernel_base)
 
@@ -172,7 +179,7 @@ def _charge_type4(f, P, taps):
 # Host-resident batches are streamed through the device in chunks of this many
 # signals: H2D of chunk i+1 and D2H of chunk i-1 (two copy streams, PCIe is
 # full duplex) overlap the solve of chunk i.
-STREAM_CHUNK = 64
+STREAM_CHUNK = int(os.environ.get("NFFT45_STREAM_CHUNK", "64"))
 
 
 def _solve_streamed(name: str, plan: InversePlan, host, passes, dest):

@@ -42,6 +42,29 @@ def test_params_validation():
 
 # --- validate_grid (grid.py:64-96) through the C library ---------------------------
 
+def test_fractional_eta_extension_params():
+    """The reference contract (integer eta, grid.py:143-144) is the default;
+    fractional_eta=True is the config-5 extension, eta * P must be integral."""
+    with pytest.raises(ValueError):
+        nf.MethodParams.from_mu(1e-15, 4096, 1.5)
+    prm = nf.MethodParams.from_mu(1e-15, 4096, 1.5, fractional_eta=True)
+    assert prm.series_terms(4096) == 6144
+    assert prm.damping_a == nf.damping_from_mu(1e-15, 4096, 1.5)
+    with pytest.raises(ValueError):
+        prm.series_terms(4095)
+    with pytest.raises(ValueError):
+        nf.MethodParams(damping_a=0.1, eta=0.5, mu=1e-3, fractional_eta=True)
+    assert nf.MethodParams.from_mu(1e-15, 64, 2).series_terms(64) == 128
+
+
+@pytest.mark.parametrize("eta", [1, 2, 3])
+def test_oracle_series_terms_restatement_reduces_to_reference(eta):
+    """v_samples_terms (extension) with R = eta P is the reference's v_samples, bitwise."""
+    t, _ = O.make_inputs(16, 0.3, 1, 5)
+    a = O.damping(1e-12, 16, eta)
+    assert np.array_equal(O.v_samples_terms(t, a, eta * 16), O.v_samples(t, a, eta))
+
+
 def test_validate_grid_semantics():
     g = nf.validate_grid([0.5, 0.25, 0.75, 0.0])
     assert list(g.order) == [3, 1, 0, 2]
