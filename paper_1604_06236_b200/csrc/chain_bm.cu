@@ -94,10 +94,10 @@ template <int L, int S>
 __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<L, kSig>())) kbm_col(
     const double2* __restrict__ in, double2* __restrict__ out, int L2, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ lo, const double2* __restrict__ hi, int sh, const double2* __restrict__ twQ, int Q,
-    const double* __restrict__ pre) {
+    const double* __restrict__ pre, int sw) {
   extern __shared__ double2 sm[];
-  const int n2 = blockIdx.x;
-  const int64_t b0 = (int64_t)blockIdx.y * kSig;
+  const int n2 = sw ? blockIdx.y : blockIdx.x;
+  const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * kSig;
   auto ld = [&](int i, int c) -> double2 {
     const int64_t idx = (int64_t)i * L2 + n2;
     double2 v = in[idx * Bp + b0 + c];
@@ -121,14 +121,14 @@ __global__ void __launch_bounds__(2 * M * SG / Tr1::E, Tr1::E == 8 ? 2 : bm_minb
     const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
-    const double* __restrict__ dd, const double2* __restrict__ sub) {
+    const double* __restrict__ dd, const double2* __restrict__ sub, int sw) {
   constexpr int NR = 2 * M;
   extern __shared__ double2 sm[];
   double* s_t0 = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + fast_smem<NR, SG>());
   double* s_t1 = s_t0 + M;
   double2* s_sb = reinterpret_cast<double2*>(s_t1 + M);
-  const int k1 = blockIdx.x;
-  const int64_t b0 = (int64_t)blockIdx.y * SG;
+  const int k1 = sw ? blockIdx.y : blockIdx.x;
+  const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * SG;
   for (int m1 = threadIdx.x; m1 < M; m1 += blockDim.x) {
     const int64_t p = (int64_t)k1 + (int64_t)M * m1;
     if (sub) {
@@ -169,11 +169,11 @@ template <int M>
 __global__ void __launch_bounds__(fast_threads<M, kSig>(), bm_minb(fast_threads<M, kSig>())) kbm_mid(
     const double2* __restrict__ U, double2* __restrict__ Z, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
-    const double2* __restrict__ ks) {
+    const double2* __restrict__ ks, int sw) {
   extern __shared__ double2 sm[];
   double2* s_ks = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + fast_smem<M, kSig>());
-  const int r = blockIdx.x;
-  const int64_t b0 = (int64_t)blockIdx.y * kSig;
+  const int r = sw ? blockIdx.y : blockIdx.x;
+  const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * kSig;
   for (int k2 = threadIdx.x; k2 < M; k2 += blockDim.x) cpa16(&s_ks[k2], &ks[(int64_t)r + (int64_t)M * k2]);
   cpa_commit();
   auto ld1 = [&](int i, int c) -> double2 { return U[((int64_t)r * M + i) * Bp + b0 + c]; };
@@ -193,15 +193,15 @@ __global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_thread
     const double2* __restrict__ Z, double2* __restrict__ Y, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
-    const double* __restrict__ cd, const double2* __restrict__ xsub, double2* __restrict__ xout) {
+    const double* __restrict__ cd, const double2* __restrict__ xsub, double2* __restrict__ xout, int sw) {
   constexpr int NC = 2 * M;
   constexpr bool kLead2 = FastTraits<NC>::radix(0) == 2;
   extern __shared__ double2 sm[];
   double* s_t0 = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + fast_smem<NC, SG>());
   double* s_t1 = s_t0 + M;
   double2* s_xs = reinterpret_cast<double2*>(s_t1 + M);
-  const int r = blockIdx.x;
-  const int64_t b0 = (int64_t)blockIdx.y * SG;
+  const int r = sw ? blockIdx.y : blockIdx.x;
+  const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * SG;
   // per-tile tables (and the xsub tile) staged with cp.async, waited for at
   // the end of the first FFT pass
   for (int k2 = threadIdx.x; k2 < M; k2 += blockDim.x) {
@@ -369,10 +369,10 @@ __global__ void __launch_bounds__(2 * M * kSig / Tr1::E, 1) kbm_band_p(
 template <int L, int S>
 __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<L, kSig>())) kbm_row(const double2* __restrict__ in,
                                                                   double2* __restrict__ out, int64_t Bp, int64_t R1,
-                                                                  const double2* __restrict__ tw) {
+                                                                  const double2* __restrict__ tw, int sw) {
   extern __shared__ double2 sm[];
-  const int r = blockIdx.x;
-  const int64_t b0 = (int64_t)blockIdx.y * kSig;
+  const int r = sw ? blockIdx.y : blockIdx.x;
+  const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * kSig;
   auto ld = [&](int i, int c) -> double2 { return in[((int64_t)r * L + i) * Bp + b0 + c]; };
   auto st = [&](int k, int c, double2 v) { out[((int64_t)r + R1 * k) * Bp + b0 + c] = v; };
   fast_tile_fft<L, kSig, S, true>(sm, ld, st, tw);
@@ -451,6 +451,11 @@ struct ChainBM {
   bool persistent = true;
   bool small_tiles = false;  // 4-signal tiles for the two-FFT kernels
   bool e8 = false;           // experiment: radix-8 / 8-element schedule for the 2M-point stage
+  bool sw = false;           // grid order: signal groups fastest (blockIdx.x) instead of tile index
+  // grid of (tiles x groups*mult); with sw the signal groups run fastest
+  dim3 gdim(int tiles, int mult = 1) const {
+    return sw ? dim3(groups * mult, (unsigned)tiles) : dim3((unsigned)tiles, groups * mult);
+  }
 
   int qtab(int64_t Q, const double2** out) {
     int status = NFFT45_OK;
@@ -470,8 +475,7 @@ struct ChainBM {
     const int64_t Q = N / last_stride<L>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    LAUNCH(bm_col, dim3((unsigned)L2, groups), T, smem, st, in, out, L2, Bp, tw, t4->lo, t4->hi, t4->s, twQ, (int)Q,
-           pre);
+    LAUNCH(bm_col, gdim(L2), T, smem, st, in, out, L2, Bp, tw, t4->lo, t4->hi, t4->s, twQ, (int)Q, pre, (int)sw);
     return NFFT45_OK;
   }
 
@@ -501,22 +505,22 @@ struct ChainBM {
       const size_t smem4 = fast_smem<2 * M, 4>() + 2 * sizeof(double) * M + (sub ? sizeof(double2) * M * 4 : 0);
       NFFT_CHECK(bm_attr(bm_band4, smem4));
       constexpr int T4 = fast_threads<2 * M, 4>();
-      LAUNCH(bm_band4, dim3((unsigned)M, groups * 2), T4, smem4, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi,
-             t.tP->s, twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
+      LAUNCH(bm_band4, gdim(M, 2), T4, smem4, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q,
+             pv.deconv, pv.decay, pv.dd, sub, (int)sw);
       return NFFT45_OK;
     }
     const size_t smem = fast_smem<2 * M, kSig>() + 2 * sizeof(double) * M + (sub ? sizeof(double2) * M * kSig : 0);
     if (e8) {
       auto bm_band8 = kbm_band<M, kSig, FastTraitsE8<2 * M>>;
       NFFT_CHECK(bm_attr(bm_band8, smem));
-      LAUNCH(bm_band8, dim3((unsigned)M, groups), 2 * M * kSig / 8, smem, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo,
-             t.tP->hi, t.tP->s, twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
+      LAUNCH(bm_band8, gdim(M), 2 * M * kSig / 8, smem, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s,
+             twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub, (int)sw);
       return NFFT45_OK;
     }
     auto bm_band = kbm_band<M, kSig>;
     NFFT_CHECK(bm_attr(bm_band, smem));
-    LAUNCH(bm_band, dim3((unsigned)M, groups), T, smem, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s,
-           twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
+    LAUNCH(bm_band, gdim(M), T, smem, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q,
+           pv.deconv, pv.decay, pv.dd, sub, (int)sw);
     return NFFT45_OK;
   }
 
@@ -528,8 +532,7 @@ struct ChainBM {
     const int64_t Q = P / last_stride<M>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    LAUNCH(bm_mid, dim3((unsigned)M, groups), T, smem, st, U, Z, Bp, t.twM, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q,
-           pv.ks);
+    LAUNCH(bm_mid, gdim(M), T, smem, st, U, Z, Bp, t.twM, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.ks, (int)sw);
     return NFFT45_OK;
   }
 
@@ -552,15 +555,15 @@ struct ChainBM {
       const size_t smem4 = fast_smem<2 * M, 4>() + 2 * sizeof(double) * M + (xout && xsub ? sizeof(double2) * M * 4 : 0);
       NFFT_CHECK(bm_attr(bm_pad4, smem4));
       constexpr int T4 = fast_threads<2 * M, 4>();
-      LAUNCH(bm_pad4, dim3((unsigned)M, groups * 2), T4, smem4, st, Z, Y, Bp, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s,
-             twQ, (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout);
+      LAUNCH(bm_pad4, gdim(M, 2), T4, smem4, st, Z, Y, Bp, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q,
+             pv.coef, pv.deconv, pv.cd, xsub, xout, (int)sw);
       return NFFT45_OK;
     }
     auto bm_pad = kbm_pad<M, kSig>;
     const size_t smem = fast_smem<2 * M, kSig>() + 2 * sizeof(double) * M + (xout && xsub ? sizeof(double2) * M * kSig : 0);
     NFFT_CHECK(bm_attr(bm_pad, smem));
-    LAUNCH(bm_pad, dim3((unsigned)M, groups), T, smem, st, Z, Y, Bp, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s, twQ,
-           (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout);
+    LAUNCH(bm_pad, gdim(M), T, smem, st, Z, Y, Bp, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q, pv.coef,
+           pv.deconv, pv.cd, xsub, xout, (int)sw);
     return NFFT45_OK;
   }
 
@@ -570,7 +573,7 @@ struct ChainBM {
     constexpr size_t smem = fast_smem<M, kSig>();
     NFFT_CHECK(bm_attr(bm_row, smem));
     constexpr int T = fast_threads<M, kSig>();
-    LAUNCH(bm_row, dim3((unsigned)(2 * M), groups), T, smem, st, Y, H, Bp, (int64_t)(2 * M), t.twM);
+    LAUNCH(bm_row, gdim(2 * M), T, smem, st, Y, H, Bp, (int64_t)(2 * M), t.twM, (int)sw);
     return NFFT45_OK;
   }
 
@@ -622,6 +625,12 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
     ch.small_tiles = small;
     static const bool e8 = getenv("NFFT45_E8") != nullptr;
     ch.e8 = e8;
+    // signal groups fastest in the grid: concurrently resident tiles then
+    // cover whole 16-KB rows of the batch-minor layout (DRAM locality; row
+    // pass -22 %, column pass -8 % on B200).  NFFT45_GRID_TILES_FIRST restores
+    // the tile-major order for A/B runs.
+    static const bool tiles_first = getenv("NFFT45_GRID_TILES_FIRST") != nullptr;
+    ch.sw = !tiles_first;
   }
   int status = NFFT45_OK;
   {
