@@ -385,11 +385,11 @@ template <int M, int RW>
 __global__ void __launch_bounds__(fast_threads<M, 4 * RW>(), bm_minb(fast_threads<M, 4 * RW>())) kbm_colin(
     const double2* __restrict__ A, int64_t batch, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
-    const double* __restrict__ decay, double2* __restrict__ AT) {
+    const double* __restrict__ decay, double2* __restrict__ AT, int sw) {
   constexpr int64_t P = (int64_t)M * M;
   extern __shared__ double2 sm[];
-  const int m20 = blockIdx.x * RW;
-  const int64_t bb = (int64_t)blockIdx.y * 4;
+  const int m20 = (sw ? blockIdx.y : blockIdx.x) * RW;
+  const int64_t bb = (int64_t)(sw ? blockIdx.x : blockIdx.y) * 4;
   auto ld = [&](int i, int c) -> double2 {
     const int64_t idx = (int64_t)i * M + m20 + (c % RW);
     const int64_t b = bb + c / RW;
@@ -409,11 +409,11 @@ __global__ void __launch_bounds__(fast_threads<M, 4 * RW>(), bm_minb(fast_thread
 template <int M, int RW>
 __global__ void __launch_bounds__(fast_threads<M, 4 * RW>(), bm_minb(fast_threads<M, 4 * RW>())) kbm_rowout(
     const double2* __restrict__ Z, double2* __restrict__ out, int64_t batch, int64_t Bp,
-    const double2* __restrict__ tw, const double* __restrict__ coef, const double2* __restrict__ xsub) {
+    const double2* __restrict__ tw, const double* __restrict__ coef, const double2* __restrict__ xsub, int sw) {
   constexpr int64_t P = (int64_t)M * M;
   extern __shared__ double2 sm[];
-  const int r0 = blockIdx.x * RW;
-  const int64_t bb = (int64_t)blockIdx.y * 4;
+  const int r0 = (sw ? blockIdx.y : blockIdx.x) * RW;
+  const int64_t bb = (int64_t)(sw ? blockIdx.x : blockIdx.y) * 4;
   auto ld = [&](int i, int c) -> double2 {
     return Z[((int64_t)(r0 + (c % RW)) * M + i) * Bp + bb + c / RW];
   };
@@ -586,8 +586,10 @@ struct ChainBM {
     const int64_t Q = P / last_stride<M>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    LAUNCH(bm_colin, dim3((unsigned)(M / RW), (unsigned)(Bp / 4)), T, smem, st, A, batch, U, Bp, t.twM, t.tP->lo,
-           t.tP->hi, t.tP->s, twQ, (int)Q, pv.decay, AT);
+    static const int bsw = getenv("NFFT45_BOUNDARY_SWAP") != nullptr;
+    const dim3 grid = bsw ? dim3((unsigned)(Bp / 4), (unsigned)(M / RW)) : dim3((unsigned)(M / RW), (unsigned)(Bp / 4));
+    LAUNCH(bm_colin, grid, T, smem, st, A, batch, U, Bp, t.twM, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.decay,
+           AT, bsw);
     return NFFT45_OK;
   }
 
@@ -597,8 +599,9 @@ struct ChainBM {
     constexpr size_t smem = fast_smem<M, 4 * RW>();
     NFFT_CHECK(bm_attr(bm_rowout, smem));
     constexpr int T = fast_threads<M, 4 * RW>();
-    LAUNCH(bm_rowout, dim3((unsigned)(M / RW), (unsigned)(Bp / 4)), T, smem, st, Z, out, batch, Bp, t.twM, pv.coef,
-           xsub);
+    static const int bsw = getenv("NFFT45_BOUNDARY_SWAP") != nullptr;
+    const dim3 grid = bsw ? dim3((unsigned)(Bp / 4), (unsigned)(M / RW)) : dim3((unsigned)(M / RW), (unsigned)(Bp / 4));
+    LAUNCH(bm_rowout, grid, T, smem, st, Z, out, batch, Bp, t.twM, pv.coef, xsub, bsw);
     return NFFT45_OK;
   }
 };

@@ -9,6 +9,7 @@
 // accumulation order is fixed (ascending nodes / ascending cells), so
 // results are bitwise reproducible and independent of the batch split.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.cuh"
 
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
                                                     int64_t Q, int64_t n, double alpha, GaussTab G,
                                                     const double2* __restrict__ amp, int64_t batch, NodeFactor nf,
                                                     double2* __restrict__ H, const int2* __restrict__ ranges, int NS,
-                                                    int64_t amp_ld, int64_t H_ld, int ngroups) {
+                                                    int64_t amp_ld, int64_t H_ld, int ngroups, int sw) {
   constexpr int SIG = 32 * SPL;
   extern __shared__ __align__(16) unsigned char smraw[];
   double2* A0 = reinterpret_cast<double2*>(smraw);                        // [cap][SIG]
@@ -269,13 +270,16 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
   __shared__ int s_off[8];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t j0 = (int64_t)blockIdx.x * kSpreadTile;
+  // sw: slices (signal-group walkers) fastest in the grid, tiles second
+  const unsigned bx = sw ? blockIdx.y : blockIdx.x, by = sw ? blockIdx.x : blockIdx.y;
+  const unsigned gy = sw ? gridDim.x : gridDim.y;
+  const int64_t j0 = (int64_t)bx * kSpreadTile;
   const int jw = (int)j0 + warp * kCPW;
   const int64_t s_lo = floordiv_b(-kM - (min(j0 + kSpreadTile, n) - 1) + n - 1, n);
   if (tid == 0) {
     int acc = 0;
     for (int si = 0; si < NS && si < 8; si++) {
-      int2 r = ranges[blockIdx.x * (int64_t)NS + si];
+      int2 r = ranges[bx * (int64_t)NS + si];
       s_off[si] = acc;
       s_cnt[si] = r.y - r.x;
       acc += r.y - r.x;
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
   auto node_at = [&](int g, int& si) -> int64_t {
     si = 0;
     while (si + 1 < NS && si + 1 < 8 && g >= s_off[si + 1]) si++;
-    return ranges[blockIdx.x * (int64_t)NS + si].x + (g - s_off[si]);
+    return ranges[bx * (int64_t)NS + si].x + (g - s_off[si]);
   };
   // geometry + padded weight rows + factors of nodes [base, base+cnt)
   auto prep_nodes = [&](int base, int cnt) {
@@ -430,13 +434,13 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
     prep_nodes(0, total);
     __syncthreads();
     compact(total);
-    int64_t g = blockIdx.y;
+    int64_t g = by;
     if (g < ngroups) stage(A0, g, total);
-    for (int it = 0; g < ngroups; it++, g += gridDim.y) {
+    for (int it = 0; g < ngroups; it++, g += gy) {
       double2* cur = (it & 1) ? A1 : A0;
       double2* nxt = (it & 1) ? A0 : A1;
-      if (g + gridDim.y < ngroups) {
-        stage(nxt, g + gridDim.y, total);
+      if (g + gy < ngroups) {
+        stage(nxt, g + gy, total);
         cp_async_wait_group<1>();
       } else {
         cp_async_wait_group<0>();
@@ -452,7 +456,7 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
       __syncthreads();  // `cur` is refilled two iterations later
     }
   } else {
-    for (int64_t g = blockIdx.y; g < ngroups; g += gridDim.y) {
+    for (int64_t g = by; g < ngroups; g += gy) {
       double2 acc[kCPW][SPL];
 #pragma unroll
       for (int c = 0; c < kCPW; c++)
@@ -486,11 +490,15 @@ int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const doubl
   const int ngroups = (int)ceil_div(H_ld, SIG);
   // enough CTAs for ~2 waves of 148 SMs, each walking several signal groups
   int slices = (int)std::min<int64_t>(ngroups, std::max<int64_t>(1, ceil_div(4 * 148, ntiles)));
+  static const int env_sl = getenv("NFFT45_SPREAD_SLICES") ? atoi(getenv("NFFT45_SPREAD_SLICES")) : 0;
+  const int sw = env_sl > 0;
+  if (env_sl > 0) slices = (int)std::min<int64_t>(ngroups, env_sl);
   size_t smem = (size_t)2 * kPipeCap * SIG * 16 + (size_t)kPipeCap * kWRow * 8 + kPipeCap * 16 + kPipeCap * 16;
   auto spread_p = k_spread_p<1>;
   NFFT_CUDA(cudaFuncSetAttribute(spread_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  LAUNCH(spread_p, dim3((unsigned)ntiles, (unsigned)slices), 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha,
-         gauss_tab(win), amp, batch, f, H, ranges, NS, amp_ld, H_ld, ngroups);
+  const dim3 grid = sw ? dim3((unsigned)slices, (unsigned)ntiles) : dim3((unsigned)ntiles, (unsigned)slices);
+  LAUNCH(spread_p, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), amp, batch, f, H, ranges,
+         NS, amp_ld, H_ld, ngroups, sw);
   if (own) NFFT_CUDA(cudaFreeAsync(own, st));
   return NFFT45_OK;
 }
@@ -739,7 +747,7 @@ template <bool OUT_BM, int SUBM, int SIG>  // SUBM: 0 none, 1 batch-minor, 2 sig
 __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 ? 4 : 5)) k_gather_p(
     const double* __restrict__ ts, const int* __restrict__ perm, int64_t Q, int64_t n, double alpha, GaussTab G,
     const double2* __restrict__ H, int64_t H_ld, int64_t batch, NodeFactor nf, const double2* __restrict__ sub,
-    int64_t sub_ld, int mode, double2* __restrict__ out, int64_t out_ld, int ngroups, int* __restrict__ overflow) {
+    int64_t sub_ld, int mode, double2* __restrict__ out, int64_t out_ld, int ngroups, int* __restrict__ overflow, int sw) {
   constexpr int HALVES = 32 / SIG, NPL = kNPW / HALVES;
   static_assert(kGatherNodes == 32, "one node per lane in the signal-major staging");
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -753,8 +761,11 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
   __shared__ int s_pq[kGatherNodes];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // sw: slices (signal-group walkers) fastest in the grid, node blocks second
+  const unsigned bx = sw ? blockIdx.y : blockIdx.x, by = sw ? blockIdx.x : blockIdx.y;
+  const unsigned gy = sw ? gridDim.x : gridDim.y;
   const int sl = lane % SIG, hf = lane / SIG;
-  const int64_t q0 = (int64_t)blockIdx.x * kGatherNodes;
+  const int64_t q0 = (int64_t)bx * kGatherNodes;
   const int nq = (int)min((int64_t)kGatherNodes, Q - q0);
   if (tid < kGatherNodes) {
     const int e = tid < nq ? tid : nq - 1;
@@ -772,7 +783,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
   const int len = ce - cs + 1;
   const int w_lo = s_c0[warp * kNPW] - kM, w_hi = s_c0[warp * kNPW + kNPW - 1] + kM;
   if (len > kGPSpan || w_hi - w_lo + 1 > kWTSpan || n < (int64_t)kGPSpan + 2 * kM + 2) {
-    if (tid == 0 && blockIdx.y == 0) overflow[blockIdx.x] = 1;  // handled by the fallback kernel
+    if (tid == 0 && by == 0) overflow[bx] = 1;  // handled by the fallback kernel
     return;
   }
   // per-warp dense weight table over the warp's cells, built once
@@ -811,12 +822,12 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
     }
     cp_async_commit();
   };
-  int64_t g = blockIdx.y;
+  int64_t g = by;
   if (g < ngroups) stage(g);
   const double2* __restrict__ yw = Y + (w_lo - cs) * SIG + sl;
   const double2* __restrict__ wr0 = reinterpret_cast<const double2*>(wt) + hf * (NPL / 2);
   const int e0 = warp * kNPW + hf * NPL;  // node of acc[0]
-  for (; g < ngroups; g += gridDim.y) {
+  for (; g < ngroups; g += gy) {
     const int64_t b0 = g * SIG;
     cp_async_wait_group<0>();
     __syncthreads();
@@ -843,7 +854,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
       }
     }
     __syncthreads();  // Y (and Sb) consumed: prefetch the next group during the epilogue
-    if (g + gridDim.y < ngroups) stage(g + gridDim.y);
+    if (g + gy < ngroups) stage(g + gy);
     if constexpr (OUT_BM) {
       const int64_t b = b0 + sl;
 #pragma unroll
@@ -896,21 +907,26 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
   }();
   const int64_t nblk = ceil_div(g.Q, kGatherNodes);
   const int ngroups = (int)ceil_div(out_ld ? out_ld : batch, SIG);
-  const int slices = (int)std::min<int64_t>(ngroups, std::max<int64_t>(1, ceil_div(4 * 148, nblk)));
+  // at least 4 signal-group walkers per node block, walkers fastest in the
+  // grid (concurrent CTAs then read 4 groups of each cell row: -4 % on C4)
+  int slices = (int)std::min<int64_t>(ngroups, std::max<int64_t>(4, ceil_div(4 * 148, nblk)));
+  static const int env_sl = getenv("NFFT45_GATHER_SLICES") ? atoi(getenv("NFFT45_GATHER_SLICES")) : 0;
+  const int sw = 1;
+  if (env_sl > 0) slices = (int)std::min<int64_t>(ngroups, env_sl);
   int* overflow = nullptr;
   NFFT_CUDA(cudaMallocAsync(&overflow, sizeof(int) * nblk, st));
   LAUNCH(k_overflow_clear, (unsigned)ceil_div(nblk, 256), 256, 0, st, overflow, nblk);
   const int subm = mode == 0 ? 0 : (sub_ld ? 1 : 2);
   size_t smem = (size_t)kGPSpan * SIG * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8 +
                 (subm == 2 ? (size_t)kGatherNodes * SIG * 16 : 0) + (out_ld ? 0 : (size_t)kGatherNodes * SIG * 16);
-  dim3 grid((unsigned)nblk, (unsigned)slices);
+  const dim3 grid = sw ? dim3((unsigned)slices, (unsigned)nblk) : dim3((unsigned)nblk, (unsigned)slices);
   GaussTab G = gauss_tab(win);
 #define NFFT_GP_LAUNCH(OBM, SM_, S_)                                                                           \
   {                                                                                                          \
     auto gather_p = k_gather_p<OBM, SM_, S_>;                                                                \
     NFFT_CUDA(cudaFuncSetAttribute(gather_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
     LAUNCH(gather_p, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, H_ld, batch, f,  \
-           sub, sub_ld, mode, out, out_ld, ngroups, overflow);                                               \
+           sub, sub_ld, mode, out, out_ld, ngroups, overflow, sw);                                           \
   }
 #define NFFT_GP_SUB(OBM, S_) \
   if (subm == 0) NFFT_GP_LAUNCH(OBM, 0, S_) else if (subm == 1) NFFT_GP_LAUNCH(OBM, 1, S_) else NFFT_GP_LAUNCH(OBM, 2, S_)
