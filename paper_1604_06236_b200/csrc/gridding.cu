@@ -106,9 +106,46 @@ struct RangeCache {
     int m, TC, NS;
     int2* d;
   };
+  struct Flags {
+    int64_t n;
+    int* d;
+    bool any;
+  };
   std::mutex mu;
   std::vector<Entry> v;
+  std::vector<Flags> gf;  // persistent-gather overflow flags per fine-grid size
 };
+
+int gather_flags_cache(const GridDev& g, int64_t n, cudaStream_t st) {
+  if (!g.rc) return NFFT45_OK;
+  {
+    std::lock_guard<std::mutex> lk(g.rc->mu);
+    for (const auto& e : g.rc->gf)
+      if (e.n == n) return NFFT45_OK;
+  }
+  const int64_t nblk = gather_blocks(g.Q);
+  int* d = nullptr;
+  NFFT_CUDA(cudaMalloc(&d, sizeof(int) * (nblk + 1)));
+  NFFT_CHECK(gather_flags_compute(g, n, d, d + nblk, st));
+  int any = 0;
+  NFFT_CUDA(cudaMemcpyAsync(&any, d + nblk, sizeof(int), cudaMemcpyDeviceToHost, st));
+  NFFT_CUDA(cudaStreamSynchronize(st));
+  std::lock_guard<std::mutex> lk(g.rc->mu);
+  g.rc->gf.push_back({n, d, any != 0});
+  return NFFT45_OK;
+}
+
+bool gather_flags_lookup(const GridDev& g, int64_t n, int** flags, bool* any) {
+  if (!g.rc) return false;
+  std::lock_guard<std::mutex> lk(g.rc->mu);
+  for (const auto& e : g.rc->gf)
+    if (e.n == n) {
+      *flags = e.d;
+      *any = e.any;
+      return true;
+    }
+  return false;
+}
 
 int tile_ranges(const GridDev& g, int64_t n, int m, int TC, int NS, cudaStream_t st, const int2** out, int2** own) {
   *own = nullptr;
@@ -153,6 +190,7 @@ RangeCache* range_cache_new() { return new RangeCache(); }
 void tile_ranges_free(GridDev& g) {
   if (!g.rc) return;
   for (auto& e : g.rc->v) cudaFree(e.d);
+  for (auto& e : g.rc->gf) cudaFree(e.d);
   delete g.rc;
   g.rc = nullptr;
 }

@@ -891,6 +891,32 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
   }
 }
 
+// Node blocks that k_gather_p cannot stage (same condition as its early
+// return): a property of the node set and n only, so it is computed once per
+// plan and the fallback launch is skipped when no block overflows.
+__global__ void k_gather_flags(const double* __restrict__ ts, int64_t Q, int64_t n, int64_t nblk,
+                               int* __restrict__ flags, int* __restrict__ any) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= nblk) return;
+  const int64_t q0 = b * kGatherNodes;
+  const int nq = (int)min((int64_t)kGatherNodes, Q - q0);
+  auto c0 = [&](int e) { return node_geo(ts[q0 + (e < nq ? e : nq - 1)], (double)n).i0; };
+  bool of = (int64_t)(c0(kGatherNodes - 1) + kM) - (c0(0) - kM) + 1 > kGPSpan || n < (int64_t)kGPSpan + 2 * kM + 2;
+  for (int w = 0; w < kGatherWarps; w++)
+    of = of || (c0(w * kNPW + kNPW - 1) + kM) - (c0(w * kNPW) - kM) + 1 > kWTSpan;
+  flags[b] = of ? 1 : 0;
+  if (of) atomicOr(any, 1);
+}
+
+int gather_flags_compute(const GridDev& g, int64_t n, int* flags, int* any, cudaStream_t st) {
+  const int64_t nblk = ceil_div(g.Q, kGatherNodes);
+  NFFT_CUDA(cudaMemsetAsync(any, 0, sizeof(int), st));
+  LAUNCH(k_gather_flags, (unsigned)ceil_div(nblk, 128), 128, 0, st, g.ts, g.Q, n, nblk, flags, any);
+  return NFFT45_OK;
+}
+
+int64_t gather_blocks(int64_t Q) { return ceil_div(Q, kGatherNodes); }
+
 __global__ void k_overflow_clear(int* f, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) f[i] = 0;
@@ -913,9 +939,15 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
   static const int env_sl = getenv("NFFT45_GATHER_SLICES") ? atoi(getenv("NFFT45_GATHER_SLICES")) : 0;
   const int sw = 1;
   if (env_sl > 0) slices = (int)std::min<int64_t>(ngroups, env_sl);
+  // overflow flags: the plan's precomputed table (fallback launched only if
+  // some block overflows), else a per-call table filled by the kernel
   int* overflow = nullptr;
-  NFFT_CUDA(cudaMallocAsync(&overflow, sizeof(int) * nblk, st));
-  LAUNCH(k_overflow_clear, (unsigned)ceil_div(nblk, 256), 256, 0, st, overflow, nblk);
+  bool cached_any = true;
+  const bool cached = gather_flags_lookup(g, n, &overflow, &cached_any);
+  if (!cached) {
+    NFFT_CUDA(cudaMallocAsync(&overflow, sizeof(int) * nblk, st));
+    LAUNCH(k_overflow_clear, (unsigned)ceil_div(nblk, 256), 256, 0, st, overflow, nblk);
+  }
   const int subm = mode == 0 ? 0 : (sub_ld ? 1 : 2);
   size_t smem = (size_t)kGPSpan * SIG * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8 +
                 (subm == 2 ? (size_t)kGatherNodes * SIG * 16 : 0) + (out_ld ? 0 : (size_t)kGatherNodes * SIG * 16);
@@ -940,8 +972,8 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
 #undef NFFT_GP_SUB
 #undef NFFT_GP_LAUNCH
   // blocks that overflowed the staging buffers: recompute them with the chunked kernel
-  NFFT_CHECK(gather_fallback(g, n, win, H, batch, f, sub, mode, out, st, H_ld, sub_ld, out_ld, overflow));
-  NFFT_CUDA(cudaFreeAsync(overflow, st));
+  if (cached_any) NFFT_CHECK(gather_fallback(g, n, win, H, batch, f, sub, mode, out, st, H_ld, sub_ld, out_ld, overflow));
+  if (!cached) NFFT_CUDA(cudaFreeAsync(overflow, st));
   return NFFT45_OK;
 }
 

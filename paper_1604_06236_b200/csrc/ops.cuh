@@ -25,6 +25,12 @@ int tile_ranges(const GridDev& g, int64_t n, int m, int TC, int NS, cudaStream_t
 int tile_ranges_cache(const GridDev& g, int64_t n, int m, int TC, cudaStream_t st);
 void tile_ranges_free(GridDev& g);
 RangeCache* range_cache_new();
+// Per-node-block overflow flags of the persistent gather for a fine grid of n
+// cells (gridding_b.cu): cached per node set at plan creation.
+int gather_flags_compute(const GridDev& g, int64_t n, int* flags, int* any, cudaStream_t st);
+int64_t gather_blocks(int64_t Q);
+int gather_flags_cache(const GridDev& g, int64_t n, cudaStream_t st);
+bool gather_flags_lookup(const GridDev& g, int64_t n, int** flags, bool* any);
 inline int tile_images(int64_t n, int m, int TC) { return (int)((2 * m + TC - 1) / n + 3); }
 
 // Gaussian taps exp(-alpha k^2), k = 0..kFastM (for the factorised weights).
