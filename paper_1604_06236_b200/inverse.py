@@ -182,8 +182,12 @@ def _charge_type4(f, P, taps):
 STREAM_CHUNK = int(os.environ.get("NFFT45_STREAM_CHUNK", "64"))
 
 
-def _solve_streamed(name: str, plan: InversePlan, host, passes, dest):
-    """Pipelined host -> device -> host solve of a [batch, P] CPU tensor."""
+def _solve_streamed(name: str, plan: InversePlan, host, passes, dest, non_blocking: bool = False):
+    """Pipelined host -> device -> host solve of a [batch, P] CPU tensor.
+
+    non_blocking (extension, torch's copy_ semantics): return once the copies
+    and solves are enqueued; the result in `dest` (pinned) is valid after the
+    caller synchronizes the current stream (or the device)."""
     torch = _device.torch
     dev = plan.device
     B, P = host.shape
@@ -220,17 +224,27 @@ def _solve_streamed(name: str, plan: InversePlan, host, passes, dest):
             d2h.wait_event(done[k])
             dest[lo:hi].copy_(bufs_out[k][:m], non_blocking=True)
             drained[k].record(d2h)
-    d2h.synchronize()
+    # the staging buffers are in flight on the copy streams: keep the caching
+    # allocator from handing them out again before those streams pass here
+    for b in bufs_in:
+        b.record_stream(h2d)
+    for b in bufs_out:
+        b.record_stream(d2h)
+    main.wait_stream(h2d)
     main.wait_stream(d2h)
+    if not non_blocking:
+        d2h.synchronize()
     return dest
 
 
-def _solve(name: str, plan: InversePlan, data, label: str, passes: int | None, dest=None):
+def _solve(name: str, plan: InversePlan, data, label: str, passes: int | None, dest=None,
+           non_blocking: bool = False):
     torch = _device.torch
     if (isinstance(data, torch.Tensor) and not data.is_cuda and data.dim() == 2
             and data.shape[0] > STREAM_CHUNK and data.shape[-1] == plan.size
             and (dest is None or not dest.is_cuda)):
-        return _solve_streamed(name, plan, data, passes, dest)
+        return _solve_streamed(name, plan, data, passes, dest,
+                               non_blocking and dest is not None and dest.is_pinned())
     a = _device.operand(data, plan.device, length=plan.size, name=label)
     if dest is not None and dest.is_cuda and dest.dtype == _device.torch.complex128 and dest.is_contiguous():
         out = dest.reshape(a.tensor.shape)
@@ -245,28 +259,30 @@ def _solve(name: str, plan: InversePlan, data, label: str, passes: int | None, d
     return a.finish(out, dest)
 
 
-def type5(plan: InversePlan, samples, flops: FlopCounter | None = None, out=None):
+def type5(plan: InversePlan, samples, flops: FlopCounter | None = None, out=None, non_blocking: bool = False):
     """Coefficients S with sum_p S_p e^{2 pi i p t_q} = samples_q (inverse.py:101-120, Fig. 2).
 
-    `out` (extension): optional preallocated torch tensor (device, or pinned host) for the result."""
-    out = _solve("type5", plan, samples, "samples", None, out)
+    `out` (extension): optional preallocated torch tensor (device, or pinned host) for the result.
+    `non_blocking` (extension): with CPU torch operands and a pinned `out`, return once the
+    work is enqueued (torch copy_ semantics: synchronize before reading `out`)."""
+    out = _solve("type5", plan, samples, "samples", None, out, non_blocking)
     _charge_type5(flops, plan.size, plan.kernel_base.taps)
     return out
 
 
-def type4(plan: InversePlan, spectrum, flops: FlopCounter | None = None, out=None):
+def type4(plan: InversePlan, spectrum, flops: FlopCounter | None = None, out=None, non_blocking: bool = False):
     """Amplitudes a with sum_q a_q e^{-2 pi i p t_q} = spectrum_p (inverse.py:123-143, Fig. 3)."""
-    out = _solve("type4", plan, spectrum, "spectrum", None, out)
+    out = _solve("type4", plan, spectrum, "spectrum", None, out, non_blocking)
     _charge_type4(flops, plan.size, plan.kernel_base.taps)
     return out
 
 
 def refine_type4(plan: InversePlan, spectrum, passes: int | None = None, flops: FlopCounter | None = None,
-                 out=None):
+                 out=None, non_blocking: bool = False):
     """type4 plus residual-correction passes (inverse.py:165-185, Section V)."""
     if passes is None:
         passes = plan.params.refine_passes
-    out = _solve("type4", plan, spectrum, "spectrum", passes, out)
+    out = _solve("type4", plan, spectrum, "spectrum", passes, out, non_blocking)
     P, taps = plan.size, plan.kernel_base.taps
     _charge_type4(flops, P, taps)
     for _ in range(passes):
@@ -278,11 +294,11 @@ def refine_type4(plan: InversePlan, spectrum, passes: int | None = None, flops: 
 
 
 def refine_type5(plan: InversePlan, samples, passes: int | None = None, flops: FlopCounter | None = None,
-                 out=None):
+                 out=None, non_blocking: bool = False):
     """type5 plus residual-correction passes in the sample domain (inverse.py:188-202)."""
     if passes is None:
         passes = plan.params.refine_passes
-    out = _solve("type5", plan, samples, "samples", passes, out)
+    out = _solve("type5", plan, samples, "samples", passes, out, non_blocking)
     P, taps = plan.size, plan.kernel_base.taps
     _charge_type5(flops, P, taps)
     for _ in range(passes):

@@ -287,6 +287,28 @@ def test_streamed_host_batches_match_device_path():
     assert rel(want5.numpy(), got5.numpy()) < 1e-15 and rel(want4.numpy(), got4.numpy()) < 1e-15
 
 
+def test_non_blocking_streamed_solves_complete_after_synchronize():
+    """non_blocking=True (torch copy_ semantics): back-to-back streamed type-5 and
+    type-4 calls into pinned outputs, one device synchronize, results equal the
+    blocking path bitwise; the staging buffers are not recycled under the copies."""
+    from paper_1604_06236_b200 import inverse as inv
+
+    P, B = 4096, inv.STREAM_CHUNK * 3 + 5
+    t, data = O.make_inputs(P, 0.3, B, 12)
+    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-15, P, 2))
+    host = torch.from_numpy(data).pin_memory()
+    want5 = nf.refine_type5(plan, host, passes=1)
+    want4 = nf.refine_type4(plan, host, passes=1)
+    o5, o4 = torch.empty_like(host).pin_memory(), torch.empty_like(host).pin_memory()
+    for _ in range(2):
+        o5.zero_()
+        o4.zero_()
+        nf.refine_type5(plan, host, passes=1, out=o5, non_blocking=True)
+        nf.refine_type4(plan, host, passes=1, out=o4, non_blocking=True)
+        torch.cuda.synchronize()
+        assert torch.equal(o5, want5) and torch.equal(o4, want4)
+
+
 _GAP_SCRIPT = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[2])
