@@ -834,6 +834,17 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
     double2 acc[NPL];
 #pragma unroll
     for (int i = 0; i < NPL; i++) acc[i] = make_double2(0.0, 0.0);
+    // batch-minor subtrahend: requested before the window sums so its latency
+    // hides under them (it is only consumed by the epilogue)
+    double2 sb_in[NPL];
+    if (SUBM == 1 && mode != 0) {
+#pragma unroll
+      for (int i = 0; i < NPL; i++) {
+        const int e = e0 + i;
+        const bool ok = e < nq && b0 + sl < batch;
+        sb_in[i] = ok ? sub[(int64_t)s_pq[e] * sub_ld + b0 + sl] : make_double2(0.0, 0.0);
+      }
+    }
 #pragma unroll 4
     for (int i = 0; i < wl; i++) {
       const double2 y = yw[i * SIG];
@@ -845,7 +856,6 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
         caxpy(acc[2 * i2 + 1], w.y, y);
       }
     }
-    double2 sb_in[NPL];
     if (SUBM == 2 && mode != 0) {
 #pragma unroll
       for (int i = 0; i < NPL; i++) {
@@ -864,7 +874,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
         double2 v = cmul(acc[i], s_fac[e]);
         const int64_t pq = s_pq[e];
         if (b < batch && mode != 0) {
-          const double2 sv = SUBM == 1 ? sub[pq * sub_ld + b] : sb_in[i];
+          const double2 sv = sb_in[i];
           v = mode == 1 ? csub(v, sv) : csub(sv, v);
         }
         out[pq * out_ld + b] = b < batch ? v : make_double2(0.0, 0.0);
@@ -875,7 +885,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
         const int e = e0 + i;
         double2 v = cmul(acc[i], e < nq ? s_fac[e] : make_double2(0.0, 0.0));
         if (mode != 0 && e < nq && b0 + sl < batch) {
-          const double2 sv = SUBM == 1 ? sub[(int64_t)s_pq[e] * sub_ld + b0 + sl] : sb_in[i];
+          const double2 sv = sb_in[i];
           v = mode == 1 ? csub(v, sv) : csub(sv, v);
         }
         O[e * SIG + swz(sl, e)] = v;
