@@ -306,6 +306,12 @@ def main():
     plan = nf.build_plan(grid, params, device=dev)
     torch.cuda.synchronize()
     plan_ms = 1e3 * (time.perf_counter() - t0)
+    # warm rebuild of the same node set (the first build also pays the
+    # library's one-time costs: lazy module loading, FFT twiddle tables)
+    t0 = time.perf_counter()
+    nf.build_plan(nf.validate_grid(t), params, device=dev)
+    torch.cuda.synchronize()
+    plan_warm_ms = 1e3 * (time.perf_counter() - t0)
 
     # ---- device-resident inputs (this rank's shard of signals), seeded
     gen = torch.Generator(device=f"cuda:{dev}")
@@ -435,6 +441,11 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "plan_ms": plan_ms,
+        "plan_warm_ms": plan_warm_ms,
+        # single transforms (the plan is not amortised for C1, C3, C5):
+        # the same metric with one warm plan build charged to every step
+        "with_plan": ({"value": pts_per_step / ((ms / args.steps + plan_warm_ms) / 1e3), "unit": "points/s",
+                       "ms_per_step": ms / args.steps + plan_warm_ms} if B == 1 else None),
         "parity": {"forward_residual_type5": resid5, "forward_residual_type4": resid4},
         "kernels_ms_per_step": {k: v[1] / args.steps for k, v in sorted(kernels_raw.items(), key=lambda kv: -kv[1][1])},
         "kernel_roofline": per_kernel_roofline,
