@@ -424,11 +424,21 @@ def main():
                 "avg_launch_ms": avg_ms, "launches": tcount, "share_of_kernel_time": tms / step_kernel_ms,
                 "peak_source": peak_src}
 
+    # per kernel family: algorithmic bytes / live time, and, where the
+    # committed ncu capture of this config has it, the kernel's MEASURED DRAM bytes
+    # per launch / live launch time (how close each kernel runs to the HBM peak on
+    # the traffic it actually moves)
+    tfile = os.path.join(REPO, "profiles", f"traffic_{args.config}.json")
+    tj = json.load(open(tfile)) if os.path.exists(tfile) else {}
     per_kernel_roofline = {}
     for name, (cnt, kms) in kprof.items():
         if name in ALGO_BYTES_PER_POINT_STEP and kms > 0:
             gbs = ALGO_BYTES_PER_POINT_STEP[name] * B * P * args.steps / (kms / 1e3) / 1e9
             per_kernel_roofline[name] = {"achieved_GBps": gbs, "frac": gbs / peak}
+            tb = tj.get(name, next((v for k, v in tj.items() if k.startswith(name + "_")), None))
+            if tb and cnt:
+                dram = tb / (kms / cnt / 1e3) / 1e9
+                per_kernel_roofline[name].update({"dram_GBps": dram, "dram_frac": dram / peak})
     total_algo = sum(ALGO_BYTES_PER_POINT_STEP[k] for k in kprof if k in ALGO_BYTES_PER_POINT_STEP) * B * P
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
