@@ -242,6 +242,25 @@ def test_batched_equals_per_signal_and_is_bitwise_reproducible():
     assert np.array_equal(full4[5], nf.refine_type4(plan, data[5], passes=1))
 
 
+@pytest.mark.parametrize("B", [3, 5, 15, 16, 17, 33])
+def test_batch_sizes_across_kernel_switches(B):
+    """Batch sizes on both sides of every kernel switch (small-batch gridding
+    with 1- and 4-signal tiles, signal-major vs batch-minor chains at 16, padded
+    batch-minor rows): every row matches its single-signal solve — type 5
+    bitwise, type 4 to rounding — and the oracle."""
+    P = 4096
+    t, data = O.make_inputs(P, 0.3, B, 100 + B)
+    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-15, P, 2))
+    oplan = O.Plan.build(t, plan.params.damping_a, 2)
+    full5 = nf.refine_type5(plan, data, passes=1)
+    full4 = nf.refine_type4(plan, data, passes=1)
+    for r in sorted({0, B // 2, B - 1}):
+        assert np.array_equal(full5[r], nf.refine_type5(plan, data[r], passes=1))
+        assert rel(nf.refine_type4(plan, data[r], passes=1), full4[r]) < 1e-13
+        assert rel(O.refine5(oplan, data[r], 1), full5[r]) <= G1
+        assert rel(O.refine4(oplan, data[r], 1), full4[r]) <= G1
+
+
 def test_torch_device_and_pinned_host_operands():
     P, B = 1 << 16, 4
     t, data = O.make_inputs(P, 0.3, B, 9)
