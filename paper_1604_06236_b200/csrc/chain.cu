@@ -391,10 +391,19 @@ bool chain_supported(int64_t P, int m) {
   return false;
 }
 
+static bool batch_minor(int64_t batch) {
+  static const bool no_bm = getenv("NFFT45_NO_BATCH_MINOR") != nullptr;  // A/B switch
+  return batch >= 16 && !no_bm;
+}
+
+bool chain_usable(int64_t P, int m, int64_t batch) {
+  if (m != kFastM) return false;
+  return chain_supported(P, m) || (batch_minor(batch) && chain_bm_supported(P));
+}
+
 int chain_run(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes, double2* out,
               double* norms, cudaStream_t st) {
-  static const bool no_bm = getenv("NFFT45_NO_BATCH_MINOR") != nullptr;  // A/B switch
-  if (batch >= 16 && !no_bm) return chain_run_bm(pv, kind, data, batch, passes, out, norms, st);
+  if (batch_minor(batch) && chain_bm_supported(pv.P)) return chain_run_bm(pv, kind, data, batch, passes, out, norms, st);
   switch (pv.P) {
     case 1024: return chain_solve<32>(pv, kind, data, batch, passes, out, norms, st);
     case 4096: return chain_solve<64>(pv, kind, data, batch, passes, out, norms, st);

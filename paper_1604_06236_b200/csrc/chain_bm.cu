@@ -2,6 +2,14 @@
 // batch-minor internal layout X[index][signal] (signal stride 1, padded
 // batch Bp = multiple of 8).
 //
+// P = R * C (R = C = M for even powers of two, R = 2C for odd ones).  The
+// P-point vectors use the layout p = k + R m (k < R, m < C); the fine grid
+// n = 2P is split R x 2C for the FFT_2P / IFFT_2P four-steps, so with
+// K = P/2 = R (C/2) the band (p - K) mod n of FFT_2P row k is exactly column
+// k of the P layout (and, in the other direction, the zero-padded IFFT_2P
+// column of P-layout row k).  Kernel tile lengths: col R, band 2C + C, mid
+// R + R, pad C + 2C, row R, colin / rowout C.
+//
 // Every tile is one row (or column) of the four-step layout for 8 signals,
 // so (i) global loads/stores are contiguous 128-byte runs over signals,
 // (ii) the per-index tables (ks, deconv*decay, coef*deconv) and the
@@ -28,63 +36,24 @@ constexpr int kSig = 8;  // signals per tile (batch-minor kernels)
 // CTAs per SM to request for a T-thread tile kernel: enough that every thread
 // keeps ~128 registers (a 16-element tile FFT spills below that).
 __host__ __device__ constexpr int bm_minb(int T) { return T >= 512 ? 1 : (T >= 256 ? 2 : 4); }
-// signals per tile of the two-FFT kernels: 8, or 4 when 8 would need a
-// CTA above 512 threads (M = 1024)
-template <int M>
-__host__ __device__ constexpr int bm_sg() { return fast_threads<2 * M, kSig>() > 512 ? kSig / 2 : kSig; }
-// rows per tile of the boundary kernels (4 signals each): 4, or 2 for M = 1024
-template <int M>
-__host__ __device__ constexpr int bm_rw() { return fast_threads<M, 16>() > 512 ? 2 : 4; }
-
+// signals per tile of the two-FFT kernels (tile lengths 2C and C): 8, or 4
+// when 8 would need a CTA above 512 threads (C = 1024)
+template <int C>
+__host__ __device__ constexpr int bm_sg() { return fast_threads<2 * C, kSig>() > 512 ? kSig / 2 : kSig; }
+// rows per tile of the boundary kernels (length C, 4 signals each): 4, or 2 for C = 1024
+template <int C>
+__host__ __device__ constexpr int bm_rw() { return fast_threads<C, 16>() > 512 ? 2 : 4; }
 
 __device__ __forceinline__ double2 rsc(double2 v, double s) { return make_double2(v.x * s, v.y * s); }
-// 0 that the compiler cannot prove constant: offsetting the tables by it inside
-// a persistent tile loop keeps loop-invariant twiddles from being hoisted into
-// (and spilled from) registers across tiles.
-__device__ __forceinline__ int opaque0() {
-  int z;
-  asm volatile("mov.u32 %0, 0;" : "=r"(z));
-  return z;
-}
 
 __device__ __forceinline__ void cpa16(void* sdst, const void* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 __device__ __forceinline__ void cpa8(void* sdst, const void* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
-}
-
-// Persistent tile loop with a double-buffered cp.async prefetch of each
-// tile's input (L rows x 8 signals, row-contiguous in the batch-minor
-// layout): while tile t computes, tile t + gridDim.x is already in flight.
-template <int L, class Src, class Body>
-__device__ __forceinline__ void persistent_tiles(int ntiles, double2* buf0, double2* buf1, const Src& src,
-                                                 const Body& body) {
-  auto prefetch = [&](int t, double2* buf) {
-    for (int e = threadIdx.x; e < L * kSig; e += blockDim.x) cpa16(&buf[e], src(t, e >> 3, e & 7));
-    cpa_commit();
-  };
-  int t = blockIdx.x;
-  if (t < ntiles) prefetch(t, buf0);
-#pragma unroll 1
-  for (int it = 0; t < ntiles; t += gridDim.x, it++) {
-    double2* cur = (it & 1) ? buf1 : buf0;
-    double2* nxt = (it & 1) ? buf0 : buf1;
-    if (t + (int)gridDim.x < ntiles) {
-      prefetch(t + gridDim.x, nxt);
-      cpa_wait<1>();
-    } else {
-      cpa_wait<0>();
-    }
-    __syncthreads();
-    body(t, cur);
-    __syncthreads();
-  }
 }
 }  // namespace
 
@@ -109,28 +78,28 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<
   fast_tile_fft<L, kSig, S, true>(sm, ld, st, tw, pt);
 }
 
-// row FFT_2P (row k1 = blockIdx.x, length 2M) -> band p = k1 + M m1 with
-// deconv*decay (or (X deconv - sub) decay) -> column IFFT_P (length M) ->
-// W_P^{+k1 k1'} -> U[(k1' M + k1)][b].
+// row FFT_2P (row k1 < R, length 2C) -> band p = k1 + R m1 (m1 < C) with
+// deconv*decay (or (X deconv - sub) decay) -> column IFFT_P (length C) ->
+// W_P^{+k1 k1'} -> U[(k1' R + k1)][b].
 // Per-tile tables (deconv*decay, or deconv and decay plus the subtrahend
 // tile) are staged into shared memory with cp.async at entry; the copies fly
 // during the first FFT pass (CpAsyncWaitHook) instead of stalling the band
 // epilogue on L2 latency.
-template <int M, int SG, class Tr1 = FastTraits<2 * M>>
-__global__ void __launch_bounds__(2 * M * SG / Tr1::E, Tr1::E == 8 ? 2 : bm_minb(2 * M * SG / Tr1::E)) kbm_band(
+template <int R, int C, int SG>
+__global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_threads<2 * C, SG>())) kbm_band(
     const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
     const double* __restrict__ dd, const double2* __restrict__ sub, int sw) {
-  constexpr int NR = 2 * M;
+  constexpr int NR = 2 * C;
   extern __shared__ double2 sm[];
   double* s_t0 = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + fast_smem<NR, SG>());
-  double* s_t1 = s_t0 + M;
-  double2* s_sb = reinterpret_cast<double2*>(s_t1 + M);
+  double* s_t1 = s_t0 + C;
+  double2* s_sb = reinterpret_cast<double2*>(s_t1 + C);
   const int k1 = sw ? blockIdx.y : blockIdx.x;
   const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * SG;
-  for (int m1 = threadIdx.x; m1 < M; m1 += blockDim.x) {
-    const int64_t p = (int64_t)k1 + (int64_t)M * m1;
+  for (int m1 = threadIdx.x; m1 < C; m1 += blockDim.x) {
+    const int64_t p = (int64_t)k1 + (int64_t)R * m1;
     if (sub) {
       cpa8(&s_t0[m1], &deconv[p]);
       cpa8(&s_t1[m1], &decay[p]);
@@ -139,13 +108,13 @@ __global__ void __launch_bounds__(2 * M * SG / Tr1::E, Tr1::E == 8 ? 2 : bm_minb
     }
   }
   if (sub)
-    for (int e = threadIdx.x; e < M * SG; e += blockDim.x)
-      cpa16(&s_sb[e], &sub[((int64_t)k1 + (int64_t)M * (e / SG)) * Bp + b0 + e % SG]);
+    for (int e = threadIdx.x; e < C * SG; e += blockDim.x)
+      cpa16(&s_sb[e], &sub[((int64_t)k1 + (int64_t)R * (e / SG)) * Bp + b0 + e % SG]);
   cpa_commit();
   auto ld1 = [&](int i, int c) -> double2 { return T[((int64_t)k1 * NR + i) * Bp + b0 + c]; };
   auto st1 = [&](int k2, int c, double2 v) {
-    const int m1 = (k2 + M / 2) & (NR - 1);
-    if (m1 < M) {
+    const int m1 = (k2 + C / 2) & (NR - 1);  // (k2 + K/R) mod 2C, K/R = C/2
+    if (m1 < C) {
       if (sub) {
         v = rsc(v, s_t0[m1]);
         v = csub(v, s_sb[m1 * SG + c]);
@@ -153,59 +122,61 @@ __global__ void __launch_bounds__(2 * M * SG / Tr1::E, Tr1::E == 8 ? 2 : bm_minb
       } else {
         v = rsc(v, s_t0[m1]);
       }
-      sm[sidx<M, SG, true>(m1, c)] = v;
+      sm[sidx<C, SG, true>(m1, c)] = v;
     }
   };
-  fast_tile_fft<NR, SG, -1, true, Tr1>(sm, ld1, st1, twR, NoPostTw(), CpAsyncWaitHook());
+  fast_tile_fft<NR, SG, -1, true>(sm, ld1, st1, twR, NoPostTw(), CpAsyncWaitHook());
   __syncthreads();
-  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, SG, true>(i, c)]; };
-  auto st2 = [&](int k1p, int c, double2 v) { U[((int64_t)k1p * M + k1) * Bp + b0 + c] = v; };
+  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<C, SG, true>(i, c)]; };
+  auto st2 = [&](int k1p, int c, double2 v) { U[((int64_t)k1p * R + k1) * Bp + b0 + c] = v; };
   const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, k1, 0};
-  fast_tile_fft_smem<M, SG, +1, true, HalfTr<M>>(sm, ld2, st2, twC, pt);
+  fast_tile_fft_smem<C, SG, +1, true, HalfTr<C>>(sm, ld2, st2, twC, pt);
 }
 
-// row IFFT_P (row r) -> * ks -> column FFT_P (column r) -> W_P^{-r k} -> Z.
-template <int M>
-__global__ void __launch_bounds__(fast_threads<M, kSig>(), bm_minb(fast_threads<M, kSig>())) kbm_mid(
+// row IFFT_P (row r < C of U, length R) -> * ks[r + C k2] -> column FFT_P
+// (length R, column r of the layout q = r + C k2) -> W_P^{-r k} -> Z[(k C + r)].
+template <int R, int C>
+__global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<R, kSig>())) kbm_mid(
     const double2* __restrict__ U, double2* __restrict__ Z, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
     const double2* __restrict__ ks, int sw) {
   extern __shared__ double2 sm[];
-  double2* s_ks = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + fast_smem<M, kSig>());
+  double2* s_ks = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + fast_smem<R, kSig>());
   const int r = sw ? blockIdx.y : blockIdx.x;
   const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * kSig;
-  for (int k2 = threadIdx.x; k2 < M; k2 += blockDim.x) cpa16(&s_ks[k2], &ks[(int64_t)r + (int64_t)M * k2]);
+  for (int k2 = threadIdx.x; k2 < R; k2 += blockDim.x) cpa16(&s_ks[k2], &ks[(int64_t)r + (int64_t)C * k2]);
   cpa_commit();
-  auto ld1 = [&](int i, int c) -> double2 { return U[((int64_t)r * M + i) * Bp + b0 + c]; };
-  auto st1 = [&](int k2, int c, double2 v) { sm[sidx<M, kSig, true>(k2, c)] = cmul(v, s_ks[k2]); };
-  fast_tile_fft<M, kSig, +1, true>(sm, ld1, st1, tw, NoPostTw(), CpAsyncWaitHook());
+  auto ld1 = [&](int i, int c) -> double2 { return U[((int64_t)r * R + i) * Bp + b0 + c]; };
+  auto st1 = [&](int k2, int c, double2 v) { sm[sidx<R, kSig, true>(k2, c)] = cmul(v, s_ks[k2]); };
+  fast_tile_fft<R, kSig, +1, true>(sm, ld1, st1, tw, NoPostTw(), CpAsyncWaitHook());
   __syncthreads();
-  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, kSig, true>(i, c)]; };
-  auto st2 = [&](int k, int c, double2 v) { Z[((int64_t)k * M + r) * Bp + b0 + c] = v; };
+  auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<R, kSig, true>(i, c)]; };
+  auto st2 = [&](int k, int c, double2 v) { Z[((int64_t)k * C + r) * Bp + b0 + c] = v; };
   const FourStepTw<-1> pt{loP, hiP, sP, twQ, Q, r, 0};
-  fast_tile_fft_smem<M, kSig, -1, true>(sm, ld2, st2, tw, pt);
+  fast_tile_fft_smem<R, kSig, -1, true>(sm, ld2, st2, tw, pt);
 }
 
-// row FFT_P (row r) -> * coef (x = [xsub -] S coef stored when xout) *
-// deconv -> zero-padded column IFFT_2P (length 2M, column r) -> W_n^{+r k} -> Y.
-template <int M, int SG>
-__global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_threads<2 * M, SG>())) kbm_pad(
+// row FFT_P (row r < R of Z, length C) -> * coef (x = [xsub -] S coef stored
+// when xout) * deconv -> zero-padded column IFFT_2P (length 2C, column r of
+// the n = R x 2C layout) -> W_n^{+r k} -> Y[(k R + r)].
+template <int R, int C, int SG>
+__global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_threads<2 * C, SG>())) kbm_pad(
     const double2* __restrict__ Z, double2* __restrict__ Y, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
     const double* __restrict__ cd, const double2* __restrict__ xsub, double2* __restrict__ xout, int sw) {
-  constexpr int NC = 2 * M;
+  constexpr int NC = 2 * C;
   constexpr bool kLead2 = FastTraits<NC>::radix(0) == 2;
   extern __shared__ double2 sm[];
   double* s_t0 = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + fast_smem<NC, SG>());
-  double* s_t1 = s_t0 + M;
-  double2* s_xs = reinterpret_cast<double2*>(s_t1 + M);
+  double* s_t1 = s_t0 + C;
+  double2* s_xs = reinterpret_cast<double2*>(s_t1 + C);
   const int r = sw ? blockIdx.y : blockIdx.x;
   const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * SG;
   // per-tile tables (and the xsub tile) staged with cp.async, waited for at
   // the end of the first FFT pass
-  for (int k2 = threadIdx.x; k2 < M; k2 += blockDim.x) {
-    const int64_t p = (int64_t)r + (int64_t)M * k2;
+  for (int k2 = threadIdx.x; k2 < C; k2 += blockDim.x) {
+    const int64_t p = (int64_t)r + (int64_t)R * k2;
     if (xout) {
       cpa8(&s_t0[k2], &coef[p]);
       cpa8(&s_t1[k2], &deconv[p]);
@@ -214,12 +185,12 @@ __global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_thread
     }
   }
   if (xout && xsub)
-    for (int e = threadIdx.x; e < M * SG; e += blockDim.x)
-      cpa16(&s_xs[e], &xsub[((int64_t)r + (int64_t)M * (e / SG)) * Bp + b0 + e % SG]);
+    for (int e = threadIdx.x; e < C * SG; e += blockDim.x)
+      cpa16(&s_xs[e], &xsub[((int64_t)r + (int64_t)R * (e / SG)) * Bp + b0 + e % SG]);
   cpa_commit();
-  auto ld1 = [&](int i, int c) -> double2 { return Z[((int64_t)r * M + i) * Bp + b0 + c]; };
+  auto ld1 = [&](int i, int c) -> double2 { return Z[((int64_t)r * C + i) * Bp + b0 + c]; };
   auto st1 = [&](int k2, int c, double2 v) {
-    const int64_t p = (int64_t)r + (int64_t)M * k2;
+    const int64_t p = (int64_t)r + (int64_t)R * k2;
     if (xout) {
       v = rsc(v, s_t0[k2]);
       if (xsub) v = csub(s_xs[k2 * SG + c], v);
@@ -228,28 +199,28 @@ __global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_thread
     } else {
       v = rsc(v, s_t0[k2]);
     }
-    const int n1 = (k2 - M / 2) & (NC - 1);
+    const int n1 = (k2 - C / 2) & (NC - 1);
     if constexpr (kLead2) {
       // The IFFT_2P column is zero outside the band, so its first Stockham
-      // pass (radix 2, pairs n1 and n1 + M) is a copy: write its outputs
-      // directly.  n1 in [0, M/2): partner zero -> (v, v); n1 in
-      // [3M/2, 2M): partner zero on the other side -> (v, -v).
-      if (n1 < M) {
+      // pass (radix 2, pairs n1 and n1 + C) is a copy: write its outputs
+      // directly.  n1 in [0, C/2): partner zero -> (v, v); n1 in
+      // [3C/2, 2C): partner zero on the other side -> (v, -v).
+      if (n1 < C) {
         sm[sidx<NC, SG, true>(2 * n1, c)] = v;
         sm[sidx<NC, SG, true>(2 * n1 + 1, c)] = v;
       } else {
-        const int j = n1 - M;
+        const int j = n1 - C;
         sm[sidx<NC, SG, true>(2 * j, c)] = v;
         sm[sidx<NC, SG, true>(2 * j + 1, c)] = make_double2(-v.x, -v.y);
       }
     } else {
       sm[sidx<NC, SG, true>(n1, c)] = v;
-      sm[sidx<NC, SG, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
+      sm[sidx<NC, SG, true>((n1 + C) & (NC - 1), c)] = make_double2(0.0, 0.0);
     }
   };
-  fast_tile_fft<M, SG, -1, true, HalfTr<M>>(sm, ld1, st1, twR, NoPostTw(), CpAsyncWaitHook());
+  fast_tile_fft<C, SG, -1, true, HalfTr<C>>(sm, ld1, st1, twR, NoPostTw(), CpAsyncWaitHook());
   __syncthreads();
-  auto st2 = [&](int k, int c, double2 v) { Y[((int64_t)k * M + r) * Bp + b0 + c] = v; };
+  auto st2 = [&](int k, int c, double2 v) { Y[((int64_t)k * R + r) * Bp + b0 + c] = v; };
   const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r, 0};
   if constexpr (kLead2) {
     fast_tile_fft_from<NC, SG, +1, true, 1, 2>(sm, st2, twC, pt);
@@ -257,112 +228,6 @@ __global__ void __launch_bounds__(fast_threads<2 * M, SG>(), bm_minb(fast_thread
     auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, SG, true>(i, c)]; };
     fast_tile_fft_smem<NC, SG, +1, true>(sm, ld2, st2, twC, pt);
   }
-}
-
-// Persistent variant of kbm_pad (one CTA per SM walks all (row, group)
-// tiles; the next tile's Z row block is prefetched during compute).
-template <int M>
-__global__ void __launch_bounds__(fast_threads<2 * M, kSig>(), 1) kbm_pad_p(
-    const double2* __restrict__ Z, double2* __restrict__ Y, int64_t Bp, int groups, const double2* __restrict__ twR,
-    const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
-    const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
-    const double* __restrict__ cd, const double2* __restrict__ xsub, double2* __restrict__ xout) {
-  constexpr int NC = 2 * M;
-  constexpr bool kLead2 = FastTraits<NC>::radix(0) == 2;
-  extern __shared__ double2 sm[];
-  double2* buf0 = sm + (fast_smem<NC, kSig>() / sizeof(double2) + 1);
-  double2* buf1 = buf0 + M * kSig;
-  auto src = [&](int t, int i, int c) -> const double2* {
-    const int r = t % M;
-    const int64_t b0 = (int64_t)(t / M) * kSig;
-    return Z + ((int64_t)r * M + i) * Bp + b0 + c;
-  };
-  auto body = [&](int t, const double2* in) {
-    const int r = t % M;
-    const int64_t b0 = (int64_t)(t / M) * kSig;
-    auto ld1 = [&](int i, int c) -> double2 { return in[i * kSig + c]; };
-    auto st1 = [&](int k2, int c, double2 v) {
-      const int64_t p = (int64_t)r + (int64_t)M * k2;
-      if (xout) {
-        v = rsc(v, __ldg(&coef[p]));
-        if (xsub) v = csub(xsub[p * Bp + b0 + c], v);
-        xout[p * Bp + b0 + c] = v;
-        v = rsc(v, __ldg(&deconv[p]));
-      } else {
-        v = rsc(v, __ldg(&cd[p]));
-      }
-      const int n1 = (k2 - M / 2) & (NC - 1);
-      if constexpr (kLead2) {
-        if (n1 < M) {
-          sm[sidx<NC, kSig, true>(2 * n1, c)] = v;
-          sm[sidx<NC, kSig, true>(2 * n1 + 1, c)] = v;
-        } else {
-          const int j = n1 - M;
-          sm[sidx<NC, kSig, true>(2 * j, c)] = v;
-          sm[sidx<NC, kSig, true>(2 * j + 1, c)] = make_double2(-v.x, -v.y);
-        }
-      } else {
-        sm[sidx<NC, kSig, true>(n1, c)] = v;
-        sm[sidx<NC, kSig, true>((n1 + M) & (NC - 1), c)] = make_double2(0.0, 0.0);
-      }
-    };
-    fast_tile_fft<M, kSig, -1, true, HalfTr<M>>(sm, ld1, st1, twR);
-    __syncthreads();
-    auto st2 = [&](int k, int c, double2 v) { Y[((int64_t)k * M + r) * Bp + b0 + c] = v; };
-    const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r, 0};
-    if constexpr (kLead2) {
-      fast_tile_fft_from<NC, kSig, +1, true, 1, 2>(sm, st2, twC, pt);
-    } else {
-      auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, kSig, true>(i, c)]; };
-      fast_tile_fft_smem<NC, kSig, +1, true>(sm, ld2, st2, twC, pt);
-    }
-  };
-  persistent_tiles<M>(M * groups, buf0, buf1, src, body);
-}
-
-// Persistent variant of kbm_band.
-template <int M, class Tr1 = FastTraits<2 * M>>
-__global__ void __launch_bounds__(2 * M * kSig / Tr1::E, 1) kbm_band_p(
-    const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, int groups, const double2* __restrict__ twR,
-    const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
-    const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
-    const double* __restrict__ dd, const double2* __restrict__ sub) {
-  constexpr int NR = 2 * M;
-  extern __shared__ double2 sm[];
-  double2* buf0 = sm + (fast_smem<NR, kSig>() / sizeof(double2) + 1);
-  double2* buf1 = buf0 + NR * kSig;
-  auto src = [&](int t, int i, int c) -> const double2* {
-    const int k1 = t % M;
-    const int64_t b0 = (int64_t)(t / M) * kSig;
-    return T + ((int64_t)k1 * NR + i) * Bp + b0 + c;
-  };
-  auto body = [&](int t, const double2* in) {
-    const int k1 = t % M;
-    const int64_t b0 = (int64_t)(t / M) * kSig;
-    auto ld1 = [&](int i, int c) -> double2 { return in[i * kSig + c]; };
-    auto st1 = [&](int k2, int c, double2 v) {
-      const int m1 = (k2 + M / 2) & (NR - 1);
-      if (m1 < M) {
-        const int64_t p = (int64_t)k1 + (int64_t)M * m1;
-        if (sub) {
-          v = rsc(v, __ldg(&deconv[p]));
-          v = csub(v, sub[p * Bp + b0 + c]);
-          v = rsc(v, __ldg(&decay[p]));
-        } else {
-          v = rsc(v, __ldg(&dd[p]));
-        }
-        sm[sidx<M, kSig, true>(m1, c)] = v;
-      }
-    };
-    const int z = opaque0();
-    fast_tile_fft<NR, kSig, -1, true, Tr1>(sm, ld1, st1, twR + z);
-    __syncthreads();
-    auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<M, kSig, true>(i, c)]; };
-    auto st2 = [&](int k1p, int c, double2 v) { U[((int64_t)k1p * M + k1) * Bp + b0 + c] = v; };
-    const FourStepTw<+1> pt{loP + z, hiP + z, sP, twQ + z, Q, k1, 0};
-    fast_tile_fft_smem<M, kSig, +1, true, HalfTr<M>>(sm, ld2, st2, twC + z, pt);
-  };
-  persistent_tiles<NR>(M * groups, buf0, buf1, src, body);
 }
 
 // row pass: row r = blockIdx.x (length L), output index r + R1 k.
@@ -378,53 +243,55 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<
   fast_tile_fft<L, kSig, S, true>(sm, ld, st, tw);
 }
 
-// Boundary, type-4 input: signal-major A[b][P] -> column IFFT_P * decay
-// (columns m2 = 4 blockIdx.x + (c & 3), signals b = 4 blockIdx.y + (c >> 2))
-// -> batch-minor U; optionally also a batch-minor copy AT of A.
-template <int M, int RW>
-__global__ void __launch_bounds__(fast_threads<M, 4 * RW>(), bm_minb(fast_threads<M, 4 * RW>())) kbm_colin(
+// Boundary, type-4 input: signal-major A[b][P] -> column IFFT_P (length C,
+// columns k = RW blockIdx.x + (c % RW) of the p = k + R m layout, signals
+// b = 4 blockIdx.y + c / RW) * decay -> batch-minor U; optionally also a
+// batch-minor copy AT of A.
+template <int R, int C, int RW>
+__global__ void __launch_bounds__(fast_threads<C, 4 * RW>(), bm_minb(fast_threads<C, 4 * RW>())) kbm_colin(
     const double2* __restrict__ A, int64_t batch, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
     const double* __restrict__ decay, double2* __restrict__ AT, int sw) {
-  constexpr int64_t P = (int64_t)M * M;
+  constexpr int64_t P = (int64_t)R * C;
   extern __shared__ double2 sm[];
   const int m20 = (sw ? blockIdx.y : blockIdx.x) * RW;
   const int64_t bb = (int64_t)(sw ? blockIdx.x : blockIdx.y) * 4;
   auto ld = [&](int i, int c) -> double2 {
-    const int64_t idx = (int64_t)i * M + m20 + (c % RW);
+    const int64_t idx = (int64_t)i * R + m20 + (c % RW);
     const int64_t b = bb + c / RW;
     double2 v = b < batch ? A[b * P + idx] : make_double2(0.0, 0.0);
     if (AT) AT[idx * Bp + b] = v;
     return rsc(v, __ldg(&decay[idx]));
   };
   auto st = [&](int k1, int c, double2 v) {
-    U[((int64_t)k1 * M + m20 + (c % RW)) * Bp + bb + c / RW] = v;
+    U[((int64_t)k1 * R + m20 + (c % RW)) * Bp + bb + c / RW] = v;
   };
   const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, m20, RW - 1};
-  fast_tile_fft<M, 4 * RW, +1, true>(sm, ld, st, tw, pt);
+  fast_tile_fft<C, 4 * RW, +1, true>(sm, ld, st, tw, pt);
 }
 
-// Boundary, type-5 output: batch-minor Z rows r = 4 blockIdx.x + (c & 3) ->
-// row FFT_P * coef [xsub (batch-minor) - .] -> signal-major out[b][P].
-template <int M, int RW>
-__global__ void __launch_bounds__(fast_threads<M, 4 * RW>(), bm_minb(fast_threads<M, 4 * RW>())) kbm_rowout(
+// Boundary, type-5 output: batch-minor Z rows r = RW blockIdx.x + (c % RW)
+// (length C) -> row FFT_P * coef [xsub (batch-minor) - .] -> signal-major
+// out[b][P] at p = r + R k.
+template <int R, int C, int RW>
+__global__ void __launch_bounds__(fast_threads<C, 4 * RW>(), bm_minb(fast_threads<C, 4 * RW>())) kbm_rowout(
     const double2* __restrict__ Z, double2* __restrict__ out, int64_t batch, int64_t Bp,
     const double2* __restrict__ tw, const double* __restrict__ coef, const double2* __restrict__ xsub, int sw) {
-  constexpr int64_t P = (int64_t)M * M;
+  constexpr int64_t P = (int64_t)R * C;
   extern __shared__ double2 sm[];
   const int r0 = (sw ? blockIdx.y : blockIdx.x) * RW;
   const int64_t bb = (int64_t)(sw ? blockIdx.x : blockIdx.y) * 4;
   auto ld = [&](int i, int c) -> double2 {
-    return Z[((int64_t)(r0 + (c % RW)) * M + i) * Bp + bb + c / RW];
+    return Z[((int64_t)(r0 + (c % RW)) * C + i) * Bp + bb + c / RW];
   };
   auto st = [&](int k, int c, double2 v) {
-    const int64_t p = (int64_t)(r0 + (c % RW)) + (int64_t)M * k;
+    const int64_t p = (int64_t)(r0 + (c % RW)) + (int64_t)R * k;
     const int64_t b = bb + c / RW;
     v = rsc(v, __ldg(&coef[p]));
     if (xsub) v = csub(xsub[p * Bp + b], v);
     if (b < batch) out[b * P + p] = v;
   };
-  fast_tile_fft<M, 4 * RW, -1, true>(sm, ld, st, tw);
+  fast_tile_fft<C, 4 * RW, -1, true>(sm, ld, st, tw);
 }
 
 // ------------------------------------------------------------ host side
@@ -436,21 +303,19 @@ static int bm_attr(K kernel, size_t bytes) {
 }
 
 struct BmTabs {
-  const double2 *twM, *tw2M;
+  const double2 *twR, *twC, *tw2C;  // tile twiddles for lengths R, C, 2C
   const FftTables *tP, *tN;
 };
 
-template <int M>
+template <int R, int C>
 struct ChainBM {
-  static constexpr int64_t P = (int64_t)M * M, n = 2 * P;
+  static constexpr int64_t P = (int64_t)R * C, n = 2 * P;
+  static constexpr int SG = bm_sg<C>();
   BmTabs t;
   int64_t Bp, batch;
   unsigned groups;  // Bp / 8
   cudaStream_t st;
-  int sms = 148;           // persistent grid size (set from the device)
-  bool persistent = true;
-  bool small_tiles = false;  // 4-signal tiles for the two-FFT kernels
-  bool e8 = false;           // experiment: radix-8 / 8-element schedule for the 2M-point stage
+  bool small_tiles = false;  // 4-signal tiles for the two-FFT kernels (A/B experiment)
   bool sw = false;           // grid order: signal groups fastest (blockIdx.x) instead of tile index
   // grid of (tiles x groups*mult); with sw the signal groups run fastest
   dim3 gdim(int tiles, int mult = 1) const {
@@ -465,151 +330,112 @@ struct ChainBM {
     return NFFT45_OK;
   }
 
-  template <int L, int S>
-  int col(const double2* in, double2* out, int L2, int64_t N, const FftTables* t4, const double2* tw,
-          const double* pre) {
-    auto bm_col = kbm_col<L, S>;
-    constexpr size_t smem = fast_smem<L, kSig>();
+  // FFT_2P column pass: R-point columns over the 2C columns of H
+  int col(const double2* in, double2* out) {
+    auto bm_col = kbm_col<R, -1>;
+    constexpr size_t smem = fast_smem<R, kSig>();
     NFFT_CHECK(bm_attr(bm_col, smem));
-    constexpr int T = fast_threads<L, kSig>();
-    const int64_t Q = N / last_stride<L>();
+    constexpr int T = fast_threads<R, kSig>();
+    const int64_t Q = n / last_stride<R>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    LAUNCH(bm_col, gdim(L2), T, smem, st, in, out, L2, Bp, tw, t4->lo, t4->hi, t4->s, twQ, (int)Q, pre, (int)sw);
+    LAUNCH(bm_col, gdim(2 * C), T, smem, st, in, out, 2 * C, Bp, t.twR, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q,
+           nullptr, (int)sw);
     return NFFT45_OK;
   }
 
-  int band(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub) {
-    constexpr int T = fast_threads<2 * M, kSig>();
-    const int64_t Q = P / last_stride<M, HalfTr<M>>();  // the column IFFT_P runs the HalfTr schedule
+  template <int G>
+  int band_g(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub) {
+    auto bm_band = kbm_band<R, C, G>;
+    const size_t smem = fast_smem<2 * C, G>() + 2 * sizeof(double) * C + (sub ? sizeof(double2) * C * G : 0);
+    NFFT_CHECK(bm_attr(bm_band, smem));
+    constexpr int T = fast_threads<2 * C, G>();
+    const int64_t Q = P / last_stride<C, HalfTr<C>>();  // the column IFFT_P runs the HalfTr schedule
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    constexpr size_t smem_p = fast_smem<2 * M, kSig>() + 16 + 2 * sizeof(double2) * 2 * M * kSig;
-    if (persistent && smem_p <= 227 * 1024) {
-      const int ntiles = M * (int)groups;
-      if (e8) {
-        auto bm_band_p8 = kbm_band_p<M, FastTraitsE8<2 * M>>;
-        NFFT_CHECK(bm_attr(bm_band_p8, smem_p));
-        LAUNCH(bm_band_p8, (unsigned)std::min(ntiles, sms), 2 * M * kSig / 8, smem_p, st, T_, U, Bp, (int)groups,
-               t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
-        return NFFT45_OK;
-      }
-      auto bm_band_p = kbm_band_p<M>;
-      NFFT_CHECK(bm_attr(bm_band_p, smem_p));
-      LAUNCH(bm_band_p, (unsigned)std::min(ntiles, sms), T, smem_p, st, T_, U, Bp, (int)groups, t.tw2M, t.twM,
-             t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub);
-      return NFFT45_OK;
-    }
-    if (small_tiles || bm_sg<M>() < kSig) {  // 4-signal tiles (always for M = 1024)
-      auto bm_band4 = kbm_band<M, 4>;
-      const size_t smem4 = fast_smem<2 * M, 4>() + 2 * sizeof(double) * M + (sub ? sizeof(double2) * M * 4 : 0);
-      NFFT_CHECK(bm_attr(bm_band4, smem4));
-      constexpr int T4 = fast_threads<2 * M, 4>();
-      LAUNCH(bm_band4, gdim(M, 2), T4, smem4, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q,
-             pv.deconv, pv.decay, pv.dd, sub, (int)sw);
-      return NFFT45_OK;
-    }
-    const size_t smem = fast_smem<2 * M, kSig>() + 2 * sizeof(double) * M + (sub ? sizeof(double2) * M * kSig : 0);
-    if (e8) {
-      auto bm_band8 = kbm_band<M, kSig, FastTraitsE8<2 * M>>;
-      NFFT_CHECK(bm_attr(bm_band8, smem));
-      LAUNCH(bm_band8, gdim(M), 2 * M * kSig / 8, smem, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s,
-             twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub, (int)sw);
-      return NFFT45_OK;
-    }
-    auto bm_band = kbm_band<M, kSig>;
-    NFFT_CHECK(bm_attr(bm_band, smem));
-    LAUNCH(bm_band, gdim(M), T, smem, st, T_, U, Bp, t.tw2M, t.twM, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q,
-           pv.deconv, pv.decay, pv.dd, sub, (int)sw);
+    LAUNCH(bm_band, gdim(R, kSig / G), T, smem, st, T_, U, Bp, t.tw2C, t.twC, t.tP->lo, t.tP->hi, t.tP->s, twQ,
+           (int)Q, pv.deconv, pv.decay, pv.dd, sub, (int)sw);
     return NFFT45_OK;
+  }
+  int band(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub) {
+    if (small_tiles || SG < kSig) return band_g<kSig / 2>(T_, U, pv, sub);  // always for C = 1024
+    return band_g<kSig>(T_, U, pv, sub);
   }
 
   int mid(const double2* U, double2* Z, const ChainPlanView& pv) {
-    auto bm_mid = kbm_mid<M>;
-    constexpr size_t smem = fast_smem<M, kSig>() + sizeof(double2) * M;
+    auto bm_mid = kbm_mid<R, C>;
+    constexpr size_t smem = fast_smem<R, kSig>() + sizeof(double2) * R;
     NFFT_CHECK(bm_attr(bm_mid, smem));
-    constexpr int T = fast_threads<M, kSig>();
-    const int64_t Q = P / last_stride<M>();
+    constexpr int T = fast_threads<R, kSig>();
+    const int64_t Q = P / last_stride<R>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    LAUNCH(bm_mid, gdim(M), T, smem, st, U, Z, Bp, t.twM, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.ks, (int)sw);
+    LAUNCH(bm_mid, gdim(C), T, smem, st, U, Z, Bp, t.twR, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.ks, (int)sw);
     return NFFT45_OK;
   }
 
-  int pad(const double2* Z, double2* Y, const ChainPlanView& pv, const double2* xsub, double2* xout) {
-    constexpr int T = fast_threads<2 * M, kSig>();
-    const int64_t Q = n / last_stride<2 * M>();
-    const double2* twQ = nullptr;
-    NFFT_CHECK(qtab(Q, &twQ));
-    constexpr size_t smem_p = fast_smem<2 * M, kSig>() + 16 + 2 * sizeof(double2) * M * kSig;
-    if (persistent && smem_p <= 227 * 1024) {
-      auto bm_pad_p = kbm_pad_p<M>;
-      NFFT_CHECK(bm_attr(bm_pad_p, smem_p));
-      const int ntiles = M * (int)groups;
-      LAUNCH(bm_pad_p, (unsigned)std::min(ntiles, sms), T, smem_p, st, Z, Y, Bp, (int)groups, t.twM, t.tw2M, t.tN->lo,
-             t.tN->hi, t.tN->s, twQ, (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout);
-      return NFFT45_OK;
-    }
-    if (small_tiles || bm_sg<M>() < kSig) {  // 4-signal tiles (always for M = 1024)
-      auto bm_pad4 = kbm_pad<M, 4>;
-      const size_t smem4 = fast_smem<2 * M, 4>() + 2 * sizeof(double) * M + (xout && xsub ? sizeof(double2) * M * 4 : 0);
-      NFFT_CHECK(bm_attr(bm_pad4, smem4));
-      constexpr int T4 = fast_threads<2 * M, 4>();
-      LAUNCH(bm_pad4, gdim(M, 2), T4, smem4, st, Z, Y, Bp, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q,
-             pv.coef, pv.deconv, pv.cd, xsub, xout, (int)sw);
-      return NFFT45_OK;
-    }
-    auto bm_pad = kbm_pad<M, kSig>;
-    const size_t smem = fast_smem<2 * M, kSig>() + 2 * sizeof(double) * M + (xout && xsub ? sizeof(double2) * M * kSig : 0);
+  template <int G>
+  int pad_g(const double2* Z, double2* Y, const ChainPlanView& pv, const double2* xsub, double2* xout) {
+    auto bm_pad = kbm_pad<R, C, G>;
+    const size_t smem =
+        fast_smem<2 * C, G>() + 2 * sizeof(double) * C + (xout && xsub ? sizeof(double2) * C * G : 0);
     NFFT_CHECK(bm_attr(bm_pad, smem));
-    LAUNCH(bm_pad, gdim(M), T, smem, st, Z, Y, Bp, t.twM, t.tw2M, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q, pv.coef,
-           pv.deconv, pv.cd, xsub, xout, (int)sw);
+    constexpr int T = fast_threads<2 * C, G>();
+    const int64_t Q = n / last_stride<2 * C>();
+    const double2* twQ = nullptr;
+    NFFT_CHECK(qtab(Q, &twQ));
+    LAUNCH(bm_pad, gdim(R, kSig / G), T, smem, st, Z, Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s, twQ,
+           (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout, (int)sw);
     return NFFT45_OK;
   }
+  int pad(const double2* Z, double2* Y, const ChainPlanView& pv, const double2* xsub, double2* xout) {
+    if (small_tiles || SG < kSig) return pad_g<kSig / 2>(Z, Y, pv, xsub, xout);  // always for C = 1024
+    return pad_g<kSig>(Z, Y, pv, xsub, xout);
+  }
 
-  // IFFT_2P row pass: 2M rows of length M -> natural-order grid
+  // IFFT_2P row pass: 2C rows of length R -> natural-order grid
   int row_grid(const double2* Y, double2* H) {
-    auto bm_row = kbm_row<M, +1>;
-    constexpr size_t smem = fast_smem<M, kSig>();
+    auto bm_row = kbm_row<R, +1>;
+    constexpr size_t smem = fast_smem<R, kSig>();
     NFFT_CHECK(bm_attr(bm_row, smem));
-    constexpr int T = fast_threads<M, kSig>();
-    LAUNCH(bm_row, gdim(2 * M), T, smem, st, Y, H, Bp, (int64_t)(2 * M), t.twM, (int)sw);
+    constexpr int T = fast_threads<R, kSig>();
+    LAUNCH(bm_row, gdim(2 * C), T, smem, st, Y, H, Bp, (int64_t)(2 * C), t.twR, (int)sw);
     return NFFT45_OK;
   }
 
   int colin(const double2* A, double2* U, const ChainPlanView& pv, double2* AT) {
-    constexpr int RW = bm_rw<M>();
-    auto bm_colin = kbm_colin<M, RW>;
-    constexpr size_t smem = fast_smem<M, 4 * RW>();
+    constexpr int RW = bm_rw<C>();
+    auto bm_colin = kbm_colin<R, C, RW>;
+    constexpr size_t smem = fast_smem<C, 4 * RW>();
     NFFT_CHECK(bm_attr(bm_colin, smem));
-    constexpr int T = fast_threads<M, 4 * RW>();
-    const int64_t Q = P / last_stride<M>();
+    constexpr int T = fast_threads<C, 4 * RW>();
+    const int64_t Q = P / last_stride<C>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    static const int bsw = getenv("NFFT45_BOUNDARY_SWAP") != nullptr;
-    const dim3 grid = bsw ? dim3((unsigned)(Bp / 4), (unsigned)(M / RW)) : dim3((unsigned)(M / RW), (unsigned)(Bp / 4));
-    LAUNCH(bm_colin, grid, T, smem, st, A, batch, U, Bp, t.twM, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.decay,
+    static const int bsw = getenv("NFFT45_BOUNDARY_SWAP") != nullptr;  // A/B switch (measured slower)
+    const dim3 grid = bsw ? dim3((unsigned)(Bp / 4), (unsigned)(R / RW)) : dim3((unsigned)(R / RW), (unsigned)(Bp / 4));
+    LAUNCH(bm_colin, grid, T, smem, st, A, batch, U, Bp, t.twC, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.decay,
            AT, bsw);
     return NFFT45_OK;
   }
 
   int rowout(const double2* Z, double2* out, const ChainPlanView& pv, const double2* xsub) {
-    constexpr int RW = bm_rw<M>();
-    auto bm_rowout = kbm_rowout<M, RW>;
-    constexpr size_t smem = fast_smem<M, 4 * RW>();
+    constexpr int RW = bm_rw<C>();
+    auto bm_rowout = kbm_rowout<R, C, RW>;
+    constexpr size_t smem = fast_smem<C, 4 * RW>();
     NFFT_CHECK(bm_attr(bm_rowout, smem));
-    constexpr int T = fast_threads<M, 4 * RW>();
+    constexpr int T = fast_threads<C, 4 * RW>();
     static const int bsw = getenv("NFFT45_BOUNDARY_SWAP") != nullptr;
-    const dim3 grid = bsw ? dim3((unsigned)(Bp / 4), (unsigned)(M / RW)) : dim3((unsigned)(M / RW), (unsigned)(Bp / 4));
-    LAUNCH(bm_rowout, grid, T, smem, st, Z, out, batch, Bp, t.twM, pv.coef, xsub, bsw);
+    const dim3 grid = bsw ? dim3((unsigned)(Bp / 4), (unsigned)(R / RW)) : dim3((unsigned)(R / RW), (unsigned)(Bp / 4));
+    LAUNCH(bm_rowout, grid, T, smem, st, Z, out, batch, Bp, t.twC, pv.coef, xsub, bsw);
     return NFFT45_OK;
   }
 };
 
-template <int M>
+template <int R, int C>
 static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes,
                           double2* out, double* norms, cudaStream_t st) {
-  using Ch = ChainBM<M>;
+  using Ch = ChainBM<R, C>;
   constexpr int64_t P = Ch::P, n = Ch::n;
   Ch ch;
   ch.st = st;
@@ -617,17 +443,8 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
   ch.Bp = ceil_div(batch, kSig) * kSig;
   ch.groups = (unsigned)(ch.Bp / kSig);
   {
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) ch.sms = nsm;
-    // persistent prefetching variants measured slower on B200 (one CTA/SM
-    // serialises the FFT compute of consecutive tiles); opt-in for experiments
-    static const bool persist = getenv("NFFT45_PERSIST") != nullptr;
-    ch.persistent = persist;
     static const bool small = getenv("NFFT45_TILE4") != nullptr;  // A/B experiment
     ch.small_tiles = small;
-    static const bool e8 = getenv("NFFT45_E8") != nullptr;
-    ch.e8 = e8;
     // signal groups fastest in the grid: concurrently resident tiles then
     // cover whole 16-KB rows of the batch-minor layout (DRAM locality; row
     // pass -22 %, column pass -8 % on B200).  NFFT45_GRID_TILES_FIRST restores
@@ -637,12 +454,15 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
   }
   int status = NFFT45_OK;
   {
-    const FftTables* a = fft_tables(M, st, &status);
+    const FftTables* a = fft_tables(R, st, &status);
     if (!a) return status;
-    const FftTables* b = fft_tables(2 * M, st, &status);
+    const FftTables* b = fft_tables(C, st, &status);
     if (!b) return status;
-    ch.t.twM = a->tw;
-    ch.t.tw2M = b->tw;
+    const FftTables* c = fft_tables(2 * C, st, &status);
+    if (!c) return status;
+    ch.t.twR = a->tw;
+    ch.t.twC = b->tw;
+    ch.t.tw2C = c->tw;
     ch.t.tP = fft_tables(P, st, &status);
     if (!ch.t.tP) return status;
     ch.t.tN = fft_tables(n, st, &status);
@@ -660,14 +480,14 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
   double2* U = Y + Bp * n;
   double2* Z = U + Bp * P;
   double2* X = Z + Bp * P;
-  double2* R = X + Bp * P;
+  double2* Rs = X + Bp * P;
   auto run = [&]() -> int {
     if (kind == 5) {
       NodeFactor fc5{pv.c5, 0.0, 0};
       // r (or s) -> spread -> colFFT_2P -> band -> mid -> Z
       auto front = [&](const double2* src, bool src_bm) -> int {
         NFFT_CHECK(spread_layout(g, n, win, src, batch, src_bm ? Bp : 0, fc5, H, Bp, st));
-        NFFT_CHECK((ch.template col<M, -1>(H, H, 2 * M, n, ch.t.tN, ch.t.twM, nullptr)));
+        NFFT_CHECK(ch.col(H, H));
         NFFT_CHECK(ch.band(H, U, pv, nullptr));
         NFFT_CHECK(ch.mid(U, Z, pv));
         return NFFT45_OK;
@@ -681,13 +501,13 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
           NFFT_CHECK(ch.row_grid(Y, H));
           NodeFactor ph{nullptr, (double)(P / 2), +1};
           // r = type2(x) - s  (s signal-major, r batch-minor)
-          NFFT_CHECK(gather_layout(g, n, win, H, Bp, batch, ph, data, 0, 1, R, Bp, st));
-          if (norms) NFFT_CHECK(norms_bm(R, P, batch, Bp, norms + (int64_t)pass * batch, st));
-          NFFT_CHECK(front(R, true));
+          NFFT_CHECK(gather_layout(g, n, win, H, Bp, batch, ph, data, 0, 1, Rs, Bp, st));
+          if (norms) NFFT_CHECK(norms_bm(Rs, P, batch, Bp, norms + (int64_t)pass * batch, st));
+          NFFT_CHECK(front(Rs, true));
         }
       }
     } else {
-      double2* AT = passes > 0 ? R : nullptr;
+      double2* AT = passes > 0 ? Rs : nullptr;
       NFFT_CHECK(ch.colin(data, U, pv, AT));
       auto back = [&](double2* dst, int64_t dst_ld, const double2* xsub, int64_t xsub_ld) -> int {
         NFFT_CHECK(ch.mid(U, Z, pv));
@@ -702,7 +522,7 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
         const bool last = pass == passes - 1;
         NodeFactor ph{nullptr, (double)(P / 2), -1};
         NFFT_CHECK(spread_layout(g, n, win, X, batch, Bp, ph, H, Bp, st));
-        NFFT_CHECK((ch.template col<M, -1>(H, H, 2 * M, n, ch.t.tN, ch.t.twM, nullptr)));
+        NFFT_CHECK(ch.col(H, H));
         NFFT_CHECK(ch.band(H, U, pv, AT));
         NFFT_CHECK(back(last ? out : X, last ? 0 : Bp, X, Bp));
       }
@@ -714,15 +534,29 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
   return status;
 }
 
+bool chain_bm_supported(int64_t P) {
+  switch (P) {
+    case 1024: case 4096: case 16384: case 65536: case 262144: case 1048576:  // R = C
+    case 2048: case 8192: case 32768: case 131072: case 524288:               // R = 2C
+      return true;
+  }
+  return false;
+}
+
 int chain_run_bm(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes, double2* out,
                  double* norms, cudaStream_t st) {
   switch (pv.P) {
-    case 1024: return chain_solve_bm<32>(pv, kind, data, batch, passes, out, norms, st);
-    case 4096: return chain_solve_bm<64>(pv, kind, data, batch, passes, out, norms, st);
-    case 16384: return chain_solve_bm<128>(pv, kind, data, batch, passes, out, norms, st);
-    case 65536: return chain_solve_bm<256>(pv, kind, data, batch, passes, out, norms, st);
-    case 262144: return chain_solve_bm<512>(pv, kind, data, batch, passes, out, norms, st);
-    case 1048576: return chain_solve_bm<1024>(pv, kind, data, batch, passes, out, norms, st);
+    case 1024: return chain_solve_bm<32, 32>(pv, kind, data, batch, passes, out, norms, st);
+    case 2048: return chain_solve_bm<64, 32>(pv, kind, data, batch, passes, out, norms, st);
+    case 4096: return chain_solve_bm<64, 64>(pv, kind, data, batch, passes, out, norms, st);
+    case 8192: return chain_solve_bm<128, 64>(pv, kind, data, batch, passes, out, norms, st);
+    case 16384: return chain_solve_bm<128, 128>(pv, kind, data, batch, passes, out, norms, st);
+    case 32768: return chain_solve_bm<256, 128>(pv, kind, data, batch, passes, out, norms, st);
+    case 65536: return chain_solve_bm<256, 256>(pv, kind, data, batch, passes, out, norms, st);
+    case 131072: return chain_solve_bm<512, 256>(pv, kind, data, batch, passes, out, norms, st);
+    case 262144: return chain_solve_bm<512, 512>(pv, kind, data, batch, passes, out, norms, st);
+    case 524288: return chain_solve_bm<1024, 512>(pv, kind, data, batch, passes, out, norms, st);
+    case 1048576: return chain_solve_bm<1024, 1024>(pv, kind, data, batch, passes, out, norms, st);
   }
   return NFFT45_ERR_INVALID_ARGUMENT;
 }

@@ -414,13 +414,13 @@ static ChainPlanView chain_view(const nfft45_plan* p) {
   return v;
 }
 
-static bool use_chain(const nfft45_plan* p) {
+static bool use_chain(const nfft45_plan* p, int64_t batch) {
   static const bool off = getenv("NFFT45_NO_CHAIN") != nullptr;  // A/B switch for tests
-  return !off && chain_supported(p->P, p->m);
+  return !off && chain_usable(p->P, p->m, batch);
 }
 
 static int type5_core(const nfft45_plan* p, const double2* s, int64_t batch, double2* out, cudaStream_t st) {
-  if (use_chain(p)) return chain_run(chain_view(p), 5, s, batch, 0, out, nullptr, st);
+  if (use_chain(p, batch)) return chain_run(chain_view(p), 5, s, batch, 0, out, nullptr, st);
   const GridDev& g = p->g->d;
   const int64_t P = p->P, n = 2 * P, K = P / 2;
   Window win = Window::make(p->m);
@@ -437,7 +437,7 @@ static int type5_core(const nfft45_plan* p, const double2* s, int64_t batch, dou
 }
 
 static int type4_core(const nfft45_plan* p, const double2* A, int64_t batch, double2* out, cudaStream_t st) {
-  if (use_chain(p)) return chain_run(chain_view(p), 4, A, batch, 0, out, nullptr, st);
+  if (use_chain(p, batch)) return chain_run(chain_view(p), 4, A, batch, 0, out, nullptr, st);
   const GridDev& g = p->g->d;
   const int64_t P = p->P, n = 2 * P, K = P / 2;
   Window win = Window::make(p->m);
@@ -477,7 +477,7 @@ static int check_norms(const double* d_norms, int64_t batch, int passes, cudaStr
 
 static int refine_core(const nfft45_plan* p, const double2* data, int64_t batch, int passes, double2* out,
                        bool type5, cudaStream_t st) {
-  if (use_chain(p) && (type5 || passes <= 1)) {
+  if (use_chain(p, batch) && (type5 || passes <= 1)) {
     Scratch norms(st);
     if (passes >= 2) NFFT_CHECK(norms.alloc(sizeof(double) * batch * passes));
     NFFT_CHECK(chain_run(chain_view(p), type5 ? 5 : 4, data, batch, passes, out, passes >= 2 ? norms.d() : nullptr,

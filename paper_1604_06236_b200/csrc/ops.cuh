@@ -71,6 +71,11 @@ struct ChainPlanView {
   const double *dd, *cd;                // deconv*decay, coef*deconv
 };
 bool chain_supported(int64_t P, int m);
+// P the batch-minor chains handle (P = R*C with R = C or R = 2C, powers of two).
+bool chain_bm_supported(int64_t P);
+// True when chain_run handles (P, m, batch): square P at any batch, the
+// rectangular R = 2C sizes for batches of 16 or more (batch-minor chains).
+bool chain_usable(int64_t P, int m, int64_t batch);
 // kind 5: type-5 (+ passes refinements); kind 4: type-4.  norms (may be
 // null): [passes][batch] residual norms for the type-5 refinement.
 int chain_run(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes, double2* out,

@@ -176,6 +176,20 @@ def test_batched_large_grids(logP):
     assert rel(nf.refine_type4(plan, data[B - 1], passes=1), full4[B - 1]) < 1e-13
 
 
+@pytest.mark.parametrize("P,B", [(2048, 16), (8192, 24), (1 << 15, 24), (1 << 17, 17), (1 << 19, 16)])
+def test_rectangular_batch_minor_chains(P, B):
+    """Odd powers of two, P = R * C with R = 2C, on the batch-minor chains
+    (batches >= 16): vs the oracle on the first and last signal, and vs the
+    single-signal solve (generic kernels) to rounding."""
+    _check_config(P, 0.3, B, 16050, passes=(1,), rows=(0, B - 1))
+    t, data = O.make_inputs(P, 0.3, B, 16050)
+    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-15, P, 2))
+    full5, full4 = nf.type5(plan, data), nf.type4(plan, data)
+    # plain solves amplify roundoff (finding 2): compare the two kernel families at that level
+    assert rel(nf.type5(plan, data[B - 1]), full5[B - 1]) < 1e-9
+    assert rel(nf.type4(plan, data[B - 1]), full4[B - 1]) < 1e-9
+
+
 @pytest.mark.parametrize("J,eta", [(0.1, 2), (0.45, 2), (0.3, 3)])
 def test_c5_sweep_2_18(J, eta):
     _check_config(1 << 18, J, 1, 16045, eta=eta, passes=(1,))
