@@ -560,6 +560,11 @@ static int run_graphed(const nfft45_plan* p, int kind, int64_t batch, int passes
     else if (++mp->gc->seen[key] >= 2 && mp->gc->execs.size() < 64) capture = true;
   }
   if (!exec && !capture) return fn(user);
+  if (exec) {  // replay straight into the caller's stream (independent solves on different streams overlap)
+    NFFT_CUDA(cudaGraphLaunch(exec, user));
+    g_launches.fetch_add(nkern, std::memory_order_relaxed);
+    return NFFT45_OK;
+  }
   cudaStream_t ls = lib_stream();
   if (!ls) return fn(user);
   cudaEvent_t e0, e1;
