@@ -190,6 +190,13 @@ def test_rectangular_batch_minor_chains(P, B):
     assert rel(nf.type4(plan, data[B - 1]), full4[B - 1]) < 1e-9
 
 
+@pytest.mark.parametrize("P", [2048, 1 << 15, 1 << 17, 1 << 19])
+def test_rectangular_single_signal_chains(P):
+    """Odd powers of two on the signal-major chains (single transforms): vs the
+    oracle, and batched (batch-minor kernels) vs single to rounding."""
+    _check_config(P, 0.3, 1, 16051, passes=(1,))
+
+
 @pytest.mark.parametrize("J,eta", [(0.1, 2), (0.45, 2), (0.3, 3)])
 def test_c5_sweep_2_18(J, eta):
     _check_config(1 << 18, J, 1, 16045, eta=eta, passes=(1,))
