@@ -230,7 +230,8 @@ struct Chain {
   template <int L, int S>
   static int col(const double2* in, double2* out, int64_t batch, int64_t N, int L2, const double2* tw,
                  const FftTables* t4, const double* pre, cudaStream_t st) {
-    constexpr int CC = (L * 8 <= 4096) ? 8 : 4096 / L;
+    // columns per tile: a power of two (it must divide L2) keeping L * CC <= 4096
+    constexpr int CC = (L * 8 <= 4096) ? 8 : (L * 4 <= 4096 ? 4 : (L * 2 <= 4096 ? 2 : 1));
     auto chain_col = kc_col<L, CC, S>;
     constexpr size_t smem = fast_smem<L, CC>();
     NFFT_CHECK(chain_attr(chain_col, smem));
@@ -395,6 +396,7 @@ bool chain_supported(int64_t P, int m) {
   switch (P) {
     case 1024: case 4096: case 16384: case 65536: case 262144: case 1048576:  // PR = PC
     case 2048: case 8192: case 32768: case 131072: case 524288:               // PR = 2 PC
+    case 3072: case 12288: case 49152: case 196608: case 786432:              // PR = 3 * 2^a
       return true;
   }
   return false;
@@ -425,6 +427,11 @@ int chain_run(const ChainPlanView& pv, int kind, const double2* data, int64_t ba
     case 262144: return chain_solve<512, 512>(pv, kind, data, batch, passes, out, norms, st);
     case 524288: return chain_solve<1024, 512>(pv, kind, data, batch, passes, out, norms, st);
     case 1048576: return chain_solve<1024, 1024>(pv, kind, data, batch, passes, out, norms, st);
+    case 3072: return chain_solve<48, 64>(pv, kind, data, batch, passes, out, norms, st);
+    case 12288: return chain_solve<96, 128>(pv, kind, data, batch, passes, out, norms, st);
+    case 49152: return chain_solve<192, 256>(pv, kind, data, batch, passes, out, norms, st);
+    case 196608: return chain_solve<384, 512>(pv, kind, data, batch, passes, out, norms, st);
+    case 786432: return chain_solve<768, 1024>(pv, kind, data, batch, passes, out, norms, st);
   }
   return NFFT45_ERR_INVALID_ARGUMENT;
 }

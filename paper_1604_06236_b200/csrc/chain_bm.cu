@@ -2,7 +2,8 @@
 // batch-minor internal layout X[index][signal] (signal stride 1, padded
 // batch Bp = multiple of 8).
 //
-// P = R * C (R = C = M for even powers of two, R = 2C for odd ones).  The
+// P = R * C (R = C = M for even powers of two, R = 2C for odd ones, R = 3 * 2^a
+// and C = 4R/3 for P = 3 * 2^k).  The
 // P-point vectors use the layout p = k + R m (k < R, m < C); the fine grid
 // n = 2P is split R x 2C for the FFT_2P / IFFT_2P four-steps, so with
 // K = P/2 = R (C/2) the band (p - K) mod n of FFT_2P row k is exactly column
@@ -538,6 +539,7 @@ bool chain_bm_supported(int64_t P) {
   switch (P) {
     case 1024: case 4096: case 16384: case 65536: case 262144: case 1048576:  // R = C
     case 2048: case 8192: case 32768: case 131072: case 524288:               // R = 2C
+    case 3072: case 12288: case 49152: case 196608: case 786432:              // R = 3 * 2^a
       return true;
   }
   return false;
@@ -557,6 +559,11 @@ int chain_run_bm(const ChainPlanView& pv, int kind, const double2* data, int64_t
     case 262144: return chain_solve_bm<512, 512>(pv, kind, data, batch, passes, out, norms, st);
     case 524288: return chain_solve_bm<1024, 512>(pv, kind, data, batch, passes, out, norms, st);
     case 1048576: return chain_solve_bm<1024, 1024>(pv, kind, data, batch, passes, out, norms, st);
+    case 3072: return chain_solve_bm<48, 64>(pv, kind, data, batch, passes, out, norms, st);
+    case 12288: return chain_solve_bm<96, 128>(pv, kind, data, batch, passes, out, norms, st);
+    case 49152: return chain_solve_bm<192, 256>(pv, kind, data, batch, passes, out, norms, st);
+    case 196608: return chain_solve_bm<384, 512>(pv, kind, data, batch, passes, out, norms, st);
+    case 786432: return chain_solve_bm<768, 1024>(pv, kind, data, batch, passes, out, norms, st);
   }
   return NFFT45_ERR_INVALID_ARGUMENT;
 }

@@ -190,6 +190,14 @@ def test_rectangular_batch_minor_chains(P, B):
     assert rel(nf.type4(plan, data[B - 1]), full4[B - 1]) < 1e-9
 
 
+@pytest.mark.parametrize("P,B", [(3072, 1), (3072, 16), (12288, 24), (49152, 1), (49152, 17), (196608, 1),
+                                 (196608, 16), (786432, 1), (786432, 16)])
+def test_three_times_power_of_two_chains(P, B):
+    """P = 3 * 2^k on the chains (PR = 3 * 2^a, PC = 4 PR / 3; radix-3 tile
+    schedules): vs the oracle, signal-major and batch-minor."""
+    _check_config(P, 0.3, B, 16052, passes=(1,), rows=(0, B - 1) if B > 1 else (0,))
+
+
 @pytest.mark.parametrize("P", [2048, 1 << 15, 1 << 17, 1 << 19])
 def test_rectangular_single_signal_chains(P):
     """Odd powers of two on the signal-major chains (single transforms): vs the
