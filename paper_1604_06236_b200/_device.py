@@ -59,13 +59,15 @@ class Operand:
         shape = (self.rows, n) if self.batched else (n,)
         return torch.empty(shape, dtype=torch.complex128, device=self.tensor.device)
 
-    def finish(self, out, dest=None):
+    def finish(self, out, dest=None, non_blocking: bool = False):
         """Return `out` in the caller's convention: numpy in -> numpy out; CUDA
         tensor in -> CUDA tensor out (async); CPU tensor in -> CPU tensor out
-        (written into `dest` when given, e.g. a pinned buffer)."""
+        (written into `dest` when given, e.g. a pinned buffer; with
+        non_blocking and a pinned dest the copy is only enqueued on the current
+        stream — torch copy_ semantics)."""
         if dest is not None:
             dest.copy_(out.reshape(dest.shape), non_blocking=True)
-            if not dest.is_cuda:
+            if not dest.is_cuda and not (non_blocking and dest.is_pinned()):
                 torch.cuda.current_stream(out.device).synchronize()
             return dest
         if self.is_torch:

@@ -256,7 +256,7 @@ def _solve(name: str, plan: InversePlan, data, label: str, passes: int | None, d
         _lib.call(f"nfft45_{name}", plan.handle, a.ptr, a.rows, out.data_ptr(), st)
     else:
         _lib.call(f"nfft45_refine_{name}", plan.handle, a.ptr, a.rows, int(passes), out.data_ptr(), st)
-    return a.finish(out, dest)
+    return a.finish(out, dest, non_blocking)
 
 
 def type5(plan: InversePlan, samples, flops: FlopCounter | None = None, out=None, non_blocking: bool = False):

@@ -357,6 +357,29 @@ def test_non_blocking_streamed_solves_complete_after_synchronize():
         assert torch.equal(o5, want5) and torch.equal(o4, want4)
 
 
+def test_non_blocking_single_signal_on_two_streams():
+    """Single-signal CPU operands with pinned outputs, type 5 and type 4 on two
+    streams with non_blocking=True: bitwise equal to the blocking path after a
+    device synchronize."""
+    P = 1 << 16
+    t, data = O.make_inputs(P, 0.3, 1, 13)
+    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-15, P, 2))
+    host = torch.from_numpy(data).pin_memory()
+    want5 = nf.refine_type5(plan, host, passes=1)
+    want4 = nf.refine_type4(plan, host, passes=1)
+    o5, o4 = torch.empty_like(host).pin_memory(), torch.empty_like(host).pin_memory()
+    side = torch.cuda.Stream()
+    for _ in range(3):
+        o5.zero_()
+        o4.zero_()
+        side.wait_stream(torch.cuda.current_stream())
+        nf.refine_type5(plan, host, passes=1, out=o5, non_blocking=True)
+        with torch.cuda.stream(side):
+            nf.refine_type4(plan, host, passes=1, out=o4, non_blocking=True)
+        torch.cuda.synchronize()
+        assert torch.equal(o5, want5) and torch.equal(o4, want4)
+
+
 _GAP_SCRIPT = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[2])
