@@ -277,13 +277,13 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="override signals per GPU (experiments)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=0, choices=[0, 1, 2],
-                    help="run the step's type-5 and type-4 solves on 1 or 2 CUDA streams (0: 2 for "
-                         "single-transform configs, whose launch-latency-bound solves overlap, else 1)")
+                    help="run the step's type-5 and type-4 solves on 1 or 2 CUDA streams (0: 2 for the "
+                         "small configs C1-C3, whose latency-bound solves overlap, else 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = dict(CONFIGS[args.config])
-    if args.streams == 0:
-        args.streams = 2 if (args.batch or cfg["B"]) == 1 else 1
+    if args.streams == 0:  # small (launch/latency-bound) configs overlap their two solves
+        args.streams = 2 if (args.batch or cfg["B"]) * cfg["P"] <= (1 << 22) else 1
     if args.batch:
         cfg["B"] = args.batch
         cfg["label"] += f" (batch override {args.batch})"
