@@ -1,6 +1,6 @@
 """Summarise a round's profiling artefacts into profiles/ (run here, no GPU).
 
-usage: python scripts/profile_summary.py <launches.csv> <full.ncu-rep> <tag> <steps-in-launch-list>
+usage: python scripts/profile_summary.py <launches.csv> <full.ncu-rep> <tag> <steps-in-launch-list> [config]
 Writes profiles/<tag>_launches.md (per-kernel share of device time from the
 ncu launch list) and profiles/<tag>_kernels.md + profiles/traffic_c4.json
 (DRAM bytes per launch from the --set full capture, used by bench.py as
@@ -52,18 +52,24 @@ def full(path):
             "issue_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "warps_active_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
             "regs": g("launch__registers_per_thread"),
+            "smem_wf": g("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+            "smem_conf": g("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+            "cycles": g("sm__cycles_active.avg"),
+            "stalls": sorted(((g(k) or 0.0, k.replace("smsp__average_warps_issue_stalled_", "").replace(
+                "_per_issue_active.ratio", "")) for k in d if k.startswith("smsp__average_warps_issue_stalled_")
+                and k.endswith("_per_issue_active.ratio") and "selected" not in k), reverse=True)[:3],
         })
     units = dict(zip(rows[0], rows[1]))
     return res, units
 
 
-def main(lpath, fpath, tag, steps):
+def main(lpath, fpath, tag, steps, config="c4"):
     os.makedirs(os.path.join(REPO, "profiles"), exist_ok=True)
     agg = launches(lpath)
     tot = sum(v[1] for v in agg.values())
-    with open(os.path.join(REPO, "profiles", f"{tag}_launches.md"), "w") as f:
+    with open(os.path.join(REPO, "profiles", f"{tag}_{config}_launches.md"), "w") as f:
         f.write(f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised)\n\n")
-        f.write(f"Command: `python bench.py --steps {steps} --warmup 3 --e2e-steps 1 --no-cpu-baseline` (C4). "
+        f.write(f"Command: `python bench.py --config {config} --steps {steps} --warmup 3 --e2e-steps 1 --no-cpu-baseline`. "
                 "Shares include warm-up/e2e launches; compare SHARES with bench.py's live kernels_ms_per_step.\n\n")
         f.write("| kernel | launches | total ms | share |\n|---|---|---|---|\n")
         for k, (n, ns) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -72,25 +78,35 @@ def main(lpath, fpath, tag, steps):
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     ur, uw = scale.get(units.get("dram__bytes_read.sum", "byte"), 1), scale.get(units.get("dram__bytes_write.sum", "byte"), 1)
     traffic = collections.defaultdict(list)
-    with open(os.path.join(REPO, "profiles", f"{tag}_kernels.md"), "w") as f:
-        f.write(f"# {tag}: ncu --set full captures (C4, batched 1024 x 2^16)\n\n")
-        f.write("| kernel | grid | ms | DRAM read GB | DRAM write GB | DRAM % peak | fp64 pipe % | L1 % | issue % | warps active % | regs |\n")
-        f.write("|---|---|---|---|---|---|---|---|---|---|---|\n")
+    tunit = units.get("gpu__time_duration.sum", "msecond")
+    tscale = {"msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6}.get(tunit, 1.0)
+    with open(os.path.join(REPO, "profiles", f"{tag}_{config}_kernels.md"), "w") as f:
+        f.write(f"# {tag}: ncu --set full captures ({config}, one bench step)\n\n")
+        f.write("Shared-memory busy = LSU shared wavefronts / (SMs x active cycles); stalls = top three "
+                "`smsp__average_warps_issue_stalled_*` per issued instruction.\n\n")
+        f.write("| kernel | grid | ms | DRAM read GB | DRAM write GB | DRAM % peak | fp64 pipe % | L1 % | SMEM busy % "
+                "| bank conflicts % | issue % | warps active % | regs | top stalls |\n")
+        f.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
         for r in res:
             rb, wb = (r["dram_bytes_read"] or 0) * ur, (r["dram_bytes_write"] or 0) * uw
             traffic[r["kernel"]].append(rb + wb)
-            f.write(f"| `{r['kernel']}` | {r['grid']} | {r['time_ms']:.3f} | {rb / 1e9:.3f} | {wb / 1e9:.3f} | "
-                    f"{r['dram_pct']:.1f} | {r['fp64_pct']:.1f} | {r['l1_pct']:.1f} | {r['issue_pct']:.1f} | "
-                    f"{r['warps_active_pct']:.1f} | {r['regs']:.0f} |\n")
+            smem = 100.0 * (r["smem_wf"] or 0) / 148 / r["cycles"] if r["cycles"] else 0.0
+            conf = 100.0 * (r["smem_conf"] or 0) / r["smem_wf"] if r["smem_wf"] else 0.0
+            st = ", ".join(f"{n} {v:.2f}" for v, n in r["stalls"])
+            f.write(f"| `{r['kernel']}` | {r['grid']} | {r['time_ms'] * tscale:.3f} | {rb / 1e9:.3f} | {wb / 1e9:.3f} | "
+                    f"{r['dram_pct']:.1f} | {r['fp64_pct']:.1f} | {r['l1_pct']:.1f} | {smem:.1f} | {conf:.1f} | "
+                    f"{r['issue_pct']:.1f} | {r['warps_active_pct']:.1f} | {r['regs']:.0f} | {st} |\n")
     short = {}
     for k, v in traffic.items():
         key = {"kbm_pad": "bm_pad", "kbm_band": "bm_band", "kbm_mid": "bm_mid", "kbm_col": "bm_col", "kbm_row": "bm_row",
                "k_spread_p": "spread_p", "k_gather_b": "gather_b", "k_gather_p": "gather_p", "kbm_colin": "bm_colin",
-               "kbm_rowout": "bm_rowout"}.get(k.split("<")[0], k.split("<")[0])
+               "kbm_rowout": "bm_rowout", "kc_col": "chain_col", "kc_band": "chain_band", "kc_mid": "chain_mid",
+               "kc_pad": "chain_pad", "kc_row": "chain_row", "k_spread_s": "spread_s1",
+               "k_gather_s": "gather_s1"}.get(k.split("<")[0], k.split("<")[0])
         short[key] = sum(v) / len(v)
-    json.dump(short, open(os.path.join(REPO, "profiles", "traffic_c4.json"), "w"), indent=1)
+    json.dump(short, open(os.path.join(REPO, "profiles", f"traffic_{config}.json"), "w"), indent=1)
     print(json.dumps(short, indent=1))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]))
+    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]), *(sys.argv[5:6]))
