@@ -33,7 +33,10 @@ def launches(path):
 
 
 def full(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):  # raw page exported on the GPU box (ncu -i rep --page raw --csv)
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[0]
     res = []
@@ -69,8 +72,10 @@ def main(lpath, fpath, tag, steps, config="c4"):
     tot = sum(v[1] for v in agg.values())
     with open(os.path.join(REPO, "profiles", f"{tag}_{config}_launches.md"), "w") as f:
         f.write(f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised)\n\n")
-        f.write(f"Command: `python bench.py --config {config} --steps {steps} --warmup 3 --e2e-steps 1 --no-cpu-baseline`. "
-                "Shares include warm-up/e2e launches; compare SHARES with bench.py's live kernels_ms_per_step.\n\n")
+        f.write(f"Command: `ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none "
+                f"python scripts/profile_step.py {config}` (scripts/gpu_profile.sh): exactly {steps} bench step(s) "
+                "(refined type-5 + refined type-4) after 3 warm-up steps; compare SHARES with bench.py's live "
+                "kernels_ms_per_step.\n\n")
         f.write("| kernel | launches | total ms | share |\n|---|---|---|---|\n")
         for k, (n, ns) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
             f.write(f"| `{k}` | {n} | {ns / 1e6:.3f} | {ns / tot * 100:.1f}% |\n")
@@ -79,7 +84,7 @@ def main(lpath, fpath, tag, steps, config="c4"):
     ur, uw = scale.get(units.get("dram__bytes_read.sum", "byte"), 1), scale.get(units.get("dram__bytes_write.sum", "byte"), 1)
     traffic = collections.defaultdict(list)
     tunit = units.get("gpu__time_duration.sum", "msecond")
-    tscale = {"msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6}.get(tunit, 1.0)
+    tscale = {"msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "us": 1e-3, "ns": 1e-6}.get(tunit, 1.0)
     with open(os.path.join(REPO, "profiles", f"{tag}_{config}_kernels.md"), "w") as f:
         f.write(f"# {tag}: ncu --set full captures ({config}, one bench step)\n\n")
         f.write("Shared-memory busy = LSU shared wavefronts / (SMs x active cycles); stalls = top three "
