@@ -56,6 +56,28 @@ __device__ __forceinline__ void cpa8(void* sdst, const void* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
 }
+
+// L2 prefetch of the input tile of the CTA `pf` launch slots ahead (about one
+// wave of resident CTAs): its DRAM reads then run while this wave computes,
+// and that CTA's first pass hits L2 instead of waiting on DRAM.  No registers
+// or shared memory are held for it (bulk prefetch, fire and forget).
+__device__ __forceinline__ void pf_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+// block coordinates (x, y) of the launch slot `pf` ahead, false past the grid
+__device__ __forceinline__ bool ahead_block(int pf, unsigned& x, unsigned& y) {
+  if (pf <= 0) return false;
+  const unsigned long long nx =
+      blockIdx.x + (unsigned long long)gridDim.x * blockIdx.y + (unsigned long long)pf;
+  if (nx >= (unsigned long long)gridDim.x * gridDim.y) return false;
+  x = (unsigned)(nx % gridDim.x);
+  y = (unsigned)(nx / gridDim.x);
+  return true;
+}
+// prefetch `rows` rows of `bytes` each, `stride` elements apart, from p
+__device__ __forceinline__ void pf_rows(const double2* p, int64_t stride, int rows, unsigned bytes) {
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) pf_l2(p + (int64_t)i * stride, bytes);
+}
 }  // namespace
 
 // column pass: columns n2 = blockIdx.x of x[i * L2 + n2] (length L), optional
@@ -64,10 +86,16 @@ template <int L, int S>
 __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<L, kSig>())) kbm_col(
     const double2* __restrict__ in, double2* __restrict__ out, int L2, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ lo, const double2* __restrict__ hi, int sh, const double2* __restrict__ twQ, int Q,
-    const double* __restrict__ pre, int sw) {
+    const double* __restrict__ pre, int sw, int pf) {
   extern __shared__ double2 sm[];
   const int n2 = sw ? blockIdx.y : blockIdx.x;
   const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * kSig;
+  {
+    unsigned ax, ay;
+    if (ahead_block(pf, ax, ay))
+      pf_rows(in + (int64_t)(sw ? ay : ax) * Bp + (int64_t)(sw ? ax : ay) * kSig, (int64_t)L2 * Bp, L,
+              kSig * sizeof(double2));
+  }
   auto ld = [&](int i, int c) -> double2 {
     const int64_t idx = (int64_t)i * L2 + n2;
     double2 v = in[idx * Bp + b0 + c];
@@ -91,7 +119,7 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
     const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
-    const double* __restrict__ dd, const double2* __restrict__ sub, int sw) {
+    const double* __restrict__ dd, const double2* __restrict__ sub, int sw, int pf) {
   constexpr int NR = 2 * C;
   extern __shared__ double2 sm[];
   double* s_t0 = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + fast_smem<NR, SG>());
@@ -99,6 +127,14 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
   double2* s_sb = reinterpret_cast<double2*>(s_t1 + C);
   const int k1 = sw ? blockIdx.y : blockIdx.x;
   const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * SG;
+  {
+    unsigned ax, ay;
+    if (ahead_block(pf, ax, ay)) {
+      const int64_t k = sw ? ay : ax, bb = (int64_t)(sw ? ax : ay) * SG;
+      pf_rows(T + k * NR * Bp + bb, Bp, NR, SG * sizeof(double2));
+      if (sub) pf_rows(sub + k * Bp + bb, (int64_t)R * Bp, C, SG * sizeof(double2));
+    }
+  }
   for (int m1 = threadIdx.x; m1 < C; m1 += blockDim.x) {
     const int64_t p = (int64_t)k1 + (int64_t)R * m1;
     if (sub) {
@@ -140,11 +176,16 @@ template <int R, int C>
 __global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<R, kSig>())) kbm_mid(
     const double2* __restrict__ U, double2* __restrict__ Z, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
-    const double2* __restrict__ ks, int sw) {
+    const double2* __restrict__ ks, int sw, int pf) {
   extern __shared__ double2 sm[];
   double2* s_ks = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + fast_smem<R, kSig>());
   const int r = sw ? blockIdx.y : blockIdx.x;
   const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * kSig;
+  {
+    unsigned ax, ay;
+    if (ahead_block(pf, ax, ay))
+      pf_rows(U + (int64_t)(sw ? ay : ax) * R * Bp + (int64_t)(sw ? ax : ay) * kSig, Bp, R, kSig * sizeof(double2));
+  }
   for (int k2 = threadIdx.x; k2 < R; k2 += blockDim.x) cpa16(&s_ks[k2], &ks[(int64_t)r + (int64_t)C * k2]);
   cpa_commit();
   auto ld1 = [&](int i, int c) -> double2 { return U[((int64_t)r * R + i) * Bp + b0 + c]; };
@@ -165,7 +206,7 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
     const double2* __restrict__ Z, double2* __restrict__ Y, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
-    const double* __restrict__ cd, const double2* __restrict__ xsub, double2* __restrict__ xout, int sw) {
+    const double* __restrict__ cd, const double2* __restrict__ xsub, double2* __restrict__ xout, int sw, int pf) {
   constexpr int NC = 2 * C;
   constexpr bool kLead2 = FastTraits<NC>::radix(0) == 2;
   extern __shared__ double2 sm[];
@@ -174,6 +215,22 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
   double2* s_xs = reinterpret_cast<double2*>(s_t1 + C);
   const int r = sw ? blockIdx.y : blockIdx.x;
   const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * SG;
+  // tile base pointers + 32-bit in-tile offsets (2C * Bp and R * C * Bp fit in
+  // 31 bits, checked on the host): keeps the epilogue's address arithmetic out
+  // of 64-bit registers (no spills at the 128-register budget)
+  const unsigned ub = (unsigned)Bp;
+  const double2* __restrict__ Zt = Z + (int64_t)r * C * Bp + b0;
+  double2* __restrict__ Yt = Y + (int64_t)r * Bp + b0;
+  double2* __restrict__ Xt = xout ? xout + (int64_t)r * Bp + b0 : nullptr;
+  const double2* __restrict__ XSt = xsub ? xsub + (int64_t)r * Bp + b0 : nullptr;
+  {
+    unsigned ax, ay;
+    if (ahead_block(pf, ax, ay)) {
+      const int64_t k = sw ? ay : ax, bb = (int64_t)(sw ? ax : ay) * SG;
+      pf_rows(Z + k * C * Bp + bb, Bp, C, SG * sizeof(double2));
+      if (xout && xsub) pf_rows(xsub + k * Bp + bb, (int64_t)R * Bp, C, SG * sizeof(double2));
+    }
+  }
   // per-tile tables (and the xsub tile) staged with cp.async, waited for at
   // the end of the first FFT pass
   for (int k2 = threadIdx.x; k2 < C; k2 += blockDim.x) {
@@ -187,15 +244,14 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
   }
   if (xout && xsub)
     for (int e = threadIdx.x; e < C * SG; e += blockDim.x)
-      cpa16(&s_xs[e], &xsub[((int64_t)r + (int64_t)R * (e / SG)) * Bp + b0 + e % SG]);
+      cpa16(&s_xs[e], &XSt[(unsigned)(R * (e / SG)) * ub + e % SG]);
   cpa_commit();
-  auto ld1 = [&](int i, int c) -> double2 { return Z[((int64_t)r * C + i) * Bp + b0 + c]; };
+  auto ld1 = [&](int i, int c) -> double2 { return Zt[(unsigned)i * ub + c]; };
   auto st1 = [&](int k2, int c, double2 v) {
-    const int64_t p = (int64_t)r + (int64_t)R * k2;
     if (xout) {
       v = rsc(v, s_t0[k2]);
       if (xsub) v = csub(s_xs[k2 * SG + c], v);
-      xout[p * Bp + b0 + c] = v;
+      Xt[(unsigned)(R * k2) * ub + c] = v;
       v = rsc(v, s_t1[k2]);
     } else {
       v = rsc(v, s_t0[k2]);
@@ -221,7 +277,7 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
   };
   fast_tile_fft<C, SG, -1, true, HalfTr<C>>(sm, ld1, st1, twR, NoPostTw(), CpAsyncWaitHook());
   __syncthreads();
-  auto st2 = [&](int k, int c, double2 v) { Y[((int64_t)k * R + r) * Bp + b0 + c] = v; };
+  auto st2 = [&](int k, int c, double2 v) { Yt[(unsigned)(k * R) * ub + c] = v; };
   const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r, 0};
   if constexpr (kLead2) {
     fast_tile_fft_from<NC, SG, +1, true, 1, 2>(sm, st2, twC, pt);
@@ -235,10 +291,15 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
 template <int L, int S>
 __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<L, kSig>())) kbm_row(const double2* __restrict__ in,
                                                                   double2* __restrict__ out, int64_t Bp, int64_t R1,
-                                                                  const double2* __restrict__ tw, int sw) {
+                                                                  const double2* __restrict__ tw, int sw, int pf) {
   extern __shared__ double2 sm[];
   const int r = sw ? blockIdx.y : blockIdx.x;
   const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * kSig;
+  {
+    unsigned ax, ay;
+    if (ahead_block(pf, ax, ay))
+      pf_rows(in + (int64_t)(sw ? ay : ax) * L * Bp + (int64_t)(sw ? ax : ay) * kSig, Bp, L, kSig * sizeof(double2));
+  }
   auto ld = [&](int i, int c) -> double2 { return in[((int64_t)r * L + i) * Bp + b0 + c]; };
   auto st = [&](int k, int c, double2 v) { out[((int64_t)r + R1 * k) * Bp + b0 + c] = v; };
   fast_tile_fft<L, kSig, S, true>(sm, ld, st, tw);
@@ -318,6 +379,7 @@ struct ChainBM {
   cudaStream_t st;
   bool small_tiles = false;  // 4-signal tiles for the two-FFT kernels (A/B experiment)
   bool sw = false;           // grid order: signal groups fastest (blockIdx.x) instead of tile index
+  int pf = 0;                // L2 prefetch distance in launch slots (0: off)
   // grid of (tiles x groups*mult); with sw the signal groups run fastest
   dim3 gdim(int tiles, int mult = 1) const {
     return sw ? dim3(groups * mult, (unsigned)tiles) : dim3((unsigned)tiles, groups * mult);
@@ -341,7 +403,7 @@ struct ChainBM {
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
     LAUNCH(bm_col, gdim(2 * C), T, smem, st, in, out, 2 * C, Bp, t.twR, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q,
-           nullptr, (int)sw);
+           nullptr, (int)sw, pf);
     return NFFT45_OK;
   }
 
@@ -355,7 +417,7 @@ struct ChainBM {
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
     LAUNCH(bm_band, gdim(R, kSig / G), T, smem, st, T_, U, Bp, t.tw2C, t.twC, t.tP->lo, t.tP->hi, t.tP->s, twQ,
-           (int)Q, pv.deconv, pv.decay, pv.dd, sub, (int)sw);
+           (int)Q, pv.deconv, pv.decay, pv.dd, sub, (int)sw, pf);
     return NFFT45_OK;
   }
   int band(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub) {
@@ -371,7 +433,7 @@ struct ChainBM {
     const int64_t Q = P / last_stride<R>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    LAUNCH(bm_mid, gdim(C), T, smem, st, U, Z, Bp, t.twR, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.ks, (int)sw);
+    LAUNCH(bm_mid, gdim(C), T, smem, st, U, Z, Bp, t.twR, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.ks, (int)sw, pf);
     return NFFT45_OK;
   }
 
@@ -386,7 +448,7 @@ struct ChainBM {
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
     LAUNCH(bm_pad, gdim(R, kSig / G), T, smem, st, Z, Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s, twQ,
-           (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout, (int)sw);
+           (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout, (int)sw, pf);
     return NFFT45_OK;
   }
   int pad(const double2* Z, double2* Y, const ChainPlanView& pv, const double2* xsub, double2* xout) {
@@ -400,7 +462,7 @@ struct ChainBM {
     constexpr size_t smem = fast_smem<R, kSig>();
     NFFT_CHECK(bm_attr(bm_row, smem));
     constexpr int T = fast_threads<R, kSig>();
-    LAUNCH(bm_row, gdim(2 * C), T, smem, st, Y, H, Bp, (int64_t)(2 * C), t.twR, (int)sw);
+    LAUNCH(bm_row, gdim(2 * C), T, smem, st, Y, H, Bp, (int64_t)(2 * C), t.twR, (int)sw, pf);
     return NFFT45_OK;
   }
 
@@ -452,6 +514,11 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
     // the tile-major order for A/B runs.
     static const bool tiles_first = getenv("NFFT45_GRID_TILES_FIRST") != nullptr;
     ch.sw = !tiles_first;
+    // L2 prefetch of the tile one wave ahead (NFFT45_PREFETCH=<launch slots>):
+    // measured slower on B200 (C4: band +0.6 ms, col +0.5 ms at 296 slots),
+    // kept as an opt-in A/B switch, off by default
+    static const int pf_env = getenv("NFFT45_PREFETCH") ? atoi(getenv("NFFT45_PREFETCH")) : 0;
+    ch.pf = pf_env;
   }
   int status = NFFT45_OK;
   {
