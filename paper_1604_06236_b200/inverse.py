@@ -12,6 +12,7 @@ import os
 
 import ctypes
 import threading
+import weakref
 
 import numpy as np
 
@@ -182,6 +183,63 @@ def _charge_type4(f, P, taps):
 STREAM_CHUNK = int(os.environ.get("NFFT45_STREAM_CHUNK", "64"))
 
 
+class _HostPipe:
+    """Per-device pipeline of the streamed host path: persistent H2D / solve / D2H
+    streams and two staging slots, so consecutive calls keep the copy engines
+    busy across call boundaries (the next call's uploads start while the previous
+    call's last downloads drain) instead of draining the pipeline at every call.
+
+    Ordering: the caller's current stream waits for the downloads at the end of
+    every call (results are valid once it is synchronized); the downloads of a
+    call wait for the caller's stream at entry (the destination may be in use
+    there); the uploads wait only for the staging slot and for this module's own
+    in-flight non_blocking destinations that overlap the input (an output fed
+    back as the next input); a plan's first solve here waits for the caller's
+    stream (plan tables built there)."""
+
+    def __init__(self, dev: int):
+        torch = _device.torch
+        self.dev = dev
+        self.lock = threading.Lock()
+        self.h2d, self.comp, self.d2h = (torch.cuda.Stream(dev) for _ in range(3))
+        self.loaded = [torch.cuda.Event() for _ in range(2)]   # upload of slot k finished
+        self.done = [torch.cuda.Event() for _ in range(2)]     # solve of slot k finished
+        self.drained = [torch.cuda.Event() for _ in range(2)]  # download of slot k finished
+        self.key = None
+        self.bufs_in = self.bufs_out = None
+        self.pending = []     # (first byte, last byte, event): non_blocking destinations in flight
+        self.plans = weakref.WeakSet()  # plans already ordered after their build
+
+    def buffers(self, chunk: int, P: int):
+        torch = _device.torch
+        if self.key != (chunk, P):
+            with torch.cuda.stream(self.comp):
+                mk = lambda: torch.empty((chunk, P), dtype=torch.complex128, device=f"cuda:{self.dev}")
+                self.bufs_in, self.bufs_out = [mk(), mk()], [mk(), mk()]
+            for b in self.bufs_in + self.bufs_out:  # used on the copy streams until freed
+                b.record_stream(self.h2d)
+                b.record_stream(self.d2h)
+            self.key = (chunk, P)
+        return self.bufs_in, self.bufs_out
+
+
+_PIPES: dict = {}
+_PIPES_LOCK = threading.Lock()
+
+
+def _pipe(dev: int) -> _HostPipe:
+    with _PIPES_LOCK:
+        p = _PIPES.get(dev)
+        if p is None:
+            p = _PIPES[dev] = _HostPipe(dev)
+        return p
+
+
+def _span(t):
+    lo = t.data_ptr()
+    return lo, lo + t.numel() * t.element_size()
+
+
 def _solve_streamed(name: str, plan: InversePlan, host, passes, dest, non_blocking: bool = False):
     """Pipelined host -> device -> host solve of a [batch, P] CPU tensor.
 
@@ -195,45 +253,52 @@ def _solve_streamed(name: str, plan: InversePlan, host, passes, dest, non_blocki
         dest = torch.empty((B, P), dtype=torch.complex128, pin_memory=True)
     src = host if host.dtype == torch.complex128 else host.to(torch.complex128)
     main = torch.cuda.current_stream(dev)
-    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    pipe = _pipe(dev)
     chunk = STREAM_CHUNK
-    bufs_in = [torch.empty((chunk, P), dtype=torch.complex128, device=f"cuda:{dev}") for _ in range(2)]
-    bufs_out = [torch.empty((chunk, P), dtype=torch.complex128, device=f"cuda:{dev}") for _ in range(2)]
-    done = [torch.cuda.Event() for _ in range(2)]      # solve of the chunk in slot k finished
-    drained = [torch.cuda.Event() for _ in range(2)]   # D2H of slot k finished
-    loaded = [torch.cuda.Event() for _ in range(2)]
-    for e in done + drained:
-        e.record(main)
-    st = main.cuda_stream
-    for i, lo in enumerate(range(0, B, chunk)):
-        hi = min(lo + chunk, B)
-        k, m = i % 2, hi - lo
-        with torch.cuda.stream(h2d):
-            h2d.wait_event(done[k])
-            bufs_in[k][:m].copy_(src[lo:hi], non_blocking=True)
-            loaded[k].record(h2d)
-        main.wait_event(loaded[k])
-        main.wait_event(drained[k])
-        if passes is None:
-            _lib.call(f"nfft45_{name}", plan.handle, bufs_in[k].data_ptr(), m, bufs_out[k].data_ptr(), st)
-        else:
-            _lib.call(f"nfft45_refine_{name}", plan.handle, bufs_in[k].data_ptr(), m, int(passes),
-                      bufs_out[k].data_ptr(), st)
-        done[k].record(main)
-        with torch.cuda.stream(d2h):
-            d2h.wait_event(done[k])
-            dest[lo:hi].copy_(bufs_out[k][:m], non_blocking=True)
-            drained[k].record(d2h)
-    # the staging buffers are in flight on the copy streams: keep the caching
-    # allocator from handing them out again before those streams pass here
-    for b in bufs_in:
-        b.record_stream(h2d)
-    for b in bufs_out:
-        b.record_stream(d2h)
-    main.wait_stream(h2d)
-    main.wait_stream(d2h)
+    with pipe.lock:
+        bufs_in, bufs_out = pipe.buffers(chunk, P)
+        entry = torch.cuda.Event()
+        entry.record(main)
+        if plan not in pipe.plans:
+            pipe.comp.wait_event(entry)
+            pipe.plans.add(plan)
+        s_lo, s_hi = _span(src)
+        live = []
+        for lo, hi, ev in pipe.pending:
+            if ev.query():
+                continue
+            live.append((lo, hi, ev))
+            if lo < s_hi and s_lo < hi:
+                pipe.h2d.wait_event(ev)
+        pipe.pending = live
+        pipe.d2h.wait_event(entry)
+        st = pipe.comp.cuda_stream
+        for i, lo in enumerate(range(0, B, chunk)):
+            hi = min(lo + chunk, B)
+            k, m = i % 2, hi - lo
+            pipe.h2d.wait_event(pipe.done[k])       # slot k's input consumed
+            with torch.cuda.stream(pipe.h2d):
+                bufs_in[k][:m].copy_(src[lo:hi], non_blocking=True)
+            pipe.loaded[k].record(pipe.h2d)
+            pipe.comp.wait_event(pipe.loaded[k])
+            pipe.comp.wait_event(pipe.drained[k])   # slot k's output downloaded
+            if passes is None:
+                _lib.call(f"nfft45_{name}", plan.handle, bufs_in[k].data_ptr(), m, bufs_out[k].data_ptr(), st)
+            else:
+                _lib.call(f"nfft45_refine_{name}", plan.handle, bufs_in[k].data_ptr(), m, int(passes),
+                          bufs_out[k].data_ptr(), st)
+            pipe.done[k].record(pipe.comp)
+            pipe.d2h.wait_event(pipe.done[k])
+            with torch.cuda.stream(pipe.d2h):
+                dest[lo:hi].copy_(bufs_out[k][:m], non_blocking=True)
+            pipe.drained[k].record(pipe.d2h)
+        fin = torch.cuda.Event()
+        fin.record(pipe.d2h)
+        main.wait_event(fin)
+        if non_blocking:
+            pipe.pending.append((*_span(dest), fin))
     if not non_blocking:
-        d2h.synchronize()
+        fin.synchronize()
     return dest
 
 

@@ -357,6 +357,33 @@ def test_non_blocking_streamed_solves_complete_after_synchronize():
         assert torch.equal(o5, want5) and torch.equal(o4, want4)
 
 
+def test_non_blocking_streamed_output_fed_back_as_input():
+    """The streamed pipeline persists across calls (uploads of the next call do not
+    wait for the caller's stream): a non_blocking output fed straight back as the
+    next call's input is still ordered after its own download, and a second plan
+    built in between is ordered after its build."""
+    from paper_1604_06236_b200 import inverse as inv
+
+    P, B = 4096, inv.STREAM_CHUNK * 2 + 9
+    t, data = O.make_inputs(P, 0.3, B, 14)
+    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-15, P, 2))
+    host = torch.from_numpy(data).pin_memory()
+    want5 = nf.refine_type5(plan, host, passes=1)
+    want45 = nf.refine_type4(plan, want5, passes=1)
+    t2, _ = O.make_inputs(P, 0.2, 1, 15)
+    plan2 = nf.build_plan(nf.validate_grid(t2), nf.MethodParams.from_mu(1e-15, P, 2))
+    want2 = nf.type5(plan2, host)
+    for _ in range(2):
+        o5, o45 = torch.zeros_like(host).pin_memory(), torch.zeros_like(host).pin_memory()
+        nf.refine_type5(plan, host, passes=1, out=o5, non_blocking=True)
+        nf.refine_type4(plan, o5, passes=1, out=o45, non_blocking=True)
+        plan3 = nf.build_plan(nf.validate_grid(t2), nf.MethodParams.from_mu(1e-15, P, 2))
+        o2 = torch.zeros_like(host).pin_memory()
+        nf.type5(plan3, host, out=o2, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        assert torch.equal(o5, want5) and torch.equal(o45, want45) and torch.equal(o2, want2)
+
+
 def test_non_blocking_single_signal_on_two_streams():
     """Single-signal CPU operands with pinned outputs, type 5 and type 4 on two
     streams with non_blocking=True: bitwise equal to the blocking path after a
