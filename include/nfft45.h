@@ -229,6 +229,22 @@ int nfft45_refine_type5(const nfft45_plan* p, const double* s_dev, int64_t batch
 int nfft45_refine_type4(const nfft45_plan* p, const double* A_dev, int64_t batch,
                         int passes, double* a_dev, void* stream);
 
+/* type5 / type4 / refine_type5 / refine_type4 on HOST-resident operands —
+ * the reference's own calling convention (numpy arrays in host memory,
+ * inverse.py:101-202).  kind = 5 or 4; passes = -1 for the plain solve, else
+ * the refine passes.  in_host, out_host: [batch][P] complex128 (pinned memory
+ * for asynchronous copies; pageable memory works but copies synchronously).
+ * The batch is streamed through the device in chunks of `chunk` signals on a
+ * per-(device, stream) pipeline of H2D / solve / D2H streams that persists
+ * across calls, so copies in both directions overlap the solves and the next
+ * call's uploads.  `stream` waits for the results; blocking != 0 also waits
+ * on the host.  With blocking == 0 the result is valid once `stream` (or the
+ * device) is synchronized; an output fed back as a later call's input is
+ * ordered after its download. */
+int nfft45_solve_host(const nfft45_plan* p, int kind, int passes, const double* in_host,
+                      int64_t batch, double* out_host, int64_t chunk, int blocking,
+                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -12,7 +12,6 @@ import os
 
 import ctypes
 import threading
-import weakref
 
 import numpy as np
 
@@ -181,133 +180,43 @@ def _charge_type4(f, P, taps):
 # signals: H2D of chunk i+1 and D2H of chunk i-1 (two copy streams, PCIe is
 # full duplex) overlap the solve of chunk i.
 STREAM_CHUNK = int(os.environ.get("NFFT45_STREAM_CHUNK", "64"))
-
-
-class _HostPipe:
-    """Per-device pipeline of the streamed host path: persistent H2D / solve / D2H
-    streams and two staging slots, so consecutive calls keep the copy engines
-    busy across call boundaries (the next call's uploads start while the previous
-    call's last downloads drain) instead of draining the pipeline at every call.
-
-    Ordering: the caller's current stream waits for the downloads at the end of
-    every call (results are valid once it is synchronized); the downloads of a
-    call wait for the caller's stream at entry (the destination may be in use
-    there); the uploads wait only for the staging slot and for this module's own
-    in-flight non_blocking destinations that overlap the input (an output fed
-    back as the next input); a plan's first solve here waits for the caller's
-    stream (plan tables built there)."""
-
-    def __init__(self, dev: int):
-        torch = _device.torch
-        self.dev = dev
-        self.lock = threading.Lock()
-        self.h2d, self.comp, self.d2h = (torch.cuda.Stream(dev) for _ in range(3))
-        self.loaded = [torch.cuda.Event() for _ in range(2)]   # upload of slot k finished
-        self.done = [torch.cuda.Event() for _ in range(2)]     # solve of slot k finished
-        self.drained = [torch.cuda.Event() for _ in range(2)]  # download of slot k finished
-        self.key = None
-        self.bufs_in = self.bufs_out = None
-        self.pending = []     # (first byte, last byte, event): non_blocking destinations in flight
-        self.plans = weakref.WeakSet()  # plans already ordered after their build
-
-    def buffers(self, chunk: int, P: int):
-        torch = _device.torch
-        if self.key != (chunk, P):
-            with torch.cuda.stream(self.comp):
-                mk = lambda: torch.empty((chunk, P), dtype=torch.complex128, device=f"cuda:{self.dev}")
-                self.bufs_in, self.bufs_out = [mk(), mk()], [mk(), mk()]
-            for b in self.bufs_in + self.bufs_out:  # used on the copy streams until freed
-                b.record_stream(self.h2d)
-                b.record_stream(self.d2h)
-            self.key = (chunk, P)
-        return self.bufs_in, self.bufs_out
-
-
-_PIPES: dict = {}
-_PIPES_LOCK = threading.Lock()
-
-
-def _pipe(dev: int) -> _HostPipe:
-    with _PIPES_LOCK:
-        p = _PIPES.get(dev)
-        if p is None:
-            p = _PIPES[dev] = _HostPipe(dev)
-        return p
-
-
-def _span(t):
-    lo = t.data_ptr()
-    return lo, lo + t.numel() * t.element_size()
+# Smaller host operands (down to this many bytes) take the same pipeline as a
+# single chunk, so a call's upload overlaps the previous call's solve and
+# download (NFFT45_PIPE_MIN_BYTES overrides, for A/B runs).
+PIPE_MIN_BYTES = int(os.environ.get("NFFT45_PIPE_MIN_BYTES", "0"))
 
 
 def _solve_streamed(name: str, plan: InversePlan, host, passes, dest, non_blocking: bool = False):
-    """Pipelined host -> device -> host solve of a [batch, P] CPU tensor.
+    """Pipelined host -> device -> host solve of a [batch, P] (or [P]) CPU tensor
+    through the library's native host pipeline (nfft45_solve_host): chunks of
+    STREAM_CHUNK signals, H2D / solve / D2H on per-(device, stream) streams that
+    persist across calls, so both copy directions stay busy across calls.
 
     non_blocking (extension, torch's copy_ semantics): return once the copies
     and solves are enqueued; the result in `dest` (pinned) is valid after the
     caller synchronizes the current stream (or the device)."""
     torch = _device.torch
     dev = plan.device
-    B, P = host.shape
+    P = host.shape[-1]
     if dest is None:
-        dest = torch.empty((B, P), dtype=torch.complex128, pin_memory=True)
+        dest = torch.empty(host.shape, dtype=torch.complex128, pin_memory=True)
     src = host if host.dtype == torch.complex128 else host.to(torch.complex128)
-    main = torch.cuda.current_stream(dev)
-    pipe = _pipe(dev)
-    chunk = STREAM_CHUNK
-    with pipe.lock:
-        bufs_in, bufs_out = pipe.buffers(chunk, P)
-        entry = torch.cuda.Event()
-        entry.record(main)
-        if plan not in pipe.plans:
-            pipe.comp.wait_event(entry)
-            pipe.plans.add(plan)
-        s_lo, s_hi = _span(src)
-        live = []
-        for lo, hi, ev in pipe.pending:
-            if ev.query():
-                continue
-            live.append((lo, hi, ev))
-            if lo < s_hi and s_lo < hi:
-                pipe.h2d.wait_event(ev)
-        pipe.pending = live
-        pipe.d2h.wait_event(entry)
-        st = pipe.comp.cuda_stream
-        for i, lo in enumerate(range(0, B, chunk)):
-            hi = min(lo + chunk, B)
-            k, m = i % 2, hi - lo
-            pipe.h2d.wait_event(pipe.done[k])       # slot k's input consumed
-            with torch.cuda.stream(pipe.h2d):
-                bufs_in[k][:m].copy_(src[lo:hi], non_blocking=True)
-            pipe.loaded[k].record(pipe.h2d)
-            pipe.comp.wait_event(pipe.loaded[k])
-            pipe.comp.wait_event(pipe.drained[k])   # slot k's output downloaded
-            if passes is None:
-                _lib.call(f"nfft45_{name}", plan.handle, bufs_in[k].data_ptr(), m, bufs_out[k].data_ptr(), st)
-            else:
-                _lib.call(f"nfft45_refine_{name}", plan.handle, bufs_in[k].data_ptr(), m, int(passes),
-                          bufs_out[k].data_ptr(), st)
-            pipe.done[k].record(pipe.comp)
-            pipe.d2h.wait_event(pipe.done[k])
-            with torch.cuda.stream(pipe.d2h):
-                dest[lo:hi].copy_(bufs_out[k][:m], non_blocking=True)
-            pipe.drained[k].record(pipe.d2h)
-        fin = torch.cuda.Event()
-        fin.record(pipe.d2h)
-        main.wait_event(fin)
-        if non_blocking:
-            pipe.pending.append((*_span(dest), fin))
-    if not non_blocking:
-        fin.synchronize()
+    src = src.contiguous()
+    rows = src.numel() // P
+    kind = 5 if name == "type5" else 4
+    _lib.call("nfft45_solve_host", plan.handle, kind, -1 if passes is None else int(passes), src.data_ptr(), rows,
+              dest.data_ptr(), STREAM_CHUNK, 0 if non_blocking else 1, _device.stream_handle(dev))
     return dest
 
 
 def _solve(name: str, plan: InversePlan, data, label: str, passes: int | None, dest=None,
            non_blocking: bool = False):
     torch = _device.torch
-    if (isinstance(data, torch.Tensor) and not data.is_cuda and data.dim() == 2
-            and data.shape[0] > STREAM_CHUNK and data.shape[-1] == plan.size
-            and (dest is None or not dest.is_cuda)):
+    if (isinstance(data, torch.Tensor) and not data.is_cuda and data.dim() in (1, 2)
+            and data.shape[-1] == plan.size
+            and ((data.dim() == 2 and data.shape[0] > STREAM_CHUNK) or data.numel() * 16 >= PIPE_MIN_BYTES)
+            and (dest is None or (not dest.is_cuda and dest.dtype == torch.complex128
+                                  and dest.is_contiguous() and dest.shape == data.shape))):
         return _solve_streamed(name, plan, data, passes, dest,
                                non_blocking and dest is not None and dest.is_pinned())
     a = _device.operand(data, plan.device, length=plan.size, name=label)
