@@ -88,6 +88,14 @@ def operand(values, dev: int, length: int | None = None, name: str = "vector") -
         host = not t.is_cuda
         t = t.to(device=f"cuda:{dev}", dtype=torch.complex128, non_blocking=True).contiguous()
         return Operand(t, True, t.dim() == 2, host)
+    arr = host_array(values, length, name)
+    t = torch.from_numpy(arr).to(f"cuda:{dev}")
+    return Operand(t, False, arr.ndim == 2)
+
+
+def host_array(values, length: int | None = None, name: str = "vector") -> np.ndarray:
+    """Coerce array-like `values` to a contiguous complex128 numpy array with the
+    reference's checks (grid.py:21-32: 1-D, nonempty, finite; [batch, P] allowed)."""
     arr = np.asarray(values, dtype=np.complex128)
     if arr.ndim not in (1, 2):
         raise LengthMismatchError(f"{name} must be one-dimensional, got shape {arr.shape}")
@@ -100,8 +108,7 @@ def operand(values, dev: int, length: int | None = None, name: str = "vector") -
     arr = np.ascontiguousarray(arr)
     if not arr.flags.writeable:
         arr = arr.copy()
-    t = torch.from_numpy(arr).to(f"cuda:{dev}")
-    return Operand(t, False, arr.ndim == 2)
+    return arr
 
 
 def real_table(values, dev: int):

@@ -212,7 +212,16 @@ def _solve_streamed(name: str, plan: InversePlan, host, passes, dest, non_blocki
 def _solve(name: str, plan: InversePlan, data, label: str, passes: int | None, dest=None,
            non_blocking: bool = False):
     torch = _device.torch
-    if (isinstance(data, torch.Tensor) and not data.is_cuda and data.dim() in (1, 2)
+    if not isinstance(data, torch.Tensor) and dest is None:
+        # the reference's convention (array-like in host memory -> numpy out):
+        # validated here, solved through the native host pipeline
+        arr = _device.host_array(data, plan.size, label)
+        res = np.empty_like(arr)
+        _lib.call("nfft45_solve_host", plan.handle, 5 if name == "type5" else 4, -1 if passes is None else int(passes),
+                  arr.ctypes.data, arr.size // plan.size, res.ctypes.data, STREAM_CHUNK, 1,
+                  _device.stream_handle(plan.device))
+        return res
+    if (isinstance(data, torch.Tensor) and not data.is_cuda and data.dim() in (1, 2) and data.numel() > 0
             and data.shape[-1] == plan.size
             and ((data.dim() == 2 and data.shape[0] > STREAM_CHUNK) or data.numel() * 16 >= PIPE_MIN_BYTES)
             and (dest is None or (not dest.is_cuda and dest.dtype == torch.complex128
@@ -256,7 +265,8 @@ def refine_type4(plan: InversePlan, spectrum, passes: int | None = None, flops: 
     """type4 plus residual-correction passes (inverse.py:165-185, Section V)."""
     if passes is None:
         passes = plan.params.refine_passes
-    out = _solve("type4", plan, spectrum, "spectrum", passes, out, non_blocking)
+    # a negative count runs no pass, like the reference's range(passes) (inverse.py:150)
+    out = _solve("type4", plan, spectrum, "spectrum", max(int(passes), 0), out, non_blocking)
     P, taps = plan.size, plan.kernel_base.taps
     _charge_type4(flops, P, taps)
     for _ in range(passes):
@@ -272,7 +282,8 @@ def refine_type5(plan: InversePlan, samples, passes: int | None = None, flops: F
     """type5 plus residual-correction passes in the sample domain (inverse.py:188-202)."""
     if passes is None:
         passes = plan.params.refine_passes
-    out = _solve("type5", plan, samples, "samples", passes, out, non_blocking)
+    # a negative count runs no pass, like the reference's range(passes) (inverse.py:150)
+    out = _solve("type5", plan, samples, "samples", max(int(passes), 0), out, non_blocking)
     P, taps = plan.size, plan.kernel_base.taps
     _charge_type5(flops, P, taps)
     for _ in range(passes):

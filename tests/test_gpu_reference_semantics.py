@@ -366,6 +366,9 @@ def test_refinement_semantics():
     assert np.array_equal(nf.refine_type5(plan, s, passes=0), nf.type5(plan, s))
     assert np.array_equal(nf.refine_type4(plan, A), nf.refine_type4(plan, A, passes=1))
     assert np.array_equal(nf.refine_type5(plan, s), nf.refine_type5(plan, s, passes=1))
+    # a negative count runs no pass (the reference loops over range(passes))
+    assert np.array_equal(nf.refine_type4(plan, A, passes=-3), nf.type4(plan, A))
+    assert np.array_equal(nf.refine_type5(plan, s, passes=-1), nf.type5(plan, s))
 
 
 def test_refine_contracts_error():
