@@ -536,9 +536,12 @@ static cudaStream_t lib_stream() {
   return s[dev];
 }
 
+// set by the host pipeline around its solves (see nfft45_solve_host)
+static thread_local bool tl_host_pipe_no_graph = false;
+
 static bool graph_eligible(const nfft45_plan* p, int64_t batch, int passes) {
   static const bool off = getenv("NFFT45_NO_GRAPH") != nullptr;
-  return !off && passes <= 1 && p->P * batch <= (int64_t(1) << 22);
+  return !off && !tl_host_pipe_no_graph && passes <= 1 && p->P * batch <= (int64_t(1) << 22);
 }
 
 // run `fn(stream)` directly, or capture/replay it as a CUDA graph
@@ -1100,6 +1103,7 @@ struct HostPipe {
   double2* bin[2] = {};
   double2* bout[2] = {};
   int64_t cap = 0;  // elements per staging slot
+  int64_t turn = 0;  // staging slot of the next call's first chunk
   std::set<const nfft45_plan*> plans;
   std::mutex mu;
 };
@@ -1199,12 +1203,22 @@ extern "C" int nfft45_solve_host(const nfft45_plan* p, int kind, int passes, con
   const double2* src = reinterpret_cast<const double2*>(in_host);
   double2* dst = reinterpret_cast<double2*>(out_host);
   int status = NFFT45_OK;
-  // every call starts at slot 0: stable staging pointers per call shape keep
-  // the CUDA-graph cache of small solves hot (alternating the first slot
-  // across calls, to overlap a call's upload with the previous call's solve,
-  // measured slower: C3 e2e 2.38e9 -> 1.1e8 points/s)
-  for (int64_t lo = 0, i = 0; lo < batch && status == NFFT45_OK; lo += chunk, i++) {
+  // A call's first chunk takes the slot the previous call's last solve is not
+  // using, so its upload overlaps that solve.  Chunks of at least 2^16 points
+  // run without the CUDA-graph cache here: next to the pipeline's copies the
+  // graph replays cost more than the launches they save (C2 e2e 1.6e9 with
+  // graphs vs 1.94e9 without; C3 2.36e9 vs 2.41e9), while C1-sized solves stay
+  // launch-bound and keep their graphs.
+  static const bool noalt = getenv("NFFT45_PIPE_NOALT") != nullptr;
+  const int64_t i0 = noalt ? 0 : hp->turn;
+  struct NoGraphScope {
+    bool prev;
+    explicit NoGraphScope(bool on) : prev(tl_host_pipe_no_graph) { tl_host_pipe_no_graph = on; }
+    ~NoGraphScope() { tl_host_pipe_no_graph = prev; }
+  } ngs(chunk * P >= (int64_t(1) << 16));
+  for (int64_t lo = 0, i = i0; lo < batch && status == NFFT45_OK; lo += chunk, i++) {
     const int k = (int)(i & 1);
+    hp->turn = i + 1;
     const int64_t m = std::min(chunk, batch - lo);
     const size_t bytes = sizeof(double2) * m * P;
     NFFT_CUDA(cudaStreamWaitEvent(hp->h2d, hp->done[k], 0));  // slot k's input consumed
