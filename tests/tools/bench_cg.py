@@ -1,7 +1,7 @@
 """CG baseline throughput: GPU CGNR vs the fast inverse
 (refine_type4) and the CPU oracle CGNR on the same type-4 systems."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 import paper_1604_06236_b200 as nf

@@ -1,6 +1,6 @@
 """Probe: which solves are bitwise equal between batched (batch-minor) and single-signal runs."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_1604_06236_b200 as nf
 from oracle import nfft_oracle as O

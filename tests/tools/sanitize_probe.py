@@ -4,7 +4,7 @@ plans (eta 2, 3, 1.5), refined solves single / batched (signal-major and
 batch-minor chains), forward NFFTs, generic sizes, clustered nodes."""
 import os, sys
 import numpy as np
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_1604_06236_b200 as nf
 from oracle import nfft_oracle as O
 
