@@ -68,3 +68,20 @@ def test_sources_never_name_forbidden_batch_copy_apis():
         for f in files:
             if f.endswith((".cu", ".cuh", ".py", ".h", ".cpp")):
                 assert not forbidden.search(open(os.path.join(root, f)).read()), f
+
+
+def test_host_solve_rejects_invalid_arguments_without_touching_the_device(lib):
+    """nfft45_solve_host validates its arguments before any CUDA call: a null plan,
+    a bad kind, an empty batch or a refine count below -1 are INVALID_ARGUMENT (9)."""
+    import numpy as np
+
+    from paper_1604_06236_b200 import _lib
+
+    L = _lib.load()
+    x = np.zeros(8, dtype=np.complex128)
+    y = np.empty_like(x)
+    for plan, kind, passes, batch in ((None, 5, 1, 1), (None, 4, -1, 1), (None, 3, 1, 1), (None, 5, 1, 0),
+                                      (None, 5, -2, 1)):
+        rc = L.nfft45_solve_host(plan, kind, passes, x.ctypes.data, batch, y.ctypes.data, 64, 1, None)
+        assert rc == 9
+        assert b"invalid host solve" in L.nfft45_last_error()
