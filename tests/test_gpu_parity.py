@@ -155,6 +155,37 @@ def test_c4_shape_65536_batched():
     _check_config(1 << 16, 0.3, 40, 16044, rows=(0, 39))
 
 
+def test_c4_full_size_1024x65536_properties():
+    """BASELINE config 4 at its full size (1024 signals x 2^16, device-resident, the bench
+    workload): every signal's forward residual (device forward NFFTs) <= 1e-10, the
+    first and last signals vs the CPU oracle <= 1e-10, and linearity of the refined
+    solves on a pair of signals (size-independent properties of the path)."""
+    P, B = 1 << 16, 1024
+    t, _ = O.make_inputs(P, 0.3, 1, 16044)
+    grid = nf.validate_grid(t)
+    prm = nf.MethodParams.from_mu(1e-15, P, 2)
+    plan = nf.build_plan(grid, prm)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(16044)
+    mk = lambda: torch.complex(torch.randn(B, P, generator=g, device="cuda", dtype=torch.float64),
+                               torch.randn(B, P, generator=g, device="cuda", dtype=torch.float64))
+    s, A = mk(), mk()
+    x5 = nf.refine_type5(plan, s, passes=1)
+    x4 = nf.refine_type4(plan, A, passes=1)
+    res5 = torch.linalg.norm(nf.nfft_type2(x5, grid) - s, dim=1) / torch.linalg.norm(s, dim=1)
+    res4 = torch.linalg.norm(nf.nfft_type1(grid, x4, P) - A, dim=1) / torch.linalg.norm(A, dim=1)
+    assert float(res5.max()) <= G1 and float(res4.max()) <= G1, (float(res5.max()), float(res4.max()))
+    oplan = O.Plan.build(t, prm.damping_a, 2)
+    for r in (0, B - 1):
+        assert rel(O.refine5(oplan, s[r].cpu().numpy(), 1), x5[r].cpu().numpy()) <= G1
+        assert rel(O.refine4(oplan, A[r].cpu().numpy(), 1), x4[r].cpu().numpy()) <= G1
+    a, b = 0.75 - 0.5j, -1.25 + 0.25j
+    mix = (a * s[3] + b * s[7]).unsqueeze(0)
+    got = nf.refine_type5(plan, mix, passes=1)[0]
+    want = a * x5[3] + b * x5[7]
+    assert float(torch.linalg.norm(got - want) / torch.linalg.norm(want)) <= 1e-12
+
+
 def test_c3_single_2_20():
     _check_config(1 << 20, 0.4, 1, 16043, passes=(1,))
 
