@@ -1,6 +1,7 @@
 // nfft45.cu — C ABI (include/nfft45.h): node sets, forward NFFTs, Lagrange
 // quantities, inverse plans and the type-4/5 solves with refinement.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -957,6 +958,12 @@ int nfft45_plan_create_terms(const nfft45_grid* g, double a, int64_t R, int m, v
   DeviceGuard dg(g->d.device);
   if (dg.status) return dg.status;
   cudaStream_t s = S(st);
+  static const bool timing = getenv("NFFT45_PLAN_TIMING") != nullptr;  // host-side breakdown (probe)
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
+  const auto T0 = now();
   nfft45_plan* p = new nfft45_plan();
   p->gc = new GraphCache();
   p->g = g;
@@ -964,7 +971,11 @@ int nfft45_plan_create_terms(const nfft45_grid* g, double a, int64_t R, int m, v
   p->a = a;
   p->eta = eta;
   p->m = m;
-  cudaError_t e = cudaMalloc(&p->tables, sizeof(double2) * 9 * P + sizeof(double) * 5 * P);
+  // stream-ordered pool allocation (release threshold infinite, DeviceGuard):
+  // a rebuilt plan reuses pooled memory instead of a fresh cudaMalloc (1-20 ms
+  // for the 184 MB of tables at P = 2^20); the build ends with a stream
+  // synchronize (check_guards), after which every stream may use the tables
+  cudaError_t e = cudaMallocAsync(&p->tables, sizeof(double2) * 9 * P + sizeof(double) * 5 * P, s);
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "cudaMalloc(plan)");
@@ -986,6 +997,7 @@ int nfft45_plan_create_terms(const nfft45_grid* g, double a, int64_t R, int m, v
   p->c5 = t + 7 * P;
   p->c4 = t + 8 * P;
   int status = NFFT45_OK;
+  const auto T1 = now();
   {
     Scratch guard(s);
     status = guard.alloc(sizeof(double) * 2);
@@ -1008,14 +1020,19 @@ int nfft45_plan_create_terms(const nfft45_grid* g, double a, int64_t R, int m, v
     }
     if (!status) status = check_guards(guard.d(), 1, 1, s);
   }
+  const auto T2 = now();
   if (!status && m == kFastM) {  // per-tile node ranges of the solve grid n = 2P (spread kernels)
     status = tile_ranges_cache(g->d, 2 * P, m, 64, s);
     if (!status) status = tile_ranges_cache(g->d, 2 * P, m, 256, s);
     if (!status) status = gather_flags_cache(g->d, 2 * P, s);
   }
+  if (timing)
+    fprintf(stderr, "plan P=%lld: alloc %.3f ms, tables+guards %.3f ms, caches %.3f ms\n", (long long)P, ms(T0, T1),
+            ms(T1, T2), ms(T2, now()));
   if (status) {
     cudaStreamSynchronize(s);
-    cudaFree(p->tables);
+    cudaFreeAsync(p->tables, s);
+    cudaStreamSynchronize(s);
     delete p->gc;
     delete p;
     return status;
@@ -1028,11 +1045,14 @@ void nfft45_plan_destroy(nfft45_plan* p) {
   if (!p) return;
   DeviceGuard dg(p->g->d.device);
   nfft45::host_pipes_forget(p);
+  // solves on any stream may still read the tables (cudaFree used to imply this
+  // device-wide wait); the memory then returns to the stream-ordered pool
+  cudaDeviceSynchronize();
   if (p->gc) {
     for (auto& kv : p->gc->execs) cudaGraphExecDestroy(kv.second);
     delete p->gc;
   }
-  cudaFree(p->tables);
+  cudaFreeAsync(p->tables, 0);
   delete p;
 }
 
