@@ -1069,6 +1069,8 @@ int nfft45_type5(const nfft45_plan* p, const double* s, int64_t batch, double* o
   if (!p) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid plan");
   DeviceGuard dg(p->g->d.device);
   if (dg.status) return dg.status;
+  if (tiny_eligible(p->P, p->m, 0, batch))
+    return tiny_solve(p->g->d, p->P, p->c5, p->c4, p->decay, p->ks, p->coef, 5, C2(s), batch, 0, D2(out), S(st));
   return run_graphed(p, 5, batch, -1, s, out, S(st),
                      [&](cudaStream_t ss) { return type5_core(p, C2(s), batch, D2(out), ss); });
 }
@@ -1077,6 +1079,8 @@ int nfft45_type4(const nfft45_plan* p, const double* A, int64_t batch, double* o
   if (!p) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid plan");
   DeviceGuard dg(p->g->d.device);
   if (dg.status) return dg.status;
+  if (tiny_eligible(p->P, p->m, 0, batch))
+    return tiny_solve(p->g->d, p->P, p->c5, p->c4, p->decay, p->ks, p->coef, 4, C2(A), batch, 0, D2(out), S(st));
   return run_graphed(p, 4, batch, -1, A, out, S(st),
                      [&](cudaStream_t ss) { return type4_core(p, C2(A), batch, D2(out), ss); });
 }
@@ -1085,6 +1089,9 @@ int nfft45_refine_type5(const nfft45_plan* p, const double* s, int64_t batch, in
   if (!p || passes < 0) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid refine arguments");
   DeviceGuard dg(p->g->d.device);
   if (dg.status) return dg.status;
+  if (tiny_eligible(p->P, p->m, passes, batch))
+    return tiny_solve(p->g->d, p->P, p->c5, p->c4, p->decay, p->ks, p->coef, 5, C2(s), batch, passes, D2(out),
+                      S(st));
   return run_graphed(p, 15, batch, passes, s, out, S(st),
                      [&](cudaStream_t ss) { return refine_core(p, C2(s), batch, passes, D2(out), true, ss); });
 }
@@ -1093,6 +1100,9 @@ int nfft45_refine_type4(const nfft45_plan* p, const double* A, int64_t batch, in
   if (!p || passes < 0) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid refine arguments");
   DeviceGuard dg(p->g->d.device);
   if (dg.status) return dg.status;
+  if (tiny_eligible(p->P, p->m, passes, batch))
+    return tiny_solve(p->g->d, p->P, p->c5, p->c4, p->decay, p->ks, p->coef, 4, C2(A), batch, passes, D2(out),
+                      S(st));
   return run_graphed(p, 14, batch, passes, A, out, S(st),
                      [&](cudaStream_t ss) { return refine_core(p, C2(A), batch, passes, D2(out), false, ss); });
 }

@@ -135,6 +135,13 @@ int norms_bm(const double2* r, int64_t len, int64_t batch, int64_t ld, double* n
 int chain_run_bm(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes, double2* out,
                  double* norms, cudaStream_t st);
 
+// Whole small solves in one CTA per signal (tiny.cu): P a power of two in
+// [32, 256], m = 14, passes <= 1, P * batch <= 2^17.
+bool tiny_eligible(int64_t P, int m, int passes, int64_t batch);
+int tiny_solve(const GridDev& g, int64_t P, double2 const* c5, double2 const* c4, const double2* decay,
+               const double2* ks, const double2* coef, int kind, const double2* in, int64_t batch, int passes,
+               double2* out, cudaStream_t st);
+
 // Device deconvolution weight 1/(n Psi(nu)) of gridding.py:90.
 __device__ __forceinline__ double deconv_weight(int64_t p, int64_t K, int64_t n, double b) {
   double nu = (double)(p - K);
