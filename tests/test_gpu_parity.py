@@ -452,6 +452,37 @@ np.savez(sys.argv[1], t5=nf.type5(plan, x), t4=nf.type4(plan, x), r4=nf.refine_t
 """
 
 
+@pytest.mark.parametrize("P", [32, 64, 128, 256])
+def test_one_cta_small_solves(P):
+    """P <= 256 solves run as ONE fused kernel per call (tiny.cu): one launch per
+    solve, refined results vs the oracle <= 1e-10 with forward residuals, batched ==
+    per-signal and passes=0 == plain bitwise, and the wrap case (a node whose rounded
+    centre is n) handled; above P * batch = 2^17 the general path takes over and
+    agrees to rounding."""
+    from paper_1604_06236_b200 import _lib
+
+    t, data = O.make_inputs(P, 0.45, 3, 900 + P)
+    t[np.argmax(t)] = 1.0 - 0.25 / (2 * P)  # rint(2P t) == 2P: centre on the wrap
+    grid = nf.validate_grid(t)
+    prm = nf.MethodParams.from_mu(1e-15, P, 2)
+    plan = nf.build_plan(grid, prm)
+    oplan = O.Plan.build(t, prm.damping_a, 2)
+    L = _lib.load()
+    before = L.nfft45_launch_count()
+    got5 = nf.refine_type5(plan, data[1], passes=1)
+    assert L.nfft45_launch_count() - before == 1
+    got4 = nf.refine_type4(plan, data[1], passes=1)
+    assert rel(O.refine5(oplan, data[1], 1), got5) <= G1 and rel(O.refine4(oplan, data[1], 1), got4) <= G1
+    assert rel(data[1], O.type2(got5, t)) <= G1 and rel(data[1], O.type1(t, got4, P)) <= G1
+    assert np.array_equal(nf.refine_type5(plan, data, passes=1)[1], got5)
+    assert np.array_equal(nf.refine_type4(plan, data, passes=1)[1], got4)
+    assert np.array_equal(nf.refine_type5(plan, data[0], passes=0), nf.type5(plan, data[0]))
+    assert np.array_equal(nf.refine_type4(plan, data[0], passes=0), nf.type4(plan, data[0]))
+    big = np.repeat(data[1:2], (1 << 17) // P + 1, axis=0)  # past the one-CTA threshold
+    assert rel(got5, nf.refine_type5(plan, big, passes=1)[-1]) < 1e-12
+    assert rel(got4, nf.refine_type4(plan, big, passes=1)[-1]) < 1e-12
+
+
 def test_persistent_gather_fallback_blocks_bitwise(tmp_path):
     """A grid with a locally stretched stretch of nodes (64 nodes at 1.7x
     spacing) puts some 32-node blocks past the persistent gather's staging
