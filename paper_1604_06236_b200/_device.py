@@ -34,7 +34,14 @@ def device_index(device=None) -> int:
     return int(device)
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle(dev: int) -> int:
+    """cudaStream_t of the caller's current stream on `dev` (the raw accessor skips
+    building a torch.cuda.Stream object: ~4 us of the ~15 us host cost of a small solve)."""
+    if _raw_stream is not None:
+        return _raw_stream(dev)
     return torch.cuda.current_stream(dev).cuda_stream
 
 

@@ -125,7 +125,9 @@ def check(status: int):
 
 
 def call(name: str, *args):
-    check(getattr(load(), name)(*args))
+    status = getattr(_lib or load(), name)(*args)
+    if status:
+        check(status)
 
 
 def profile_enable(on: bool):

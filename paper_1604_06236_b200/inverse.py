@@ -230,7 +230,7 @@ def _solve(name: str, plan: InversePlan, data, label: str, passes: int | None, d
                                non_blocking and dest is not None and dest.is_pinned())
     a = _device.operand(data, plan.device, length=plan.size, name=label)
     if dest is not None and dest.is_cuda and dest.dtype == _device.torch.complex128 and dest.is_contiguous():
-        out = dest.reshape(a.tensor.shape)
+        out = dest if dest.shape == a.tensor.shape else dest.reshape(a.tensor.shape)
         dest = None
     else:
         out = a.empty_like_rows(plan.size)
