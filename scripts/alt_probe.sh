@@ -6,7 +6,7 @@ for v in "X=1" "NFFT45_PIPE_ALT=1" "NFFT45_NO_GRAPH=1" "NFFT45_PIPE_ALT=1 NFFT45
 import json, sys
 c = sys.argv[1]
 d = json.loads(open(f"gpurun_out/alt_{c}.log").read().strip().splitlines()[-1])
-print(sys.argv[2], c, f"{d['ms_per_step']:.4f} ms/step", f"e2e {d['e2e']['value']:.3g}", d["e2e"].get("warmup_ms"))
+print(sys.argv[2], c, f"{d['ms_per_step']:.4f} ms/step", f"e2e {d['e2e']['value']:.3g}", d["e2e"].get("warmup_steps"))
 PY
  done
 done

@@ -10,6 +10,6 @@ c = sys.argv[1]
 d = json.loads(open(f"gpurun_out/bench_{c}.log").read().strip().splitlines()[-1])
 rf = d.get("roofline") or {}
 print(c, f"{d['ms_per_step']:.4f} ms/step", f"value {d['value']:.3g}", f"e2e {d['e2e']['value']:.3g}",
-      rf.get("kernel"), rf.get("frac"), d["e2e"].get("warmup_ms"))
+      rf.get("kernel"), rf.get("frac"), d["e2e"].get("warmup_steps"))
 PY
 done

@@ -7,7 +7,7 @@ for v in "NFFT45_PIPE_MIN_BYTES=0" "NFFT45_PIPE_MIN_BYTES=100000000000"; do
 import json, sys
 c = sys.argv[1]
 d = json.loads(open(f"gpurun_out/pab_{c}.log").read().strip().splitlines()[-1])
-print(sys.argv[2], c, f"{d['ms_per_step']:.4f} ms/step", f"value {d['value']:.3g}", f"e2e {d['e2e']['value']:.3g}", d["e2e"].get("warmup_ms"))
+print(sys.argv[2], c, f"{d['ms_per_step']:.4f} ms/step", f"value {d['value']:.3g}", f"e2e {d['e2e']['value']:.3g}", d["e2e"].get("warmup_steps"))
 PY
  done
 done
