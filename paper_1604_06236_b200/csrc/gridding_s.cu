@@ -71,7 +71,7 @@ __device__ __forceinline__ int64_t floordiv_s(int64_t a, int64_t b) {
 
 // amp == nullptr: unit amplitudes (the plan's log-sum NFFT, lagrange.py:57-75).
 template <int SB>
-__global__ void __launch_bounds__(kSTile) k_spread_s(const double* __restrict__ ts, const int* __restrict__ perm,
+__global__ void __launch_bounds__(kSTile, SB == 1 ? 5 : 2) k_spread_s(const double* __restrict__ ts, const int* __restrict__ perm,
                                                      int64_t Q, int64_t n, double alpha, GaussTab G,
                                                      const double2* __restrict__ amp, int64_t batch, NodeFactor nf,
                                                      double2* __restrict__ H, const int2* __restrict__ ranges,
@@ -111,19 +111,24 @@ __global__ void __launch_bounds__(kSTile) k_spread_s(const double* __restrict__ 
       for (int e = tid; e < cnt; e += kSTile) {
         const int64_t q = base + e;
         const double t = ts[q];
+        const int pq = perm[q];
+        // the amplitudes (a dependent global load through perm) are requested
+        // before the weights are computed, so their latency hides under it
+        double2 av[SB];
+#pragma unroll
+        for (int s = 0; s < SB; s++)
+          av[s] = (amp && b0 + s < batch) ? amp[(b0 + s) * Q + pq] : make_double2(0.0, 0.0);
+        const double2 fq = factor_s(nf, q, t);
         const NodeGeo geo = node_geo(t, (double)n);
         Cc[e] = (int)((int64_t)geo.i0 - shift);
         double w[kTaps];
         taps29s(geo.f, alpha, G, w);
 #pragma unroll
         for (int k = 0; k < kTaps; k++) W[e * kTaps + k] = w[k];
-        const double2 fq = factor_s(nf, q, t);
-        const int pq = perm[q];
 #pragma unroll
         for (int s = 0; s < SB; s++) {
-          const int64_t b = b0 + s;
           double2 a = make_double2(0.0, 0.0);
-          if (b < batch) a = amp ? cmul(amp[b * Q + pq], fq) : fq;
+          if (b0 + s < batch) a = amp ? cmul(av[s], fq) : fq;
           A[s * kSCap + e] = a;
         }
       }
@@ -139,6 +144,7 @@ __global__ void __launch_bounds__(kSTile) k_spread_s(const double* __restrict__ 
       __syncthreads();
       // phase 2: this thread's cell j0 + tid, contributing nodes in ascending order
       const int lo = Fx[tid], hi = Fx[tid + 2 * kM + 1];  // centres in [tid - kM, tid + kM]
+#pragma unroll 4
       for (int e = lo; e < hi; e++) {
         const double wk = W[e * kTaps + (tid - Cc[e] + kM)];
 #pragma unroll
