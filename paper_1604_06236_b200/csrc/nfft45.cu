@@ -542,7 +542,8 @@ static thread_local bool tl_host_pipe_no_graph = false;
 
 static bool graph_eligible(const nfft45_plan* p, int64_t batch, int passes) {
   static const bool off = getenv("NFFT45_NO_GRAPH") != nullptr;
-  return !off && !tl_host_pipe_no_graph && passes <= 1 && p->P * batch <= (int64_t(1) << 22);
+  // per-kernel profiling needs the individual launches (graph replays bypass LAUNCH)
+  return !off && !tl_host_pipe_no_graph && !g_profiling.load(std::memory_order_relaxed) && passes <= 1 && p->P * batch <= (int64_t(1) << 22);
 }
 
 // run `fn(stream)` directly, or capture/replay it as a CUDA graph
