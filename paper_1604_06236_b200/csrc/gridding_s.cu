@@ -195,10 +195,21 @@ __global__ void __launch_bounds__(kGNodes, SB == 1 ? 3 : 2) k_gather_s(const dou
     for (int s = 0; s < SB; s++) {
       const int64_t b = min(b0 + s, batch - 1);
       const double2* row = H + b * n;
-      for (int c = tid; c < len; c += kGNodes) {
+      // all of this thread's cells are requested before the first is stored
+      // (one global round trip instead of one per staged cell)
+      constexpr int kPer = kGCap / kGNodes;
+      double2 v[kPer];
+#pragma unroll
+      for (int i = 0; i < kPer; i++) {
+        const int c = tid + i * kGNodes;
         int cell = cs + c;
         cell = cell < 0 ? cell + ni : (cell >= ni ? cell - ni : cell);
-        Y[s * kRow + gslot(c)] = row[cell];
+        if (c < len) v[i] = row[cell];
+      }
+#pragma unroll
+      for (int i = 0; i < kPer; i++) {
+        const int c = tid + i * kGNodes;
+        if (c < len) Y[s * kRow + gslot(c)] = v[i];
       }
     }
   }
