@@ -71,6 +71,9 @@ ALGO_BYTES_PER_POINT_STEP = {
     "bm_pad": 3 * 48,
     "bm_row": 3 * 32,            # 3 x IFFT_2P row pass
     "bm_rowout": 16,             # 1 x FFT_P row pass (type-5 output, batch-minor -> signal-major)
+    # one-CTA fused small solves (P <= 256): a whole refined solve per launch, so only the
+    # operand read and the result write reach HBM (2 launches per step: type-5, type-4)
+    "tiny": 2 * 32,
 }
 
 

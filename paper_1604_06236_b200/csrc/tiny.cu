@@ -276,9 +276,9 @@ int tiny_solve(const GridDev& g, int64_t P, double2 const* c5, double2 const* c4
   Window win = Window::make(kTM);
   TinyArgs a{g.ts, g.perm, c5, c4, decay, ks, coef, (int)P, win.alpha, win.b, gauss_tab(win)};
   const size_t smem = sizeof(double2) * (2 * 2 * P + 4 * P) + sizeof(double) * P * (kTTaps + 1) + sizeof(int) * P;
-  auto k = k_tiny_solve;
-  if (smem > 48 * 1024) NFFT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  LAUNCH(k, (unsigned)batch, kTThreads, smem, st, a, kind, passes < 0 ? 0 : passes, in, out);
+  auto tiny = k_tiny_solve;  // the launched name keys the per-kernel profile
+  if (smem > 48 * 1024) NFFT_CUDA(cudaFuncSetAttribute(tiny, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  LAUNCH(tiny, (unsigned)batch, kTThreads, smem, st, a, kind, passes < 0 ? 0 : passes, in, out);
   return NFFT45_OK;
 }
 
