@@ -170,6 +170,65 @@ __global__ void __launch_bounds__(kSTile, (SB == 1 ? 5 : 2) * 256 / kSTile) k_sp
   }
 }
 
+// Warp-tiled variant for one signal: every warp is an independent 32-cell
+// tile with its own cached node range (tile ranges at TC = 32), no CTA
+// barriers.  Per chunk of <= 32 contributing nodes (all periodic images in
+// increasing order, nodes ascending), lane l stages node l's centre, 29
+// weights and amplitude x factor; then every lane (= cell) walks the chunk's
+// nodes in ascending order -- a warp-uniform loop, so the centre and the
+// amplitude are broadcast reads and the weights of one node sit in
+// consecutive words across the lanes -- and accumulates the nodes whose
+// window covers its cell.  Same terms, same order, same fma sequence as the
+// other spreading kernels: bitwise identical results.
+constexpr int kWWarps = 4;
+__global__ void __launch_bounds__(kWWarps * 32, 7) k_spread_w(const double* __restrict__ ts, const int* __restrict__ perm,
+                                                              int64_t Q, int64_t n, double alpha, GaussTab G,
+                                                              const double2* __restrict__ amp, NodeFactor nf,
+                                                              double2* __restrict__ H, const int2* __restrict__ ranges,
+                                                              int NS) {
+  __shared__ __align__(16) double Wsh[kWWarps][32 * kTaps];
+  __shared__ __align__(16) double2 Ash[kWWarps][32];
+  __shared__ int Csh[kWWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t tile = (int64_t)blockIdx.x * kWWarps + w;
+  const int64_t j0 = tile * 32;
+  if (j0 >= n) return;
+  double* W = Wsh[w];
+  double2* A = Ash[w];
+  int* C = Csh[w];
+  const int64_t x_lo = -kM - (min(j0 + 32, n) - 1) + n - 1;
+  const int64_t s_lo = n > kM ? (x_lo < 0 ? -1 : 0) : floordiv_s(x_lo, n);
+  double2 acc = make_double2(0.0, 0.0);
+  for (int si = 0; si < NS; si++) {
+    const int2 r = ranges[tile * NS + si];
+    const int64_t shift = (s_lo + si) * n + j0;
+    for (int base = r.x; base < r.y; base += 32) {
+      const int cnt = min(32, r.y - base);
+      if (lane < cnt) {
+        const int64_t q = base + lane;
+        const double t = ts[q];
+        const int pq = perm[q];
+        const double2 av = amp ? amp[pq] : make_double2(0.0, 0.0);
+        const double2 fq = factor_s(nf, q, t);
+        const NodeGeo geo = node_geo(t, (double)n);
+        C[lane] = (int)((int64_t)geo.i0 - shift);
+        double wt[kTaps];
+        taps29s(geo.f, alpha, G, wt);
+#pragma unroll
+        for (int k = 0; k < kTaps; k++) W[lane * kTaps + k] = wt[k];
+        A[lane] = amp ? cmul(av, fq) : fq;
+      }
+      __syncwarp();
+      for (int e = 0; e < cnt; e++) {
+        const int d = lane - C[e] + kM;
+        if (d >= 0 && d < kTaps) caxpy(acc, W[e * kTaps + d], A[e]);
+      }
+      __syncwarp();
+    }
+  }
+  if (j0 + lane < n) H[j0 + lane] = acc;
+}
+
 // mode 0: out = v;  1: out = v - sub;  2: out = sub - v  (v = factor * window sum)
 template <int SB>
 __global__ void __launch_bounds__(kGNodes, SB == 1 ? 3 : 2) k_gather_s(const double* __restrict__ ts, const int* __restrict__ perm,
@@ -267,6 +326,22 @@ int spread_small(const GridDev& g, int64_t n, const Window& win, const double2* 
   // 128-cell tiles (default): ~80 nodes per CTA, 10 CTAs/SM, barrier groups of 4 warps;
   // single transforms 0.3-2 % faster than 256-cell tiles, bitwise identical (scripts/ab_env.sh)
   const int tile = env_tile == 256 ? 256 : 128;
+  // single signals on grids up to 2^17 cells: warp tiles (P = 2^14 .. 2^16 single
+  // transforms 1.5-3.5 % faster; at 2^19 .. 2^21 cells 1-3 % slower: every node's
+  // weights are computed by ~2 warps).  NFFT45_SPREAD_WARP=0 / 1 forces off / on.
+  static const int warp_env = getenv("NFFT45_SPREAD_WARP") ? atoi(getenv("NFFT45_SPREAD_WARP")) : -1;
+  const bool warp_tiles = warp_env < 0 ? n <= (int64_t(1) << 17) : warp_env > 0;
+  if (warp_tiles && batch == 1 && win.m == kM && tile_images(n, win.m, 32) <= 8) {
+    const int NSw = tile_images(n, win.m, 32);
+    const int2* rw = nullptr;
+    int2* ownw = nullptr;
+    NFFT_CHECK(tile_ranges(g, n, win.m, 32, NSw, st, &rw, &ownw));
+    const GaussTab Gw = gauss_tab(win);
+    LAUNCH(k_spread_w, (unsigned)ceil_div(ceil_div(n, 32), kWWarps), kWWarps * 32, 0, st, g.ts, g.perm, g.Q, n,
+           win.alpha, Gw, amp, f, H, rw, NSw);
+    if (ownw) NFFT_CUDA(cudaFreeAsync(ownw, st));
+    return NFFT45_OK;
+  }
   const int64_t ntiles = ceil_div(n, tile);
   const int NS = tile_images(n, win.m, tile);
   if (NS > 8 || win.m != kM) return NFFT45_ERR_INVALID_ARGUMENT;
