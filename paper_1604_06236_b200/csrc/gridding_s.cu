@@ -40,8 +40,7 @@ template <int TILE> struct STile {
     return sizeof(double) * cap * kTaps + sizeof(double2) * sb * cap + sizeof(int) * (cap + xs);
   }
 };
-constexpr int kGNodes = 256;       // gather: nodes per CTA (= threads)
-constexpr int kGCap = 1024;        // gather: staged cells per CTA (and signal)
+// gather: kGNodes nodes per CTA (= threads), 4 x kGNodes staged cells per CTA (and signal)
 
 __device__ __forceinline__ int gslot(int c) { return c + (c >> 3); }  // skewed staging slot
 
@@ -230,13 +229,14 @@ __global__ void __launch_bounds__(kWWarps * 32, 7) k_spread_w(const double* __re
 }
 
 // mode 0: out = v;  1: out = v - sub;  2: out = sub - v  (v = factor * window sum)
-template <int SB>
-__global__ void __launch_bounds__(kGNodes, SB == 1 ? 3 : 2) k_gather_s(const double* __restrict__ ts, const int* __restrict__ perm,
+template <int SB, int kGNodes>
+__global__ void __launch_bounds__(kGNodes, (SB == 1 ? 3 : 2) * 256 / kGNodes) k_gather_s(const double* __restrict__ ts, const int* __restrict__ perm,
                                                       int64_t Q, int64_t n, double alpha, GaussTab G,
                                                       const double2* __restrict__ H, int64_t batch, NodeFactor nf,
                                                       const double2* __restrict__ sub, int mode,
                                                       double2* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smraw[];
+  constexpr int kGCap = 4 * kGNodes;
   double2* Y = reinterpret_cast<double2*>(smraw);  // [SB][gslot(kGCap)]
   constexpr int kRow = kGCap + kGCap / 8;
 
@@ -375,17 +375,26 @@ int gather_small(const GridDev& g, int64_t n, const Window& win, const double2* 
   if (!sub) mode = 0;
   const GaussTab G = gauss_tab(win);
   const int sb = batch >= 4 ? 4 : 1;
-  const size_t smem = sizeof(double2) * sb * (kGCap + kGCap / 8);
-  const dim3 grid((unsigned)ceil_div(g.Q, kGNodes), (unsigned)ceil_div(batch, sb));
-  if (sb == 4) {
-    auto gather_s4 = k_gather_s<4>;
-    NFFT_CUDA(cudaFuncSetAttribute(gather_s4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    LAUNCH(gather_s4, grid, kGNodes, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, batch, f, sub, mode, out);
-  } else {
-    auto gather_s1 = k_gather_s<1>;
-    NFFT_CUDA(cudaFuncSetAttribute(gather_s1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    LAUNCH(gather_s1, grid, kGNodes, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, batch, f, sub, mode, out);
+  static const int env_nodes = getenv("NFFT45_GNODES") ? atoi(getenv("NFFT45_GNODES")) : 0;  // A/B switch
+  // 128-node CTAs (default): 6 CTAs/SM; single transforms up to 1.5 % faster than
+  // 256-node CTAs at P >= 2^18, equal below, bitwise identical (scripts/ab_env.sh)
+  const int nodes = env_nodes == 256 ? 256 : (env_nodes == 64 ? 64 : 128);
+  const size_t smem = sizeof(double2) * sb * (4 * nodes + 4 * nodes / 8);
+  const dim3 grid((unsigned)ceil_div(g.Q, nodes), (unsigned)ceil_div(batch, sb));
+#define NFFT45_GATHER_S(name, SBv, NODESv)                                                                 \
+  {                                                                                                       \
+    auto name = k_gather_s<SBv, NODESv>;                                                                  \
+    NFFT_CUDA(cudaFuncSetAttribute(name, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
+    LAUNCH(name, grid, NODESv, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, batch, f, sub, mode, out); \
   }
+  if (nodes == 128) {
+    if (sb == 4) NFFT45_GATHER_S(gather_s4, 4, 128) else NFFT45_GATHER_S(gather_s1, 1, 128)
+  } else if (nodes == 64) {
+    if (sb == 4) NFFT45_GATHER_S(gather_s4, 4, 64) else NFFT45_GATHER_S(gather_s1, 1, 64)
+  } else {
+    if (sb == 4) NFFT45_GATHER_S(gather_s4, 4, 256) else NFFT45_GATHER_S(gather_s1, 1, 256)
+  }
+#undef NFFT45_GATHER_S
   return NFFT45_OK;
 }
 
