@@ -1024,7 +1024,7 @@ int nfft45_plan_create_terms(const nfft45_grid* g, double a, int64_t R, int m, v
   const auto T2 = now();
   if (!status && m == kFastM) {  // per-tile node ranges of the solve grid n = 2P (spread kernels)
     status = tile_ranges_cache(g->d, 2 * P, m, 64, s);
-    if (!status) status = tile_ranges_cache(g->d, 2 * P, m, getenv("NFFT45_STILE") ? 256 : 128, s);
+    if (!status) status = tile_ranges_cache(g->d, 2 * P, m, getenv("NFFT45_STILE") ? atoi(getenv("NFFT45_STILE")) : 128, s);
     if (!status && 2 * P <= (int64_t(1) << 17)) status = tile_ranges_cache(g->d, 2 * P, m, 32, s);  // warp tiles
     if (!status) status = gather_flags_cache(g->d, 2 * P, s);
   }
