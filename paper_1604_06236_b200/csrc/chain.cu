@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(fast_threads<2 * PC, C>(), 2) kc_band(
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
     const double* __restrict__ deconv, const double* __restrict__ decay, const double* __restrict__ dd,
     const double2* __restrict__ sub, const double2* __restrict__ twQ, int Q) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int64_t P = (int64_t)PR * PC, n = 2 * P;
   constexpr int NR = 2 * PC;
   extern __shared__ double2 sm[];
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(fast_threads<PR, C>()) kc_mid(const double2* _
                                                                const double2* __restrict__ hiP, int sP,
                                                                const double2* __restrict__ ks,
                                                                const double2* __restrict__ twQ, int Q) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int64_t P = (int64_t)PR * PC;
   extern __shared__ double2 sm[];
   const int r0 = blockIdx.x * C;
@@ -106,6 +108,7 @@ __global__ void __launch_bounds__(fast_threads<2 * PC, C>(), 2) kc_pad(
     const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
     const double* __restrict__ coef, const double* __restrict__ deconv, const double* __restrict__ cd,
     const double2* __restrict__ xsub, double2* __restrict__ xout, const double2* __restrict__ twQ, int Q) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int64_t P = (int64_t)PR * PC, n = 2 * P;
   constexpr int NC = 2 * PC;
   extern __shared__ double2 sm[];
@@ -143,6 +146,7 @@ __global__ void __launch_bounds__(fast_threads<L, C>()) kc_row(const double2* __
                                                               const double2* __restrict__ tw,
                                                               const double* __restrict__ post,
                                                               const double2* __restrict__ xsub) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   extern __shared__ double2 sm[];
   const int r0 = blockIdx.x * C;
   const int64_t base = (int64_t)blockIdx.y * len;
@@ -166,6 +170,7 @@ __global__ void __launch_bounds__(fast_threads<L, C>()) kc_col(const double2* __
                                                               const double2* __restrict__ hi, int s,
                                                               const double* __restrict__ pre,
                                                               const double2* __restrict__ twQ, int Q) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   extern __shared__ double2 sm[];
   const int c0 = blockIdx.x * C;
   const int64_t base = (int64_t)blockIdx.y * N;
@@ -241,7 +246,7 @@ struct Chain {
     const double2* twQ = q_table(Q, st, &status);
     if (!twQ) return status;
     dim3 grid((unsigned)(L2 / CC), (unsigned)batch);
-    LAUNCH(chain_col, grid, T, smem, st, in, out, N, L2, tw, t4->lo, t4->hi, t4->s, pre, twQ, (int)Q);
+    LAUNCH_PDL(chain_col, grid, T, smem, st, in, out, N, L2, tw, t4->lo, t4->hi, t4->s, pre, twQ, (int)Q);
     return NFFT45_OK;
   }
 
@@ -256,7 +261,7 @@ struct Chain {
     const double2* twQ = q_table(Q, st, &status);
     if (!twQ) return status;
     dim3 grid((unsigned)(PR / C), (unsigned)batch);
-    LAUNCH(chain_band, grid, T, smem, st, T_, U, t.tw2C, t.twC, t.tP->lo, t.tP->hi, t.tP->s, deconv, decay, dd, sub,
+    LAUNCH_PDL(chain_band, grid, T, smem, st, T_, U, t.tw2C, t.twC, t.tP->lo, t.tP->hi, t.tP->s, deconv, decay, dd, sub,
            twQ, (int)Q);
     return NFFT45_OK;
   }
@@ -272,7 +277,7 @@ struct Chain {
     const double2* twQ = q_table(Q, st, &status);
     if (!twQ) return status;
     dim3 grid((unsigned)(PC / C), (unsigned)batch);
-    LAUNCH(chain_mid, grid, T, smem, st, U, Z, t.twR, t.tP->lo, t.tP->hi, t.tP->s, ks, twQ, (int)Q);
+    LAUNCH_PDL(chain_mid, grid, T, smem, st, U, Z, t.twR, t.tP->lo, t.tP->hi, t.tP->s, ks, twQ, (int)Q);
     return NFFT45_OK;
   }
 
@@ -287,7 +292,7 @@ struct Chain {
     const double2* twQ = q_table(Q, st, &status);
     if (!twQ) return status;
     dim3 grid((unsigned)(PR / C), (unsigned)batch);
-    LAUNCH(chain_pad, grid, T, smem, st, Z, Y, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s, coef, deconv, cd, xsub,
+    LAUNCH_PDL(chain_pad, grid, T, smem, st, Z, Y, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s, coef, deconv, cd, xsub,
            xout, twQ, (int)Q);
     return NFFT45_OK;
   }
@@ -301,7 +306,7 @@ struct Chain {
     NFFT_CHECK(chain_attr(chain_row, smem));
     constexpr int T = fast_threads<L, C>();
     dim3 grid((unsigned)(rows / C), (unsigned)batch);
-    LAUNCH(chain_row, grid, T, smem, st, in, out, len, R1, tw, post, xsub);
+    LAUNCH_PDL(chain_row, grid, T, smem, st, in, out, len, R1, tw, post, xsub);
     return NFFT45_OK;
   }
 };

@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<
     const double2* __restrict__ in, double2* __restrict__ out, int L2, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ lo, const double2* __restrict__ hi, int sh, const double2* __restrict__ twQ, int Q,
     const double* __restrict__ pre, int sw, int pf) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   extern __shared__ double2 sm[];
   const int n2 = sw ? blockIdx.y : blockIdx.x;
   const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * kSig;
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
     const double* __restrict__ dd, const double2* __restrict__ sub, int sw, int pf) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int NR = 2 * C;
   extern __shared__ double2 sm[];
   double* s_t0 = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + fast_smem<NR, SG>());
@@ -177,6 +179,7 @@ __global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<
     const double2* __restrict__ U, double2* __restrict__ Z, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
     const double2* __restrict__ ks, int sw, int pf) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   extern __shared__ double2 sm[];
   double2* s_ks = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + fast_smem<R, kSig>());
   const int r = sw ? blockIdx.y : blockIdx.x;
@@ -207,6 +210,7 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
     const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
     const double* __restrict__ cd, const double2* __restrict__ xsub, double2* __restrict__ xout, int sw, int pf) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int NC = 2 * C;
   constexpr bool kLead2 = FastTraits<NC>::radix(0) == 2;
   extern __shared__ double2 sm[];
@@ -292,6 +296,7 @@ template <int L, int S>
 __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<L, kSig>())) kbm_row(const double2* __restrict__ in,
                                                                   double2* __restrict__ out, int64_t Bp, int64_t R1,
                                                                   const double2* __restrict__ tw, int sw, int pf) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   extern __shared__ double2 sm[];
   const int r = sw ? blockIdx.y : blockIdx.x;
   const int64_t b0 = (int64_t)(sw ? blockIdx.x : blockIdx.y) * kSig;
@@ -314,6 +319,7 @@ __global__ void __launch_bounds__(fast_threads<C, 4 * RW>(), bm_minb(fast_thread
     const double2* __restrict__ A, int64_t batch, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
     const double* __restrict__ decay, double2* __restrict__ AT, int sw) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int64_t P = (int64_t)R * C;
   extern __shared__ double2 sm[];
   const int m20 = (sw ? blockIdx.y : blockIdx.x) * RW;
@@ -339,6 +345,7 @@ template <int R, int C, int RW>
 __global__ void __launch_bounds__(fast_threads<C, 4 * RW>(), bm_minb(fast_threads<C, 4 * RW>())) kbm_rowout(
     const double2* __restrict__ Z, double2* __restrict__ out, int64_t batch, int64_t Bp,
     const double2* __restrict__ tw, const double* __restrict__ coef, const double2* __restrict__ xsub, int sw) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int64_t P = (int64_t)R * C;
   extern __shared__ double2 sm[];
   const int r0 = (sw ? blockIdx.y : blockIdx.x) * RW;
@@ -402,7 +409,7 @@ struct ChainBM {
     const int64_t Q = n / last_stride<R>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    LAUNCH(bm_col, gdim(2 * C), T, smem, st, in, out, 2 * C, Bp, t.twR, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q,
+    LAUNCH_PDL(bm_col, gdim(2 * C), T, smem, st, in, out, 2 * C, Bp, t.twR, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q,
            nullptr, (int)sw, pf);
     return NFFT45_OK;
   }
@@ -416,7 +423,7 @@ struct ChainBM {
     const int64_t Q = P / last_stride<C, HalfTr<C>>();  // the column IFFT_P runs the HalfTr schedule
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    LAUNCH(bm_band, gdim(R, kSig / G), T, smem, st, T_, U, Bp, t.tw2C, t.twC, t.tP->lo, t.tP->hi, t.tP->s, twQ,
+    LAUNCH_PDL(bm_band, gdim(R, kSig / G), T, smem, st, T_, U, Bp, t.tw2C, t.twC, t.tP->lo, t.tP->hi, t.tP->s, twQ,
            (int)Q, pv.deconv, pv.decay, pv.dd, sub, (int)sw, pf);
     return NFFT45_OK;
   }
@@ -433,7 +440,7 @@ struct ChainBM {
     const int64_t Q = P / last_stride<R>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    LAUNCH(bm_mid, gdim(C), T, smem, st, U, Z, Bp, t.twR, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.ks, (int)sw, pf);
+    LAUNCH_PDL(bm_mid, gdim(C), T, smem, st, U, Z, Bp, t.twR, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.ks, (int)sw, pf);
     return NFFT45_OK;
   }
 
@@ -447,7 +454,7 @@ struct ChainBM {
     const int64_t Q = n / last_stride<2 * C>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    LAUNCH(bm_pad, gdim(R, kSig / G), T, smem, st, Z, Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s, twQ,
+    LAUNCH_PDL(bm_pad, gdim(R, kSig / G), T, smem, st, Z, Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s, twQ,
            (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout, (int)sw, pf);
     return NFFT45_OK;
   }
@@ -462,7 +469,7 @@ struct ChainBM {
     constexpr size_t smem = fast_smem<R, kSig>();
     NFFT_CHECK(bm_attr(bm_row, smem));
     constexpr int T = fast_threads<R, kSig>();
-    LAUNCH(bm_row, gdim(2 * C), T, smem, st, Y, H, Bp, (int64_t)(2 * C), t.twR, (int)sw, pf);
+    LAUNCH_PDL(bm_row, gdim(2 * C), T, smem, st, Y, H, Bp, (int64_t)(2 * C), t.twR, (int)sw, pf);
     return NFFT45_OK;
   }
 
@@ -477,7 +484,7 @@ struct ChainBM {
     NFFT_CHECK(qtab(Q, &twQ));
     static const int bsw = getenv("NFFT45_BOUNDARY_SWAP") != nullptr;  // A/B switch (measured slower)
     const dim3 grid = bsw ? dim3((unsigned)(Bp / 4), (unsigned)(R / RW)) : dim3((unsigned)(R / RW), (unsigned)(Bp / 4));
-    LAUNCH(bm_colin, grid, T, smem, st, A, batch, U, Bp, t.twC, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.decay,
+    LAUNCH_PDL(bm_colin, grid, T, smem, st, A, batch, U, Bp, t.twC, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q, pv.decay,
            AT, bsw);
     return NFFT45_OK;
   }
@@ -490,7 +497,7 @@ struct ChainBM {
     constexpr int T = fast_threads<C, 4 * RW>();
     static const int bsw = getenv("NFFT45_BOUNDARY_SWAP") != nullptr;
     const dim3 grid = bsw ? dim3((unsigned)(Bp / 4), (unsigned)(R / RW)) : dim3((unsigned)(R / RW), (unsigned)(Bp / 4));
-    LAUNCH(bm_rowout, grid, T, smem, st, Z, out, batch, Bp, t.twC, pv.coef, xsub, bsw);
+    LAUNCH_PDL(bm_rowout, grid, T, smem, st, Z, out, batch, Bp, t.twC, pv.coef, xsub, bsw);
     return NFFT45_OK;
   }
 };

@@ -1,6 +1,7 @@
 // common.cuh — shared device/host helpers for libnfft45 (sm_100a, fp64).
 #pragma once
 
+#include <utility>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -44,6 +45,51 @@ void prof_end(int slot, const char* name, cudaStream_t st);
   do {                                                                     \
     int _ps = g_profiling.load(std::memory_order_relaxed) ? prof_begin(stream) : -1; \
     kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);            \
+    if (_ps >= 0) prof_end(_ps, #kernel, stream);                          \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                    \
+    cudaError_t _le = cudaGetLastError();                                  \
+    if (_le == cudaSuccess && g_debug_sync) _le = cudaStreamSynchronize(stream); \
+    if (_le != cudaSuccess) return cuda_fail(_le, #kernel);                \
+  } while (0)
+
+// Programmatic dependent launch (PDL) for the chain / gridding kernels of a
+// solve: each is launched with programmatic stream serialisation, so its
+// launch and CTA rasterisation overlap the tail of the producer kernel on the
+// stream, and it starts with pdl_enter(): griddepcontrol.wait (blocks until
+// the producer grid has completed and its writes are visible -- before ANY
+// global read or write of this kernel).  No kernel triggers its dependents
+// early (launch_dependents): measured, that let waiting CTAs of the next
+// kernel take SM slots and made single transforms at P >= 2^18 up to 20 %
+// slower; wait-only PDL is 2-4 % faster for P <= 2^17 single transforms and
+// neutral elsewhere (scripts/pdl_ab.sh).  Without the launch attribute the
+// wait is a no-op.  NFFT45_NO_PDL=1 turns the attribute off (A/B switch).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+extern const bool g_pdl;
+template <typename... K, typename... A>
+inline cudaError_t launch_pdl(void (*k)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+#define LAUNCH_PDL(kernel, grid, block, smem, stream, ...)                  \
+  do {                                                                     \
+    int _ps = g_profiling.load(std::memory_order_relaxed) ? prof_begin(stream) : -1; \
+    if (g_pdl) {                                                           \
+      cudaError_t _pe = launch_pdl(kernel, dim3(grid), dim3(block), (smem), (stream), __VA_ARGS__); \
+      if (_pe != cudaSuccess) return cuda_fail(_pe, #kernel);              \
+    } else {                                                               \
+      kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);          \
+    }                                                                      \
     if (_ps >= 0) prof_end(_ps, #kernel, stream);                          \
     g_launches.fetch_add(1, std::memory_order_relaxed);                    \
     cudaError_t _le = cudaGetLastError();                                  \

@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
                                                     const double2* __restrict__ amp, int64_t batch, NodeFactor nf,
                                                     double2* __restrict__ H, const int2* __restrict__ ranges, int NS,
                                                     int64_t amp_ld, int64_t H_ld, int ngroups, int sw) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int SIG = 32 * SPL;
   extern __shared__ __align__(16) unsigned char smraw[];
   double2* A0 = reinterpret_cast<double2*>(smraw);                        // [cap][SIG]
@@ -497,7 +498,7 @@ int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const doubl
   auto spread_p = k_spread_p<1>;
   NFFT_CUDA(cudaFuncSetAttribute(spread_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const dim3 grid = sw ? dim3((unsigned)slices, (unsigned)ntiles) : dim3((unsigned)ntiles, (unsigned)slices);
-  LAUNCH(spread_p, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), amp, batch, f, H, ranges,
+  LAUNCH_PDL(spread_p, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), amp, batch, f, H, ranges,
          NS, amp_ld, H_ld, ngroups, sw);
   if (own) NFFT_CUDA(cudaFreeAsync(own, st));
   return NFFT45_OK;
@@ -715,6 +716,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 2) k_gather_b(const double*
                                                     const double2* __restrict__ sub, int mode,
                                                     double2* __restrict__ out, int64_t H_ld, int64_t sub_ld,
                                                     int64_t out_ld, const int* __restrict__ only, int ny) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   // only != nullptr: process just the node blocks flagged there (fallback use;
   // launched with one CTA row that walks all ny signal groups)
   if (only && !only[blockIdx.x]) return;
@@ -748,6 +750,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
     const double* __restrict__ ts, const int* __restrict__ perm, int64_t Q, int64_t n, double alpha, GaussTab G,
     const double2* __restrict__ H, int64_t H_ld, int64_t batch, NodeFactor nf, const double2* __restrict__ sub,
     int64_t sub_ld, int mode, double2* __restrict__ out, int64_t out_ld, int ngroups, int* __restrict__ overflow, int sw) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int HALVES = 32 / SIG, NPL = kNPW / HALVES;
   static_assert(kGatherNodes == 32, "one node per lane in the signal-major staging");
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -967,7 +970,7 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
   {                                                                                                          \
     auto gather_p = k_gather_p<OBM, SM_, S_>;                                                                \
     NFFT_CUDA(cudaFuncSetAttribute(gather_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
-    LAUNCH(gather_p, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, H_ld, batch, f,  \
+    LAUNCH_PDL(gather_p, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, H_ld, batch, f,  \
            sub, sub_ld, mode, out, out_ld, ngroups, overflow, sw);                                           \
   }
 #define NFFT_GP_SUB(OBM, S_) \
@@ -1004,12 +1007,12 @@ int gather_fallback(const GridDev& g, int64_t n, const Window& win, const double
   if (H_ld) {
     auto gather_b = k_gather_b<true>;
     NFFT_CUDA(cudaFuncSetAttribute(gather_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    LAUNCH(gather_b, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), H, batch, f,
+    LAUNCH_PDL(gather_b, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), H, batch, f,
            sub, mode, out, H_ld, sub_ld, out_ld, only, ny);
   } else {
     auto gather_b = k_gather_b<false>;
     NFFT_CUDA(cudaFuncSetAttribute(gather_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    LAUNCH(gather_b, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), H, batch, f,
+    LAUNCH_PDL(gather_b, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), H, batch, f,
            sub, mode, out, H_ld, sub_ld, out_ld, only, ny);
   }
   return NFFT45_OK;

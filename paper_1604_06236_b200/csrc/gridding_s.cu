@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kSTile, (SB == 1 ? 5 : 2) * 256 / kSTile) k_sp
                                                      const double2* __restrict__ amp, int64_t batch, NodeFactor nf,
                                                      double2* __restrict__ H, const int2* __restrict__ ranges,
                                                      int NS) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int kSCap = STile<kSTile>::cap;
   extern __shared__ __align__(16) unsigned char smraw[];
   double* W = reinterpret_cast<double*>(smraw);                   // [cap][kTaps]
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(kWWarps * 32, 7) k_spread_w(const double* __re
                                                               const double2* __restrict__ amp, NodeFactor nf,
                                                               double2* __restrict__ H, const int2* __restrict__ ranges,
                                                               int NS) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   __shared__ __align__(16) double Wsh[kWWarps][32 * kTaps];
   __shared__ __align__(16) double2 Ash[kWWarps][32];
   __shared__ int Csh[kWWarps][32];
@@ -235,6 +237,7 @@ __global__ void __launch_bounds__(kGNodes, (SB == 1 ? 3 : 2) * 256 / kGNodes) k_
                                                       const double2* __restrict__ H, int64_t batch, NodeFactor nf,
                                                       const double2* __restrict__ sub, int mode,
                                                       double2* __restrict__ out) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int kGCap = 4 * kGNodes;
   double2* Y = reinterpret_cast<double2*>(smraw);  // [SB][gslot(kGCap)]
@@ -337,7 +340,7 @@ int spread_small(const GridDev& g, int64_t n, const Window& win, const double2* 
     int2* ownw = nullptr;
     NFFT_CHECK(tile_ranges(g, n, win.m, 32, NSw, st, &rw, &ownw));
     const GaussTab Gw = gauss_tab(win);
-    LAUNCH(k_spread_w, (unsigned)ceil_div(ceil_div(n, 32), kWWarps), kWWarps * 32, 0, st, g.ts, g.perm, g.Q, n,
+    LAUNCH_PDL(k_spread_w, (unsigned)ceil_div(ceil_div(n, 32), kWWarps), kWWarps * 32, 0, st, g.ts, g.perm, g.Q, n,
            win.alpha, Gw, amp, f, H, rw, NSw);
     if (ownw) NFFT_CUDA(cudaFreeAsync(ownw, st));
     return NFFT45_OK;
@@ -357,7 +360,7 @@ int spread_small(const GridDev& g, int64_t n, const Window& win, const double2* 
     auto name = k_spread_s<SBv, TILEv>;                                                                   \
     const size_t smem = STile<TILEv>::smem(SBv);                                                          \
     NFFT_CUDA(cudaFuncSetAttribute(name, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
-    LAUNCH(name, grid, TILEv, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, amp, batch, f, H, ranges, NS); \
+    LAUNCH_PDL(name, grid, TILEv, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, amp, batch, f, H, ranges, NS); \
   }
   if (tile == 128) {
     if (sb == 4) NFFT45_SPREAD_S(spread_s4, 4, 128) else NFFT45_SPREAD_S(spread_s1, 1, 128)
@@ -385,7 +388,7 @@ int gather_small(const GridDev& g, int64_t n, const Window& win, const double2* 
   {                                                                                                       \
     auto name = k_gather_s<SBv, NODESv>;                                                                  \
     NFFT_CUDA(cudaFuncSetAttribute(name, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
-    LAUNCH(name, grid, NODESv, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, batch, f, sub, mode, out); \
+    LAUNCH_PDL(name, grid, NODESv, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, batch, f, sub, mode, out); \
   }
   if (nodes == 128) {
     if (sb == 4) NFFT45_GATHER_S(gather_s4, 4, 128) else NFFT45_GATHER_S(gather_s1, 1, 128)

@@ -20,6 +20,7 @@ namespace nfft45 {
 
 std::atomic<int64_t> g_launches{0};
 const bool g_debug_sync = getenv("NFFT45_DEBUG_SYNC") != nullptr;
+const bool g_pdl = getenv("NFFT45_NO_PDL") == nullptr;
 std::atomic<int> g_profiling{0};
 static thread_local std::string tl_err;
 
