@@ -504,3 +504,47 @@ def test_persistent_gather_fallback_blocks_bitwise(tmp_path):
         outs.append(np.load(f))
     for k in ("t5", "t4", "r4"):
         assert np.array_equal(outs[0][k], outs[1][k]), k
+
+
+_VARIANT_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[2])
+import paper_1604_06236_b200 as nf
+out = {}
+for P, B, J in [(1000, 1, 0.3), (4096, 1, 0.45), (4096, 4, 0.3), (1 << 16, 1, 0.3), (1 << 18, 1, 0.4)]:
+    rng = np.random.default_rng(P + B)
+    t = np.mod((np.arange(P) + rng.uniform(-J, J, P)) / P, 1.0)
+    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-15, P, 2))
+    x = (rng.standard_normal((B, P)) + 1j * rng.standard_normal((B, P))) / np.sqrt(2)
+    x = x[0] if B == 1 else x
+    out[f"t5_{P}_{B}"] = nf.refine_type5(plan, x, passes=1)
+    out[f"t4_{P}_{B}"] = nf.refine_type4(plan, x, passes=1)
+np.savez(sys.argv[1], **out)
+"""
+
+
+def test_kernel_variants_bitwise(tmp_path):
+    """The launch / tiling variants kept as A/B switches compute the same terms
+    in the same order: programmatic dependent launch off (NFFT45_NO_PDL),
+    warp-tiled single-signal spreading forced on / off (NFFT45_SPREAD_WARP),
+    256-cell spreading tiles (NFFT45_STILE) and 256-node interpolation CTAs
+    (NFFT45_GNODES) must all give bitwise the outputs of the default build,
+    for single signals on both sides of the warp-tile threshold, a 4-signal
+    batch and a non-chain size."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    variants = ({}, {"NFFT45_NO_PDL": "1"}, {"NFFT45_SPREAD_WARP": "1"}, {"NFFT45_SPREAD_WARP": "0"},
+                {"NFFT45_STILE": "256", "NFFT45_GNODES": "256"})
+    outs = []
+    for i, extra in enumerate(variants):
+        f = tmp_path / f"v{i}.npz"
+        subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, str(f), root], check=True,
+                       env=dict(os.environ, **extra), timeout=300)
+        outs.append(np.load(f))
+    for extra, o in zip(variants[1:], outs[1:]):
+        for k in outs[0].files:
+            assert np.array_equal(outs[0][k], o[k]), (extra, k)
