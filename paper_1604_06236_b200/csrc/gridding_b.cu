@@ -266,7 +266,6 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
   int* Cc2 = reinterpret_cast<int*>(F + kPipeCap);                        // [cap]
   int* Pi = Cc2 + kPipeCap;                                               // [cap]
   int* Qs = Pi + kPipeCap;                                                // [cap]
-  int* Si = Qs + kPipeCap;                                                // [cap]
   __shared__ int s_cnt[8];
   __shared__ int s_off[8];
 
@@ -291,7 +290,7 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
   for (int si = 0; si < NS && si < 8; si++) total += s_cnt[si];
   const bool pipelined = total <= kPipeCap;
 
-  // node list (first batch) -> Qs, Pi, Si
+  // node list (first batch) -> Qs, Pi
   auto node_at = [&](int g, int& si) -> int64_t {
     si = 0;
     while (si + 1 < NS && si + 1 < 8 && g >= s_off[si + 1]) si++;
