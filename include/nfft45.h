@@ -223,7 +223,10 @@ int nfft45_type4(const nfft45_plan* p, const double* A_dev, int64_t batch, doubl
 /* refine_type5 / refine_type4 (plan, data, passes) — inverse.py:146-202
  * (Section V).  passes = 0 is bitwise the plain solve.  For passes >= 2 the
  * call synchronizes once at the end and returns NON_CONVERGENCE if, for any
- * signal of the batch, a residual norm grew between passes (inverse.py:155). */
+ * signal of the batch, a residual norm grew between passes (inverse.py:155).
+ * In-place calls (S_dev overlapping s_dev) are allowed: the refinement re-reads
+ * its operand after writing x, so an overlapping operand is first copied to
+ * stream-ordered scratch (cost: one D2D copy; the CUDA-graph cache is skipped). */
 int nfft45_refine_type5(const nfft45_plan* p, const double* s_dev, int64_t batch,
                         int passes, double* S_dev, void* stream);
 int nfft45_refine_type4(const nfft45_plan* p, const double* A_dev, int64_t batch,

@@ -564,7 +564,15 @@ static int run_graphed(const nfft45_plan* p, int kind, int64_t batch, int passes
       exec = it->second;
       nkern = mp->gc->kernels[key];
     }
-    else if (++mp->gc->seen[key] >= 2 && mp->gc->execs.size() < 64) capture = true;
+    else if (mp->gc->execs.size() < 64) {
+      // `seen` only counts keys while the cache can still take a graph, and is
+      // trimmed so a long-lived plan fed fresh output pointers stays bounded
+      if (mp->gc->seen.size() >= 512) mp->gc->seen.clear();
+      if (++mp->gc->seen[key] >= 2) {
+        capture = true;
+        mp->gc->seen.erase(key);
+      }
+    }
   }
   if (!exec && !capture) return fn(user);
   if (exec) {  // replay straight into the caller's stream (independent solves on different streams overlap)
@@ -596,7 +604,16 @@ static int run_graphed(const nfft45_plan* p, int kind, int64_t batch, int passes
       }
       // the captured launches were counted by LAUNCH already; replays add nkern each
       ce = cudaGraphInstantiate(&exec, graph, 0);
-      if (ce == cudaSuccess) {
+      if (ce != cudaSuccess) {
+        // could not instantiate: drop the capture and run directly on the caller's stream
+        exec = nullptr;
+        cudaGraphDestroy(graph);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaGetLastError();
+        return fn(user);
+      }
+      {
         std::lock_guard<std::mutex> lk(mp->gc->mu);
         auto it = mp->gc->execs.find(key);
         if (it == mp->gc->execs.end()) {
@@ -640,6 +657,19 @@ void host_pipes_forget(const nfft45_plan* p);
 }
 
 // ================================================================== C ABI
+
+namespace nfft45 {
+// Rows per kernel launch: several launch paths put the row count in
+// gridDim.y (capped at 65535), so every batched C entry point walks its rows
+// in slices of at most kMaxRows (rows are independent solves / transforms).
+constexpr int64_t kMaxRows = 65535;
+template <class F>
+static int by_rows(int64_t batch, const F& f) {
+  if (batch <= kMaxRows) return f((int64_t)0, batch);
+  for (int64_t b0 = 0; b0 < batch; b0 += kMaxRows) NFFT_CHECK(f(b0, std::min(kMaxRows, batch - b0)));
+  return NFFT45_OK;
+}
+}  // namespace nfft45
 
 extern "C" {
 
@@ -781,14 +811,20 @@ int nfft45_type1(const nfft45_grid* g, const double* a, int64_t batch, int64_t R
   if (!g || R < 1 || m < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid type-1 arguments");
   DeviceGuard dg(g->d.device);
   if (dg.status) return dg.status;
-  return type1_core(g->d, C2(a), batch, R, m, R, nullptr, nullptr, D2(out), S(st));
+  const int64_t Q = g->d.Q;
+  return by_rows(batch, [&](int64_t b0, int64_t nb) {
+    return type1_core(g->d, C2(a) + b0 * Q, nb, R, m, R, nullptr, nullptr, D2(out) + b0 * R, S(st));
+  });
 }
 
 int nfft45_type2(const nfft45_grid* g, const double* Sc, int64_t batch, int64_t P, int m, double* out, void* st) {
   if (!g || P < 1 || m < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid type-2 arguments");
   DeviceGuard dg(g->d.device);
   if (dg.status) return dg.status;
-  return type2_core(g->d, C2(Sc), batch, P, m, nullptr, D2(out), S(st));
+  const int64_t Q = g->d.Q;
+  return by_rows(batch, [&](int64_t b0, int64_t nb) {
+    return type2_core(g->d, C2(Sc) + b0 * P, nb, P, m, nullptr, D2(out) + b0 * Q, S(st));
+  });
 }
 
 int nfft45_nonuniform_conv(const nfft45_grid* g, const double* a, int64_t batch, const double* lam, int64_t R,
@@ -803,10 +839,13 @@ int nfft45_nonuniform_conv(const nfft45_grid* g, const double* a, int64_t batch,
   DeviceGuard dg(g->d.device);
   if (dg.status) return dg.status;
   cudaStream_t s = S(st);
-  Scratch V(s);
-  NFFT_CHECK(V.alloc(sizeof(double2) * batch * P));
-  NFFT_CHECK(type1_core(g->d, C2(a), batch, R, m, P, C2(lam), nullptr, V.c(), s));
-  return fft_run(V.c(), D2(out), batch, P, +1, nullptr, nullptr, s);
+  const int64_t Q = g->d.Q;
+  return by_rows(batch, [&](int64_t b0, int64_t nb) {
+    Scratch V(s);
+    NFFT_CHECK(V.alloc(sizeof(double2) * nb * P));
+    NFFT_CHECK(type1_core(g->d, C2(a) + b0 * Q, nb, R, m, P, C2(lam), nullptr, V.c(), s));
+    return fft_run(V.c(), D2(out) + b0 * P, nb, P, +1, nullptr, nullptr, s);
+  });
 }
 
 // cg_solve(grid, rhs, which, tol, max_iter, spread_width) — baselines.py:108-181.
@@ -868,19 +907,27 @@ int nfft45_type1_direct(const nfft45_grid* g, const double* a, int64_t batch, in
   if (!g || R < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid direct type-1 arguments");
   DeviceGuard dg(g->d.device);
   if (dg.status) return dg.status;
-  return direct_type1(g->d, C2(a), batch, R, D2(out), S(st));
+  const int64_t Q = g->d.Q;
+  return by_rows(batch, [&](int64_t b0, int64_t nb) {
+    return direct_type1(g->d, C2(a) + b0 * Q, nb, R, D2(out) + b0 * R, S(st));
+  });
 }
 
 int nfft45_type2_direct(const nfft45_grid* g, const double* Sc, int64_t batch, int64_t P, double* out, void* st) {
   if (!g || P < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid direct type-2 arguments");
   DeviceGuard dg(g->d.device);
   if (dg.status) return dg.status;
-  return direct_type2(g->d, C2(Sc), batch, P, D2(out), S(st));
+  const int64_t Q = g->d.Q;
+  return by_rows(batch, [&](int64_t b0, int64_t nb) {
+    return direct_type2(g->d, C2(Sc) + b0 * P, nb, P, D2(out) + b0 * Q, S(st));
+  });
 }
 
 int nfft45_dft(const double* in, double* out, int64_t batch, int64_t N, int sign, void* st) {
   if (N < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "DFT length must be >= 1");
-  return fft_run(C2(in), D2(out), batch, N, sign, nullptr, nullptr, S(st));
+  return by_rows(batch, [&](int64_t b0, int64_t nb) {
+    return fft_run(C2(in) + b0 * N, D2(out) + b0 * N, nb, N, sign, nullptr, nullptr, S(st));
+  });
 }
 
 int nfft45_v_samples(const nfft45_grid* g, double a, int eta, int m, double* v, void* st) {
@@ -1070,6 +1117,10 @@ int nfft45_plan_table(const nfft45_plan* p, int which, double* dst, void* st) {
 
 int nfft45_type5(const nfft45_plan* p, const double* s, int64_t batch, double* out, void* st) {
   if (!p) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid plan");
+  if (batch > kMaxRows)  // independent rows: slices keep every launch's gridDim.y in range
+    return by_rows(batch, [&](int64_t b0, int64_t nb) {
+      return nfft45_type5(p, s + 2 * b0 * p->P, nb, out + 2 * b0 * p->P, st);
+    });
   DeviceGuard dg(p->g->d.device);
   if (dg.status) return dg.status;
   if (tiny_eligible(p->P, p->m, 0, batch))
@@ -1080,6 +1131,10 @@ int nfft45_type5(const nfft45_plan* p, const double* s, int64_t batch, double* o
 
 int nfft45_type4(const nfft45_plan* p, const double* A, int64_t batch, double* out, void* st) {
   if (!p) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid plan");
+  if (batch > kMaxRows)  // independent rows: slices keep every launch's gridDim.y in range
+    return by_rows(batch, [&](int64_t b0, int64_t nb) {
+      return nfft45_type4(p, A + 2 * b0 * p->P, nb, out + 2 * b0 * p->P, st);
+    });
   DeviceGuard dg(p->g->d.device);
   if (dg.status) return dg.status;
   if (tiny_eligible(p->P, p->m, 0, batch))
@@ -1088,24 +1143,66 @@ int nfft45_type4(const nfft45_plan* p, const double* A, int64_t batch, double* o
                      [&](cudaStream_t ss) { return type4_core(p, C2(A), batch, D2(out), ss); });
 }
 
+}  // extern "C"
+
+namespace nfft45 {
+// The refinement re-reads its operand after writing the first solution x into
+// `out` (residual = forward(x) - data), so an operand that overlaps `out` is
+// first copied to stream-ordered scratch (the one-CTA small solves consume each
+// row before writing it and need no copy).  Returns the operand to use.
+static int unalias(const double* in, const double* out, int64_t n_doubles, cudaStream_t st, Scratch& copy,
+                   const double** use) {
+  *use = in;
+  const uintptr_t a0 = (uintptr_t)in, a1 = a0 + sizeof(double) * n_doubles;
+  const uintptr_t b0 = (uintptr_t)out, b1 = b0 + sizeof(double) * n_doubles;
+  if (n_doubles <= 0 || a1 <= b0 || b1 <= a0) return NFFT45_OK;
+  NFFT_CHECK(copy.alloc(sizeof(double) * n_doubles));
+  NFFT_CUDA(cudaMemcpyAsync(copy.d(), in, sizeof(double) * n_doubles, cudaMemcpyDeviceToDevice, st));
+  *use = copy.d();
+  return NFFT45_OK;
+}
+}  // namespace nfft45
+
+extern "C" {
+
 int nfft45_refine_type5(const nfft45_plan* p, const double* s, int64_t batch, int passes, double* out, void* st) {
   if (!p || passes < 0) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid refine arguments");
+  if (batch > kMaxRows)  // independent rows: slices keep every launch's gridDim.y in range
+    return by_rows(batch, [&](int64_t b0, int64_t nb) {
+      return nfft45_refine_type5(p, s + 2 * b0 * p->P, nb, passes, out + 2 * b0 * p->P, st);
+    });
   DeviceGuard dg(p->g->d.device);
   if (dg.status) return dg.status;
   if (tiny_eligible(p->P, p->m, passes, batch))
     return tiny_solve(p->g->d, p->P, p->c5, p->c4, p->decay, p->ks, p->coef, 5, C2(s), batch, passes, D2(out),
                       S(st));
+  if (passes > 0) {
+    Scratch copy(S(st));
+    const double* use = s;
+    NFFT_CHECK(unalias(s, out, 2 * batch * p->P, S(st), copy, &use));
+    if (use != s) return refine_core(p, C2(use), batch, passes, D2(out), true, S(st));
+  }
   return run_graphed(p, 15, batch, passes, s, out, S(st),
                      [&](cudaStream_t ss) { return refine_core(p, C2(s), batch, passes, D2(out), true, ss); });
 }
 
 int nfft45_refine_type4(const nfft45_plan* p, const double* A, int64_t batch, int passes, double* out, void* st) {
   if (!p || passes < 0) return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid refine arguments");
+  if (batch > kMaxRows)  // independent rows: slices keep every launch's gridDim.y in range
+    return by_rows(batch, [&](int64_t b0, int64_t nb) {
+      return nfft45_refine_type4(p, A + 2 * b0 * p->P, nb, passes, out + 2 * b0 * p->P, st);
+    });
   DeviceGuard dg(p->g->d.device);
   if (dg.status) return dg.status;
   if (tiny_eligible(p->P, p->m, passes, batch))
     return tiny_solve(p->g->d, p->P, p->c5, p->c4, p->decay, p->ks, p->coef, 4, C2(A), batch, passes, D2(out),
                       S(st));
+  if (passes > 0) {
+    Scratch copy(S(st));
+    const double* use = A;
+    NFFT_CHECK(unalias(A, out, 2 * batch * p->P, S(st), copy, &use));
+    if (use != A) return refine_core(p, C2(use), batch, passes, D2(out), false, S(st));
+  }
   return run_graphed(p, 14, batch, passes, A, out, S(st),
                      [&](cudaStream_t ss) { return refine_core(p, C2(A), batch, passes, D2(out), false, ss); });
 }

@@ -36,7 +36,8 @@ def gather_rows(local, batch: int, world: int, rank: int, group=None, dst: int =
     if world == 1:
         return local
     if local.is_complex():  # collectives move the interleaved (re, im) doubles
-        full = gather_rows(torch.view_as_real(local).reshape(local.shape[0], -1), batch, world, rank, group, dst)
+        full = gather_rows(torch.view_as_real(local).reshape(local.shape[0], 2 * local.shape[1]), batch, world, rank,
+                           group, dst)
         return None if full is None else torch.view_as_complex(full.reshape(batch, -1, 2).contiguous())
     n = local.shape[1]
     rows = [shard_bounds(batch, world, r) for r in range(world)]

@@ -57,7 +57,7 @@ def _worker(rank, world, port, batch, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("batch", [5, 8])
+@pytest.mark.parametrize("batch", [1, 5, 8])
 def test_two_rank_sharded_solve_matches_single_process(batch):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

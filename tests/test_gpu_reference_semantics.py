@@ -453,3 +453,69 @@ def test_input_validation_errors():
         nf.nfft_type1(g, np.ones(9), 8)
     with pytest.raises(ValueError):
         nf.nfft_type1(g, np.ones(8), 0)
+
+
+# ------------------------------------------- advisor findings (round 1)
+
+@pytest.mark.parametrize("P,batch", [(64, 3), (1000, 2), (4096, 1), (4096, 20), (1 << 14, 40)])
+@pytest.mark.parametrize("kind", [5, 4])
+def test_refine_in_place_out_equals_input(P, batch, kind):
+    """out= aliasing the operand (S_dev == s_dev) gives the out-of-place result:
+    the refinement re-reads its operand after writing x (tiny, chain and generic paths)."""
+    import torch
+
+    rng = np.random.default_rng(P + batch)
+    g = jittered(P, rng)
+    plan = nf.build_plan(g, std_params(P, mu=1e-15))
+    x = torch.from_numpy(np.stack([randc(P, rng) for _ in range(batch)])).cuda()
+    fn = nf.refine_type5 if kind == 5 else nf.refine_type4
+    for passes in (1, 2):
+        ref = fn(plan, x, passes=passes)
+        y = x.clone()
+        got = fn(plan, y, passes=passes, out=y)
+        assert got.data_ptr() == y.data_ptr()
+        assert torch.equal(ref, y), (passes, float((ref - y).abs().max()))
+
+
+def test_more_than_65535_rows_at_non_power_of_two_size():
+    """Batched launches walk rows in slices of 65535 (gridDim.y cap): forward
+    NFFTs, DFTs and solves with 70000 rows match the row-wise results."""
+    import torch
+
+    rng = np.random.default_rng(70000)
+    P, rows = 6, 70000
+    g = jittered(P, rng)
+    plan = nf.build_plan(g, std_params(P, mu=1e-11))
+    x = torch.from_numpy(rng.standard_normal((rows, P)) + 1j * rng.standard_normal((rows, P))).cuda()
+    pick = [0, 1, 65534, 65535, 65536, rows - 1]
+
+    def close(a, b):  # batched and single-row kernels may differ in rounding only
+        return float((a - b).abs().max() / b.abs().max()) < 1e-12
+
+    out = nf.nfft_type2(x, g)
+    for r in pick:
+        assert close(out[r], nf.nfft_type2(x[r:r + 1], g)[0])
+    d = nf.dft(x)
+    for r in pick:
+        assert close(d[r], nf.dft(x[r:r + 1])[0])
+    for fn in (nf.refine_type5, nf.refine_type4):
+        y = fn(plan, x, passes=1)
+        for r in pick:
+            assert close(y[r], fn(plan, x[r:r + 1], passes=1)[0])
+
+
+def test_graph_cache_stays_bounded_with_fresh_outputs():
+    """A plan fed a fresh output buffer on every call keeps working (the
+    capture-candidate table is trimmed) and results stay bitwise equal."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    P = 4096
+    g = jittered(P, rng)
+    plan = nf.build_plan(g, std_params(P, mu=1e-15))
+    x = torch.from_numpy(randc(P, rng)).cuda()
+    ref = nf.refine_type5(plan, x, passes=1)
+    keep = []
+    for _ in range(600):
+        keep.append(nf.refine_type5(plan, x, passes=1))
+    assert all(torch.equal(ref, k) for k in keep[::50])
