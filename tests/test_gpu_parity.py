@@ -236,9 +236,50 @@ def test_rectangular_single_signal_chains(P):
     _check_config(P, 0.3, 1, 16051, passes=(1,))
 
 
-@pytest.mark.parametrize("J,eta", [(0.1, 2), (0.45, 2), (0.3, 3)])
-def test_c5_sweep_2_18(J, eta):
-    _check_config(1 << 18, J, 1, 16045, eta=eta, passes=(1,))
+# BASELINE config 5, every oracle-backed cell: P = 2^18, one signal (seed 16045),
+# J x eta x mu.  The gate is G1 at the cell's stated pass count: passes = 1,
+# except where the reference's OWN one-pass output has not converged — its
+# distance to its own two-pass result (the "self-floor", measured live below
+# and listed in profiles/c5_sweep.md) exceeds 1e-11, i.e. the over-damped
+# corner mu <= 1e-17 at eta = 2 and mu = 1e-16 at J = 0.45 (reference
+# self-floor 5e-11 ... 8e-10, one-pass residual up to 8e-10).  There the
+# comparison is at passes = 2 (both converge to ~1e-15).
+C5_PASSES2 = {(0.1, 2, 1e-17), (0.3, 2, 1e-17), (0.45, 2, 1e-17), (0.45, 2, 1e-16)}
+C5_CELLS = [(J, eta, mu) for J in (0.1, 0.3, 0.45) for eta in (2, 3) for mu in (1e-17, 1e-16, 1e-15, 1e-14, 1e-13)]
+
+
+def _oracle_two_passes(oplan, x, kind, t, P):
+    """The reference's refinement (inverse.py:146-162) unrolled: x1 and x2 and the residuals."""
+    solve = O.solve5 if kind == 5 else O.solve4
+    fwd = (lambda v: O.type2(v, t)) if kind == 5 else (lambda v: O.type1(t, v, P))
+    x0 = solve(oplan, x)
+    x1 = x0 - solve(oplan, fwd(x0) - x)
+    r1 = fwd(x1) - x
+    x2 = x1 - solve(oplan, r1)
+    return x1, x2, float(np.linalg.norm(r1) / np.linalg.norm(x))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("J,eta,mu", C5_CELLS)
+def test_c5_grid_2_18(J, eta, mu):
+    P = 1 << 18
+    t, data = O.make_inputs(P, J, 1, 16045)
+    x = data[0]
+    prm = nf.MethodParams.from_mu(mu, P, eta)
+    plan = nf.build_plan(nf.validate_grid(t), prm)
+    oplan = O.Plan.build(t, prm.damping_a, eta)
+    passes = 2 if (J, eta, mu) in C5_PASSES2 else 1
+    for kind in (5, 4):
+        x1, x2, ref_res1 = _oracle_two_passes(oplan, x, kind, t, P)
+        floor = rel(x2, x1)  # the reference's own one-pass non-convergence
+        if passes == 1:
+            assert floor <= 1e-11, (kind, floor)  # the stated pass count is the right one
+        else:
+            assert floor > 1e-11, (kind, floor)
+        got = (nf.refine_type5 if kind == 5 else nf.refine_type4)(plan, x, passes=passes)
+        err = rel(x1 if passes == 1 else x2, got)
+        res = rel(x, O.type2(got, t)) if kind == 5 else rel(x, O.type1(t, got, P))
+        assert err <= G1 and res <= G1, (kind, passes, err, res, floor, ref_res1)
 
 
 # Extension: BASELINE config 5's eta = 1.5 (the reference needs an integer
@@ -266,11 +307,6 @@ def test_c5_fractional_eta_truth_by_construction():
     plan_v = plan.kernel_data.v_samples
     oracle_v = O.v_samples_terms(t, plan.params.damping_a, 3 * P // 2)
     assert rel(oracle_v, plan_v) < 1e-10  # length-3P/2 series, FFT sizes 3*2^k: rounding-level agreement
-
-
-@pytest.mark.parametrize("mu", [1e-17, 1e-13])
-def test_c5_attenuation_sweep(mu):
-    _check_config(1 << 18, 0.3, 1, 16045, mu=mu, passes=(1,))
 
 
 def test_plain_path_is_at_least_as_accurate_as_reference():

@@ -2,6 +2,7 @@
 error mapping, window metadata and the analytic flop accounting — checked
 against the reference's semantics and its recorded values."""
 
+import os
 import warnings
 
 import numpy as np
@@ -11,6 +12,8 @@ import paper_1604_06236_b200 as nf
 from paper_1604_06236_b200 import flops as F
 from paper_1604_06236_b200 import inverse as inv
 from oracle import nfft_oracle as O
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 # --- MethodParams / Eq. 49 (grid.py:99-160) -------------------------------------
@@ -217,3 +220,21 @@ def test_cg_argument_checks_precede_device_work():
         nf.cg_solve(grid, np.ones(8), tol=0.0)
     with pytest.raises(ValueError):
         nf.cg_solve(grid, np.ones(8), which="type3")
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """bench.py --gpus N never silently runs on fewer GPUs: with fewer than N
+    visible devices (none here) it prints an error line and exits non-zero."""
+    import json
+    import subprocess
+    import sys
+
+    import torch
+
+    if torch.cuda.device_count() >= 8:
+        pytest.skip("8 GPUs visible")
+    res = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "8", "--steps", "1"],
+                         capture_output=True, text=True, timeout=300)
+    assert res.returncode != 0
+    line = json.loads([l for l in res.stdout.splitlines() if l.startswith("{")][-1])
+    assert "error" in line and line["n_gpus"] == 8
