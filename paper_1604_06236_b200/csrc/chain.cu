@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(fast_threads<2 * PC, C>(), 2) kc_band(
     const double2* __restrict__ T, double2* __restrict__ U, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
     const double* __restrict__ deconv, const double* __restrict__ decay, const double* __restrict__ dd,
-    const double2* __restrict__ sub, const double2* __restrict__ twQ, int Q) {
+    const double2* __restrict__ sub, const double2* __restrict__ twQ, int Q, double2* __restrict__ rsave) {
   pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int64_t P = (int64_t)PR * PC, n = 2 * P;
   constexpr int NR = 2 * PC;
@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(fast_threads<2 * PC, C>(), 2) kc_band(
       if (sub) {  // type-4 residual: (X deconv - A) decay
         v = rscale(v, __ldg(&deconv[p]));
         v = csub(v, sub[bi * P + p]);
+        if (rsave) rsave[bi * P + p] = v;  // the residual itself (norms for passes >= 2)
         v = rscale(v, __ldg(&decay[p]));
       } else {
         v = rscale(v, __ldg(&dd[p]));  // deconv * decay
@@ -251,7 +252,8 @@ struct Chain {
   }
 
   static int band(const double2* T_, double2* U, int64_t batch, const ChainTabs& t, const double* deconv,
-                  const double* decay, const double* dd, const double2* sub, cudaStream_t st) {
+                  const double* decay, const double* dd, const double2* sub, cudaStream_t st,
+                  double2* rsave = nullptr) {
     auto chain_band = kc_band<PR, PC, C>;
     constexpr size_t smem = fast_smem<2 * PC, C>();
     NFFT_CHECK(chain_attr(chain_band, smem));
@@ -262,7 +264,7 @@ struct Chain {
     if (!twQ) return status;
     dim3 grid((unsigned)(PR / C), (unsigned)batch);
     LAUNCH_PDL(chain_band, grid, T, smem, st, T_, U, t.tw2C, t.twC, t.tP->lo, t.tP->hi, t.tP->s, deconv, decay, dd, sub,
-           twQ, (int)Q);
+           twQ, (int)Q, rsave);
     return NFFT45_OK;
   }
 
@@ -385,7 +387,10 @@ static int chain_solve(const ChainPlanView& pv, int kind, const double2* data, i
         NodeFactor ph{nullptr, (double)(P / 2), -1};
         NFFT_CHECK(spread(g, n, win, out, batch, ph, b.H, st));
         NFFT_CHECK((Ch::template col<PR, -1>(b.H, b.H, batch, n, 2 * PC, t.twR, t.tN, nullptr, st)));
-        NFFT_CHECK(Ch::band(b.H, b.U, batch, t, pv.deconv, pv.decay, pv.dd, data, st));
+        // passes >= 2: the band epilogue also stores r itself, whose norms feed the
+        // NonConvergence check (inverse.py:154-159)
+        NFFT_CHECK(Ch::band(b.H, b.U, batch, t, pv.deconv, pv.decay, pv.dd, data, st, norms ? R : nullptr));
+        if (norms) NFFT_CHECK(row_norms(R, P, batch, norms + (int64_t)pass * batch, st));
         NFFT_CHECK(back(nullptr, out, out, false));
       }
     }

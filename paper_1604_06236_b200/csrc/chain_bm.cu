@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
     const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
-    const double* __restrict__ dd, const double2* __restrict__ sub, int sw, int pf) {
+    const double* __restrict__ dd, const double2* __restrict__ sub, int sw, int pf, double2* __restrict__ rsave) {
   pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int NR = 2 * C;
   extern __shared__ double2 sm[];
@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
       if (sub) {
         v = rsc(v, s_t0[m1]);
         v = csub(v, s_sb[m1 * SG + c]);
+        if (rsave) rsave[((int64_t)k1 + (int64_t)R * m1) * Bp + b0 + c] = v;  // r itself (norms, passes >= 2)
         v = rsc(v, s_t1[m1]);
       } else {
         v = rsc(v, s_t0[m1]);
@@ -415,7 +416,7 @@ struct ChainBM {
   }
 
   template <int G>
-  int band_g(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub) {
+  int band_g(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub, double2* rsave) {
     auto bm_band = kbm_band<R, C, G>;
     const size_t smem = fast_smem<2 * C, G>() + 2 * sizeof(double) * C + (sub ? sizeof(double2) * C * G : 0);
     NFFT_CHECK(bm_attr(bm_band, smem));
@@ -424,12 +425,12 @@ struct ChainBM {
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
     LAUNCH_PDL(bm_band, gdim(R, kSig / G), T, smem, st, T_, U, Bp, t.tw2C, t.twC, t.tP->lo, t.tP->hi, t.tP->s, twQ,
-           (int)Q, pv.deconv, pv.decay, pv.dd, sub, (int)sw, pf);
+           (int)Q, pv.deconv, pv.decay, pv.dd, sub, (int)sw, pf, rsave);
     return NFFT45_OK;
   }
-  int band(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub) {
-    if (small_tiles || SG < kSig) return band_g<kSig / 2>(T_, U, pv, sub);  // always for C = 1024
-    return band_g<kSig>(T_, U, pv, sub);
+  int band(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub, double2* rsave = nullptr) {
+    if (small_tiles || SG < kSig) return band_g<kSig / 2>(T_, U, pv, sub, rsave);  // always for C = 1024
+    return band_g<kSig>(T_, U, pv, sub, rsave);
   }
 
   int mid(const double2* U, double2* Z, const ChainPlanView& pv) {
@@ -598,7 +599,10 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
         NodeFactor ph{nullptr, (double)(P / 2), -1};
         NFFT_CHECK(spread_layout(g, n, win, X, batch, Bp, ph, H, Bp, st));
         NFFT_CHECK(ch.col(H, H));
-        NFFT_CHECK(ch.band(H, U, pv, AT));
+        // passes >= 2: the band epilogue also stores r itself into Y (free until
+        // the pad below), whose norms feed the NonConvergence check (inverse.py:154-159)
+        NFFT_CHECK(ch.band(H, U, pv, AT, norms ? Y : nullptr));
+        if (norms) NFFT_CHECK(norms_bm(Y, P, batch, Bp, norms + (int64_t)pass * batch, st));
         NFFT_CHECK(back(last ? out : X, last ? 0 : Bp, X, Bp));
       }
     }

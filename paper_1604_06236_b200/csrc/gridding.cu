@@ -440,26 +440,33 @@ int gather_layout(const GridDev& g, int64_t n, const Window& win, const double2*
   return gather_mode(g, n, win, H, batch, f, sub, mode, out, st);
 }
 
-__global__ void k_norms_bm(const double2* __restrict__ r, int64_t len, int64_t ld, double* __restrict__ norms) {
-  __shared__ double part[256];
-  const int64_t b = blockIdx.x;
+// Per-signal residual norms over a batch-minor [len][ld] array: lanes run over
+// 32 consecutive signals (coalesced 512-B rows), the 8 warps of a block over
+// interleaved rows; fixed-order warp partials, then a fixed-order sum.
+__global__ void __launch_bounds__(256) k_norms_bm(const double2* __restrict__ r, int64_t len, int64_t ld,
+                                                  int64_t batch, double* __restrict__ norms) {
+  __shared__ double part[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t b = (int64_t)blockIdx.x * 32 + lane;
   double s = 0.0;
-  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
-    double2 v = r[i * ld + b];
-    s = fma(v.x, v.x, fma(v.y, v.y, s));
-  }
-  part[threadIdx.x] = s;
+  if (b < batch)
+    for (int64_t i = w; i < len; i += 8) {
+      const double2 v = r[i * ld + b];
+      s = fma(v.x, v.x, fma(v.y, v.y, s));
+    }
+  part[w][lane] = s;
   __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
-    __syncthreads();
+  if (w == 0 && b < batch) {
+    double t = part[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; k++) t += part[k][lane];
+    norms[b] = sqrt(t);
   }
-  if (threadIdx.x == 0) norms[b] = sqrt(part[0]);
 }
 
 int norms_bm(const double2* r, int64_t len, int64_t batch, int64_t ld, double* norms, cudaStream_t st) {
   if (batch <= 0) return NFFT45_OK;
-  LAUNCH(k_norms_bm, (unsigned)batch, 256, 0, st, r, len, ld, norms);
+  LAUNCH(k_norms_bm, (unsigned)ceil_div(batch, 32), 256, 0, st, r, len, ld, batch, norms);
   return NFFT45_OK;
 }
 

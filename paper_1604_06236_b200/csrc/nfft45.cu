@@ -480,7 +480,7 @@ static int check_norms(const double* d_norms, int64_t batch, int passes, cudaStr
 
 static int refine_core(const nfft45_plan* p, const double2* data, int64_t batch, int passes, double2* out,
                        bool type5, cudaStream_t st) {
-  if (use_chain(p, batch) && (type5 || passes <= 1)) {
+  if (use_chain(p, batch)) {
     Scratch norms(st);
     if (passes >= 2) NFFT_CHECK(norms.alloc(sizeof(double) * batch * passes));
     NFFT_CHECK(chain_run(chain_view(p), type5 ? 5 : 4, data, batch, passes, out, passes >= 2 ? norms.d() : nullptr,

@@ -584,3 +584,37 @@ def test_kernel_variants_bitwise(tmp_path):
     for extra, o in zip(variants[1:], outs[1:]):
         for k in outs[0].files:
             assert np.array_equal(outs[0][k], o[k]), (extra, k)
+
+
+# ------------------------------------- fused multi-pass type-4 refinement
+
+@pytest.mark.parametrize("B", [1, 20])
+def test_type4_multi_pass_on_fused_chains(B):
+    """refine_type4 with passes >= 2 runs on the fused chains (signal-major for
+    B < 16, batch-minor otherwise): the band epilogue stores the residual for
+    the NonConvergence norms (inverse.py:146-185).  Over-damped cell where the
+    second pass matters (J = 0.45, mu = 1e-17): vs the oracle at 2 and 3 passes."""
+    P = 4096
+    t, data = O.make_inputs(P, 0.45, B, 16048)
+    prm = nf.MethodParams.from_mu(1e-17, P, 2)
+    plan = nf.build_plan(nf.validate_grid(t), prm)
+    oplan = O.Plan.build(t, prm.damping_a, 2)
+    x = data if B > 1 else data[0]
+    for passes in (2, 3):
+        got = np.atleast_2d(nf.refine_type4(plan, x, passes=passes))
+        for r in sorted({0, B - 1}):
+            assert rel(O.refine4(oplan, data[r], passes), got[r]) <= G1
+            assert rel(data[r], O.type1(t, got[r], P)) <= G1
+
+
+@pytest.mark.parametrize("B", [1, 20])
+def test_type4_multi_pass_nonconvergence_on_fused_chains(B):
+    """eta = 1, mu = 1e-16, J = 0.45 at P = 4096: the reference's residual grows
+    between passes (oracle raises); the fused chain path raises NonConvergenceError."""
+    P = 4096
+    t, data = O.make_inputs(P, 0.45, B, 16048)
+    with pytest.raises(O.NonConvergence):
+        O.refine4(O.Plan.build(t, O.damping(1e-16, P, 1), 1), data[0], 4)
+    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-16, P, 1))
+    with pytest.raises(nf.NonConvergenceError):
+        nf.refine_type4(plan, data if B > 1 else data[0], passes=4)
