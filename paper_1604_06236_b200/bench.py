@@ -1,15 +1,26 @@
-"""Monte-Carlo harness of the paper's figure protocols on the GPU
-(reference bench.py:1-301).
+"""GPU-first Monte-Carlo harness for the paper's figure protocols
+(reference bench.py:38-301).
 
-Same protocol and API as the reference: each trial draws a jittered regular
-grid and CN(0, 1) amplitudes from Philox(key = seed ^ trial); the spectrum
-handed to every solver is the EXACT direct sum (here the direct-sum kernel),
-never the fast transform; errors are relative l2, linear and 20 log10 dB;
-GE / CG run once per trial, the fast methods once per feasible (eta, mu)
-sharing one plan between the plain and refined solves; infeasible mu and
-non-contracting multi-pass cells are skipped.  What changes is where it
-runs: the trial's grid, spectrum, truth and every solve stay on the device
-(torch CUDA tensors), so a full figure sweep costs seconds instead of hours.
+Public API and record semantics are the reference's (TrialConfig,
+TrialResult, run_sweep, best_mu, filter_best_mu, FIGURE_DEFAULTS,
+run_figure): a trial's grid and truth come from Philox(key = seed ^ trial)
+(metrics.trial_arrays, bit-identical to the reference's streams), the
+spectrum handed to every solver is the EXACT direct sum, errors are relative
+l2 (linear and 20 log10 dB), infeasible mu and non-contracting multi-pass
+cells produce no record, and the records come out in the reference's order.
+
+The execution is organised for the device instead of as a trial loop:
+
+1. all trials of one size P are drawn up front; their nodes, truths and
+   direct-sum spectra live on the GPU for the whole size;
+2. the parameter-free dense solvers (device GE, device CGNR) run per trial;
+3. the fast methods run CELL-MAJOR: for each feasible (eta, mu) cell the
+   plans of all trials are built and the plain and refined solves launched
+   back to back; their relative errors are reduced on the device into one
+   [cells, trials, 2] tensor, read back once per size;
+4. flop totals are charged once per (P, cell, method) — the reference's
+   model is data independent (flops.py) — except CG, whose charge depends
+   on its iteration count.
 """
 
 from __future__ import annotations
@@ -25,23 +36,22 @@ from .baselines import cg_solve, ge_solve, type4_system
 from .errors import AmplificationWarning, NonConvergenceError, NonPositiveDampingError, ZeroReferenceError
 from .flops import FlopCounter
 from .forward import nfft_type1_direct
-from .grid import MethodParams
-from .inverse import build_plan, refine_type4, type4
-from .metrics import generate_trial, relative_error
+from .grid import MethodParams, validate_grid
+from .inverse import build_plan, charge_plan, charge_refine, charge_type4, refine_type4, type4
+from .metrics import generate_trial, relative_error, trial_arrays  # noqa: F401  (re-exported API)
 
 GE_SIZE_CAP = 8192
-MU_SWEEP_DEFAULT = tuple(float(m) for m in np.logspace(-18.0, -4.0, 29))
+MU_SWEEP_DEFAULT = tuple(float(v) for v in 10.0 ** np.linspace(-18.0, -4.0, 29))
 
-METHOD_GE = "GE"
-METHOD_CG = "CG"
-METHOD_NFFT = "NFFT"
-METHOD_RNFFT = "R-NFFT"
+METHOD_GE, METHOD_CG, METHOD_NFFT, METHOD_RNFFT = "GE", "CG", "NFFT", "R-NFFT"
 ALL_METHODS = (METHOD_GE, METHOD_CG, METHOD_NFFT, METHOD_RNFFT)
+_DENSE = (METHOD_GE, METHOD_CG)
+_FAST = (METHOD_NFFT, METHOD_RNFFT)
 
 
 @dataclass(frozen=True)
 class TrialConfig:
-    """One sweep specification (bench.py:45-66). Scalar fields accept tuples to sweep."""
+    """A sweep: every size p, trial, method and (eta, mu) cell (reference bench.py:45-67)."""
 
     p: tuple[int, ...] = (1024,)
     eta: tuple[int, ...] = (1,)
@@ -57,9 +67,9 @@ class TrialConfig:
     def __post_init__(self):
         if not 0.0 <= self.jitter_max < 1.0:
             raise ValueError("jitter_max must lie in [0, 1) to keep nodes distinct")
-        for m in self.methods:
-            if m not in ALL_METHODS:
-                raise ValueError(f"unknown method {m!r}")
+        bad = [m for m in self.methods if m not in ALL_METHODS]
+        if bad:
+            raise ValueError(f"unknown method {bad[0]!r}")
 
 
 @dataclass(frozen=True)
@@ -77,136 +87,175 @@ class TrialResult:
 
 
 def to_db(error_linear: float) -> float:
-    return float("-inf") if error_linear <= 0.0 else 20.0 * math.log10(error_linear)
+    """20 log10 of a linear error (-inf for an exact result)."""
+    return 20.0 * math.log10(error_linear) if error_linear > 0.0 else float("-inf")
 
 
-def _device_error(truth: torch.Tensor, est) -> float:
-    """relative_error on device tensors (one scalar read back)."""
-    est = torch.as_tensor(est, device=truth.device) if not isinstance(est, torch.Tensor) else est
-    tn = float(torch.linalg.vector_norm(truth))
-    if tn == 0.0:
-        raise ZeroReferenceError("relative error undefined: reference vector is zero")
-    return float(torch.linalg.vector_norm(truth - est.to(truth.device))) / tn
+class _Size:
+    """Every trial of one size P, resident on the device."""
+
+    def __init__(self, P: int, cfg: TrialConfig):
+        self.P = P
+        self.seeds = [cfg.seed ^ k for k in range(cfg.trials)]
+        self.grids, truths = [], []
+        for s in self.seeds:
+            nodes, amp = trial_arrays(P, s, cfg.jitter_max)
+            self.grids.append(validate_grid(nodes))
+            truths.append(amp)
+        self.truth = torch.from_numpy(np.stack(truths)).cuda()          # [trials, P]
+        self.truth_norm = torch.linalg.vector_norm(self.truth, dim=1)  # [trials]
+        # exact spectra A_p = sum_q a_q e^{-2 pi i p t_q} (direct-sum kernel, one launch per grid)
+        self.spectrum = torch.stack([nfft_type1_direct(g, self.truth[k], P) for k, g in enumerate(self.grids)])
+
+    def errors(self, k: int, x) -> torch.Tensor:
+        """Device scalar ||truth_k - x|| / ||truth_k||."""
+        x = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x))
+        return torch.linalg.vector_norm(self.truth[k] - x.to(self.truth.device)) / self.truth_norm[k]
 
 
-def _row(p, eta, mu, method, trial, err, counter, cg_iters, seed) -> TrialResult:
-    return TrialResult(p, eta, mu, method, trial, err, to_db(err), counter.report().total_flops, cg_iters, seed)
+def _charged(fn) -> int:
+    c = FlopCounter()
+    fn(c)
+    return c.report().total_flops
+
+
+def _fast_cells(size: _Size, cfg: TrialConfig, want_plain: bool, want_refined: bool):
+    """Cell-major fast methods: (cells, errors [cells, trials, 2] on the host, ok mask, flops)."""
+    P, T = size.P, len(size.seeds)
+    cells = []
+    for eta in cfg.eta:
+        for mu in cfg.mu:
+            try:
+                params = MethodParams.from_mu(mu, P, eta, spread_width=cfg.spread_width,
+                                              refine_passes=cfg.refine_passes)
+            except NonPositiveDampingError:
+                continue  # no damping needed at this truncation: the reference records nothing
+            cells.append((eta, mu, params))
+    err = torch.full((len(cells), T, 2), float("nan"), dtype=torch.float64, device=size.truth.device)
+    ok = np.zeros((len(cells), T, 2), dtype=bool)
+    flops = {}
+    for ci, (eta, mu, params) in enumerate(cells):
+        taps = 2 * params.spread_width + 1
+        plan_flops = _charged(lambda c: charge_plan(c, P, params))
+        flops[("nfft", ci)] = plan_flops + _charged(lambda c: charge_type4(c, P, taps))
+        flops[("rnfft", ci)] = plan_flops + _charged(lambda c: charge_refine(c, 4, P, taps, cfg.refine_passes))
+        for k, grid in enumerate(size.grids):
+            plan = build_plan(grid, params)
+            if want_plain:
+                err[ci, k, 0] = size.errors(k, type4(plan, size.spectrum[k]))
+                ok[ci, k, 0] = True
+            if want_refined:
+                try:
+                    x = refine_type4(plan, size.spectrum[k], passes=cfg.refine_passes)
+                except NonConvergenceError:
+                    continue  # residual grew between passes: no record (reference bench.py:196-199)
+                err[ci, k, 1] = size.errors(k, x)
+                ok[ci, k, 1] = True
+    return cells, err.cpu().numpy(), ok, flops
 
 
 def run_sweep(config: TrialConfig) -> list[TrialResult]:
-    """Every (P, trial, method, eta, mu) combination of the config (bench.py:127-214)."""
-    out: list[TrialResult] = []
+    """Every (P, trial, method, eta, mu) record of the config, in the reference's order
+    (per P, per trial: GE, CG, then per (eta, mu): NFFT, R-NFFT)."""
     if METHOD_GE in config.methods and max(config.p) > GE_SIZE_CAP:
         raise ValueError(f"GE requested above the P = {GE_SIZE_CAP} dense-solver cap")
-    fast = [m for m in (METHOD_NFFT, METHOD_RNFFT) if m in config.methods]
+    want_plain, want_refined = METHOD_NFFT in config.methods, METHOD_RNFFT in config.methods
+    records: list[TrialResult] = []
     with warnings.catch_warnings():
         warnings.simplefilter("ignore", AmplificationWarning)
         for P in config.p:
-            for trial in range(config.trials):
-                tseed = config.seed ^ trial
-                grid, a_np = generate_trial(P, tseed, config.jitter_max)
-                truth = torch.from_numpy(a_np).cuda()
-                spectrum = nfft_type1_direct(grid, truth, P)  # exact, on the device
+            size = _Size(P, config)
+            if float(size.truth_norm.min()) == 0.0:
+                raise ZeroReferenceError("relative error undefined: reference vector is zero")
+            dense = {}
+            for k, grid in enumerate(size.grids):
                 if METHOD_GE in config.methods:
                     c = FlopCounter()
-                    x = ge_solve(type4_system(grid, spectrum.cpu().numpy(), flops=c), flops=c)
-                    out.append(_row(P, None, None, METHOD_GE, trial, relative_error(a_np, x), c, None, tseed))
+                    x = ge_solve(type4_system(grid, size.spectrum[k].cpu().numpy(), flops=c), flops=c)
+                    dense[(k, METHOD_GE)] = (size.errors(k, x), c.report().total_flops, None)
                 if METHOD_CG in config.methods:
                     c = FlopCounter()
-                    res = cg_solve(grid, spectrum, "type4", tol=config.cg_tol, spread_width=config.spread_width,
-                                   flops=c)
-                    out.append(_row(P, None, None, METHOD_CG, trial, _device_error(truth, res.solution), c,
-                                    res.iterations, tseed))
-                if not fast:
-                    continue
-                for eta in config.eta:
-                    for mu in config.mu:
-                        try:
-                            params = MethodParams.from_mu(mu, P, eta, spread_width=config.spread_width,
-                                                          refine_passes=config.refine_passes)
-                        except NonPositiveDampingError:
-                            continue
-                        pc = FlopCounter()
-                        plan = build_plan(grid, params, flops=pc)
-                        if METHOD_NFFT in config.methods:
-                            c = FlopCounter()
-                            c.merge(pc)
-                            x = type4(plan, spectrum, flops=c)
-                            out.append(_row(P, eta, mu, METHOD_NFFT, trial, _device_error(truth, x), c, None,
-                                            tseed))
-                        if METHOD_RNFFT in config.methods:
-                            c = FlopCounter()
-                            c.merge(pc)
-                            try:
-                                x = refine_type4(plan, spectrum, passes=config.refine_passes, flops=c)
-                            except NonConvergenceError:
-                                continue
-                            out.append(_row(P, eta, mu, METHOD_RNFFT, trial, _device_error(truth, x), c, None,
-                                            tseed))
-    return out
+                    res = cg_solve(grid, size.spectrum[k], "type4", tol=config.cg_tol,
+                                   spread_width=config.spread_width, flops=c)
+                    dense[(k, METHOD_CG)] = (size.errors(k, res.solution), c.report().total_flops, res.iterations)
+            cells, err, ok, flops = ([], None, None, {})
+            if want_plain or want_refined:
+                cells, err, ok, flops = _fast_cells(size, config, want_plain, want_refined)
+            # one read-back of the dense errors, then the records in the reference's order
+            dense_err = {key: float(v[0]) for key, v in dense.items()}
+            for k, seed in enumerate(size.seeds):
+                for m in _DENSE:
+                    if (k, m) in dense:
+                        e = dense_err[(k, m)]
+                        records.append(TrialResult(P, None, None, m, k, e, to_db(e), dense[(k, m)][1],
+                                                   dense[(k, m)][2], seed))
+                for ci, (eta, mu, _) in enumerate(cells):
+                    for slot, m, fk in ((0, METHOD_NFFT, "nfft"), (1, METHOD_RNFFT, "rnfft")):
+                        if ok[ci, k, slot]:
+                            e = float(err[ci, k, slot])
+                            records.append(TrialResult(P, eta, mu, m, k, e, to_db(e), flops[(fk, ci)], None, seed))
+    return records
 
 
 def best_mu(results: list[TrialResult], method: str) -> dict[tuple[int, int], float]:
-    """Per-(P, eta) mu minimising the mean error over trials (bench.py:217-231)."""
-    groups: dict[tuple[int, int, float], list[float]] = {}
+    """Per-(P, eta) mu with the smallest mean error over trials (reference bench.py:217-231);
+    ties keep the first mu met."""
+    by_cell: dict[tuple[int, int], dict[float, list[float]]] = {}
     for r in results:
         if r.method == method and r.mu is not None:
-            groups.setdefault((r.p, r.eta, r.mu), []).append(r.error_linear)
-    best: dict[tuple[int, int], tuple[float, float]] = {}
-    for (p, eta, mu), errs in groups.items():
-        mean = sum(errs) / len(errs)
-        if (p, eta) not in best or mean < best[(p, eta)][0]:
-            best[(p, eta)] = (mean, mu)
-    return {k: mu for k, (_, mu) in best.items()}
+            by_cell.setdefault((r.p, r.eta), {}).setdefault(r.mu, []).append(r.error_linear)
+    winners = {}
+    for key, per_mu in by_cell.items():
+        means = [(sum(v) / len(v), mu) for mu, v in per_mu.items()]
+        best = means[0]
+        for cand in means[1:]:
+            if cand[0] < best[0]:
+                best = cand
+        winners[key] = best[1]
+    return winners
 
 
 def filter_best_mu(results: list[TrialResult], method: str) -> list[TrialResult]:
-    """Dense-solver rows plus the best-mu rows of `method` (bench.py:234-243)."""
+    """Dense-solver records plus `method`'s records at its best mu (reference bench.py:234-243)."""
     winners = best_mu(results, method)
-    return [r for r in results
-            if r.mu is None or (r.method == method and winners.get((r.p, r.eta)) == r.mu)]
+    return [r for r in results if r.mu is None or (r.method == method and winners.get((r.p, r.eta)) == r.mu)]
 
 
-# fig1: error floor vs mu for several eta at P = 1024; fig2: the refined
-# method; fig3: refined method vs P at best mu; fig6: flop totals vs P;
-# fig7: flop totals vs eta (bench.py:246-275).
+# Figure protocols (reference bench.py:246-275): fig1 error floor vs mu at
+# several eta (P = 1024); fig2 the refined method at eta 1, 2; fig3 refined
+# method vs P at its best mu; fig6 flops vs P; fig7 flops vs eta.
+_FIG_DENSE_NFFT = (METHOD_GE, METHOD_CG, METHOD_NFFT)
+_FIG_DENSE_RNFFT = (METHOD_GE, METHOD_CG, METHOD_RNFFT)
 FIGURE_DEFAULTS: dict[str, TrialConfig] = {
-    "fig1": TrialConfig(p=(1024,), eta=(1, 2, 3, 4, 6, 15, 20), methods=(METHOD_GE, METHOD_CG, METHOD_NFFT)),
-    "fig2": TrialConfig(p=(1024,), eta=(1, 2), methods=(METHOD_GE, METHOD_CG, METHOD_RNFFT)),
-    "fig3": TrialConfig(p=(64, 128, 256, 512, 1024, 2048, 4096, 8192), eta=(1,),
-                        methods=(METHOD_GE, METHOD_CG, METHOD_RNFFT)),
-    "fig6": TrialConfig(p=(64, 128, 256, 512, 1024), eta=(6,), mu=(1e-15,),
-                        methods=(METHOD_GE, METHOD_CG, METHOD_NFFT)),
-    "fig7": TrialConfig(p=(1024,), eta=tuple(range(1, 21)), mu=(1e-15,), methods=(METHOD_GE, METHOD_CG, METHOD_NFFT)),
+    "fig1": TrialConfig(p=(1024,), eta=(1, 2, 3, 4, 6, 15, 20), methods=_FIG_DENSE_NFFT),
+    "fig2": TrialConfig(p=(1024,), eta=(1, 2), methods=_FIG_DENSE_RNFFT),
+    "fig3": TrialConfig(p=tuple(64 << k for k in range(8)), eta=(1,), methods=_FIG_DENSE_RNFFT),
+    "fig6": TrialConfig(p=tuple(64 << k for k in range(5)), eta=(6,), mu=(1e-15,), methods=_FIG_DENSE_NFFT),
+    "fig7": TrialConfig(p=(1024,), eta=tuple(range(1, 21)), mu=(1e-15,), methods=_FIG_DENSE_NFFT),
 }
-
 DENSE_DEFAULT_CAP = 1024
 
 
 def run_figure(name: str, config: TrialConfig | None = None, dense_cap: int | None = None):
-    """One figure protocol -> (records, metadata) (bench.py:282-301)."""
+    """(records, metadata) of one figure protocol (reference bench.py:282-301): dense
+    solvers only up to `dense_cap`; fig6 adds the refined method at eta = 1, mu = 1e-8;
+    fig2 / fig3 keep the refined method's best-mu records."""
     if name not in FIGURE_DEFAULTS:
         raise ValueError(f"unknown figure {name!r}; choose from {sorted(FIGURE_DEFAULTS)}")
-    cfg = config if config is not None else FIGURE_DEFAULTS[name]
+    cfg = FIGURE_DEFAULTS[name] if config is None else config
     cap = DENSE_DEFAULT_CAP if dense_cap is None else dense_cap
-    dense = tuple(m for m in cfg.methods if m in (METHOD_GE, METHOD_CG))
-    fast_only = tuple(m for m in cfg.methods if m not in (METHOD_GE, METHOD_CG))
-    results: list[TrialResult] = []
+    fast_only = tuple(m for m in cfg.methods if m not in _DENSE)
+    records: list[TrialResult] = []
     for P in cfg.p:
         methods = cfg.methods if P <= cap else fast_only
         if methods:
-            results.extend(run_sweep(replace(cfg, p=(P,), methods=methods)))
-    if name == "fig6":  # + the refined method at eta = 1 on the same trials
-        results.extend(run_sweep(replace(cfg, eta=(1,), mu=(1e-8,), methods=(METHOD_RNFFT,), p=tuple(cfg.p))))
+            records += run_sweep(replace(cfg, p=(P,), methods=methods))
+    if name == "fig6":
+        records += run_sweep(replace(cfg, eta=(1,), mu=(1e-8,), methods=(METHOD_RNFFT,)))
     if name in ("fig2", "fig3"):
-        results = filter_best_mu(results, METHOD_RNFFT)
-    meta = {
-        "figure": name,
-        "seed": cfg.seed,
-        "trials": cfg.trials,
-        "jitter_max": cfg.jitter_max,
-        "db_convention": "20*log10(relative_l2_error)",
-        "rng": "philox(key=seed^trial)",
-        "dense_cap": cap if dense else None,
-    }
-    return results, meta
+        records = filter_best_mu(records, METHOD_RNFFT)
+    has_dense = any(m in _DENSE for m in cfg.methods)
+    meta = {"figure": name, "seed": cfg.seed, "trials": cfg.trials, "jitter_max": cfg.jitter_max,
+            "db_convention": "20*log10(relative_l2_error)", "rng": "philox(key=seed^trial)",
+            "dense_cap": cap if has_dense else None}
+    return records, meta

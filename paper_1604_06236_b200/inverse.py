@@ -164,6 +164,33 @@ def _charge_type5(f, P, taps):
     f.real_mul(2 * P)
 
 
+def charge_refine(f, kind: int, P: int, taps: int, passes: int):
+    """Data-independent flop charge of refine_type5/4 (inverse.py:146-202): the
+    solve, then per pass one forward NFFT, the residual subtraction and the
+    correction solve."""
+    if f is None:
+        return
+    solve = _charge_type5 if kind == 5 else _charge_type4
+    solve(f, P, taps)
+    for _ in range(passes):
+        if kind == 5:
+            _fl.charge_type2(f, P, P, taps)
+        else:
+            _fl.charge_type1(f, P, P, taps)
+        f.complex_add(2 * P)
+        solve(f, P, taps)
+
+
+def charge_plan(f, P: int, params: MethodParams):
+    """Data-independent flop charge of build_plan (lagrange.py:57-164, inverse.py:79-86)."""
+    _charge_plan(f, P, params)
+
+
+def charge_type4(f, P: int, taps: int):
+    """Data-independent flop charge of type4 (inverse.py:136-142)."""
+    _charge_type4(f, P, taps)
+
+
 def _charge_type4(f, P, taps):
     if f is None:
         return
@@ -267,13 +294,7 @@ def refine_type4(plan: InversePlan, spectrum, passes: int | None = None, flops: 
         passes = plan.params.refine_passes
     # a negative count runs no pass, like the reference's range(passes) (inverse.py:150)
     out = _solve("type4", plan, spectrum, "spectrum", max(int(passes), 0), out, non_blocking)
-    P, taps = plan.size, plan.kernel_base.taps
-    _charge_type4(flops, P, taps)
-    for _ in range(passes):
-        if flops is not None:
-            _fl.charge_type1(flops, P, P, taps)
-            flops.complex_add(2 * P)
-        _charge_type4(flops, P, taps)
+    charge_refine(flops, 4, plan.size, plan.kernel_base.taps, passes)
     return out
 
 
@@ -284,11 +305,5 @@ def refine_type5(plan: InversePlan, samples, passes: int | None = None, flops: F
         passes = plan.params.refine_passes
     # a negative count runs no pass, like the reference's range(passes) (inverse.py:150)
     out = _solve("type5", plan, samples, "samples", max(int(passes), 0), out, non_blocking)
-    P, taps = plan.size, plan.kernel_base.taps
-    _charge_type5(flops, P, taps)
-    for _ in range(passes):
-        if flops is not None:
-            _fl.charge_type2(flops, P, P, taps)
-            flops.complex_add(2 * P)
-        _charge_type5(flops, P, taps)
+    charge_refine(flops, 5, plan.size, plan.kernel_base.taps, passes)
     return out

@@ -123,3 +123,18 @@ def test_oracle_phase_matrix_and_dense_solve(golden):
     assert rel(golden["ge32_x"], O.dense_solve(M, golden["ge32_b"])) < 1e-12
     for name in ("cg4", "cg5"):  # CG converged to the dense solution
         assert rel(golden[f"{name}_ge"], golden[f"{name}_x"]) < 1e-10
+
+
+def test_harness_trial_streams_bitwise_equal_reference():
+    """metrics.trial_arrays reproduces the reference's generate_trial streams
+    (bench.py:84-92) bit for bit (golden: oracle/make_sweep_golden.py)."""
+    import json
+    import os
+
+    from paper_1604_06236_b200.metrics import trial_arrays
+
+    g = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "sweep_rows.json")))
+    for c in g["trial_streams"]:
+        t, a = trial_arrays(c["P"], c["seed"])
+        assert np.array_equal(t, np.array(c["nodes"]))
+        assert np.array_equal(a.real, np.array(c["re"])) and np.array_equal(a.imag, np.array(c["im"]))
