@@ -188,8 +188,10 @@ def test_multi_pass_sweep_skips_diverging_cells():
 # the same records in the same order (the reference's trial streams are
 # reproduced bit for bit), the same data-independent flop totals, CG
 # iteration counts within 2, and errors at the reference's level: never more
-# than 2x above it, and within 2x of it wherever the method's own error
-# dominates (>= 1e-11).  The one allowed difference: where the reference's
+# than 2x above it (in the roundoff-amplified cells — small mu, eta = 1 — this
+# path's exactly reduced phases are 10-100x MORE accurate than the
+# reference's), and within 10 % of it where the truncation error dominates
+# (plain solves at mu >= 1e-8).  The one allowed difference: where the reference's
 # two-pass refinement diverges (its plain error ~1) this path's more accurate
 # phases may still contract and then produce an R-NFFT record the reference
 # skipped.
@@ -235,6 +237,6 @@ def test_harness_rows_match_reference(case):
             assert o["total_flops"] == r["total_flops"], (o, r)
         e, er = o["error_linear"], r["error_linear"]
         assert e <= 2.0 * er + 1e-13, (o, r)
-        if er >= 1e-11:
-            assert e >= er / 2.0, (o, r)
+        if o["method"] == "NFFT" and o["mu"] >= 1e-8:
+            assert abs(e / er - 1.0) <= 0.1, (o, r)
         assert abs(o["error_db"] - 20.0 * math.log10(e)) < 1e-9

