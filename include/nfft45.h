@@ -248,6 +248,21 @@ int nfft45_solve_host(const nfft45_plan* p, int kind, int passes, const double* 
                       int64_t batch, double* out_host, int64_t chunk, int blocking,
                       void* stream);
 
+/* nfft45_solve_host with flags.  Pageable operands (ordinary numpy / malloc
+ * memory, detected with cudaPointerGetAttributes) are staged through pinned
+ * library buffers by a pool of host copy threads, overlapped with the device
+ * work of the neighbouring chunks; such calls always block.
+ *   NFFT45_HOST_CHECK_FINITE: scan every staged input chunk on the device and
+ *     return NFFT45_ERR_INVALID_ARGUMENT ("operand contains NaN or Inf
+ *     entries") if any entry is not finite (grid.py:30-31 as_complex_vector);
+ *     the output is then unspecified.  Pageable path only.
+ *   NFFT45_HOST_NO_STAGING: copy pageable operands directly (A/B runs). */
+#define NFFT45_HOST_CHECK_FINITE 1
+#define NFFT45_HOST_NO_STAGING 2
+int nfft45_solve_host_ex(const nfft45_plan* p, int kind, int passes, const double* in_host,
+                         int64_t batch, double* out_host, int64_t chunk, int blocking, int flags,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

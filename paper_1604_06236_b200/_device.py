@@ -100,9 +100,11 @@ def operand(values, dev: int, length: int | None = None, name: str = "vector") -
     return Operand(t, False, arr.ndim == 2)
 
 
-def host_array(values, length: int | None = None, name: str = "vector") -> np.ndarray:
+def host_array(values, length: int | None = None, name: str = "vector", check_finite: bool = True) -> np.ndarray:
     """Coerce array-like `values` to a contiguous complex128 numpy array with the
-    reference's checks (grid.py:21-32: 1-D, nonempty, finite; [batch, P] allowed)."""
+    reference's checks (grid.py:21-32: 1-D, nonempty, finite; [batch, P] allowed).
+    check_finite=False leaves the finiteness check to the caller (the host
+    pipeline scans the staged chunks on the device)."""
     arr = np.asarray(values, dtype=np.complex128)
     if arr.ndim not in (1, 2):
         raise LengthMismatchError(f"{name} must be one-dimensional, got shape {arr.shape}")
@@ -110,7 +112,7 @@ def host_array(values, length: int | None = None, name: str = "vector") -> np.nd
         raise LengthMismatchError(f"{name} must be nonempty")
     if length is not None and arr.shape[-1] != length:
         raise LengthMismatchError(f"{name} has length {arr.shape[-1]}, expected {length}")
-    if not np.isfinite(arr).all():
+    if check_finite and not np.isfinite(arr).all():
         raise ValueError(f"{name} contains NaN or Inf entries")
     arr = np.ascontiguousarray(arr)
     if not arr.flags.writeable:

@@ -66,6 +66,8 @@ _SIGS = {
                                            ctypes.c_void_p]),
     "nfft45_solve_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, _i64,
                                          ctypes.c_void_p, _i64, ctypes.c_int, ctypes.c_void_p]),
+    "nfft45_solve_host_ex": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, _i64,
+                                            ctypes.c_void_p, _i64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
     "nfft45_ge_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _i64, ctypes.c_void_p, ctypes.c_double,
                                        ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]),
     "nfft45_cg_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, _i64, ctypes.c_double, _i64,

@@ -1,7 +1,10 @@
 // nfft45.cu — C ABI (include/nfft45.h): node sets, forward NFFTs, Lagrange
 // quantities, inverse plans and the type-4/5 solves with refinement.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -1234,6 +1237,12 @@ struct HostPipe {
   double2* bout[2] = {};
   int64_t cap = 0;  // elements per staging slot
   int64_t turn = 0;  // staging slot of the next call's first chunk
+  // pageable operands (numpy arrays): pinned host staging slots filled / drained
+  // by the copy pool, and a device flag for the non-finite input check
+  double2* hin[2] = {};
+  double2* hout[2] = {};
+  int64_t hcap = 0;
+  int* d_flag = nullptr;
   std::set<const nfft45_plan*> plans;
   std::mutex mu;
 };
@@ -1286,6 +1295,123 @@ int pipe_reserve(HostPipe* hp, int64_t elems) {
   hp->cap = elems;
   return NFFT45_OK;
 }
+
+int pipe_reserve_host(HostPipe* hp, int64_t elems) {
+  if (!hp->d_flag) NFFT_CUDA(cudaMalloc(&hp->d_flag, sizeof(int)));
+  if (hp->hcap >= elems) return NFFT45_OK;
+  for (cudaStream_t s : {hp->h2d, hp->comp, hp->d2h}) NFFT_CUDA(cudaStreamSynchronize(s));
+  for (int k = 0; k < 2; k++) {
+    cudaFreeHost(hp->hin[k]);
+    cudaFreeHost(hp->hout[k]);
+    hp->hin[k] = hp->hout[k] = nullptr;
+  }
+  hp->hcap = 0;
+  for (int k = 0; k < 2; k++) {
+    NFFT_CUDA(cudaHostAlloc(&hp->hin[k], sizeof(double2) * elems, cudaHostAllocDefault));
+    NFFT_CUDA(cudaHostAlloc(&hp->hout[k], sizeof(double2) * elems, cudaHostAllocDefault));
+  }
+  hp->hcap = elems;
+  return NFFT45_OK;
+}
+
+// Host memcpy across a small pool of threads (pageable <-> pinned staging):
+// one job at a time, split in >= 1 MiB parts; the caller works too.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  void copy(void* dst, const void* src, size_t bytes) {
+    const size_t part = std::max<size_t>(size_t(1) << 20, (bytes + nth_) / (nth_ + 1));
+    const int nparts = (int)((bytes + part - 1) / part);
+    if (nparts <= 1 || th_.empty()) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    std::lock_guard<std::mutex> job(job_mu_);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      d_ = static_cast<char*>(dst);
+      s_ = static_cast<const char*>(src);
+      n_ = bytes;
+      part_ = part;
+      nparts_ = nparts;
+      next_.store(0);
+      finished_.store(0);
+      gen_++;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return finished_.load() == nparts_; });
+  }
+
+ private:
+  CopyPool() {
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    nth_ = (int)std::min(7u, hw / 2);
+    if (const char* e = getenv("NFFT45_COPY_THREADS")) nth_ = std::max(0, atoi(e) - 1);
+    for (int i = 0; i < nth_; i++) th_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void work() {
+    for (int i; (i = next_.fetch_add(1)) < nparts_;) {
+      const size_t off = (size_t)i * part_;
+      std::memcpy(d_ + off, s_ + off, std::min(part_, n_ - off));
+      if (finished_.fetch_add(1) + 1 == nparts_) {
+        std::lock_guard<std::mutex> lk(mu_);
+        done_cv_.notify_all();
+      }
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  int nth_ = 0;
+  std::vector<std::thread> th_;
+  std::mutex job_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  char* d_ = nullptr;
+  const char* s_ = nullptr;
+  size_t n_ = 0, part_ = 0;
+  int nparts_ = 0;
+  std::atomic<int> next_{0}, finished_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+__global__ void k_nonfinite(const double* __restrict__ x, int64_t n, int* __restrict__ flag) {
+  int bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+bool is_pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
 }  // namespace
 
 void host_pipes_forget(const nfft45_plan* p) {
@@ -1297,8 +1423,84 @@ void host_pipes_forget(const nfft45_plan* p) {
 }
 }  // namespace nfft45
 
+namespace nfft45 {
+// Pageable operands: chunk i's input is copied (thread pool) into a pinned
+// staging slot while the device works on chunk i-1, uploaded, solved and
+// downloaded into the pinned output slot, then copied out to the caller's
+// array while chunk i+1 is in flight.  Always blocking (the results are on
+// the host when the call returns).
+static int solve_host_pageable(const nfft45_plan* p, HostPipe* hp, int kind, int passes, const double2* src,
+                               int64_t batch, double2* dst, int64_t chunk, bool check_finite) {
+  const int64_t P = p->P;
+  NFFT_CHECK(pipe_reserve_host(hp, chunk * P));
+  if (check_finite) NFFT_CUDA(cudaMemsetAsync(hp->d_flag, 0, sizeof(int), hp->comp));
+  CopyPool& pool = CopyPool::get();
+  int status = NFFT45_OK;
+  int64_t prev_lo = -1, prev_m = 0;
+  int prev_k = 0;
+  auto drain = [&]() -> int {  // copy the previous chunk's results out to the caller
+    if (prev_lo < 0) return NFFT45_OK;
+    NFFT_CUDA(cudaEventSynchronize(hp->drained[prev_k]));
+    pool.copy(dst + prev_lo * P, hp->hout[prev_k], sizeof(double2) * prev_m * P);
+    prev_lo = -1;
+    return NFFT45_OK;
+  };
+  for (int64_t lo = 0, i = 0; lo < batch; lo += chunk, i++) {
+    const int k = (int)(i & 1);
+    const int64_t m = std::min(chunk, batch - lo);
+    const size_t bytes = sizeof(double2) * m * P;
+    NFFT_CUDA(cudaEventSynchronize(hp->loaded[k]));  // pinned slot k uploaded (chunk i-2)
+    pool.copy(hp->hin[k], src + lo * P, bytes);
+    NFFT_CUDA(cudaStreamWaitEvent(hp->h2d, hp->done[k], 0));  // device slot k's input consumed
+    NFFT_CUDA(cudaMemcpyAsync(hp->bin[k], hp->hin[k], bytes, cudaMemcpyHostToDevice, hp->h2d));
+    NFFT_CUDA(cudaEventRecord(hp->loaded[k], hp->h2d));
+    NFFT_CUDA(cudaStreamWaitEvent(hp->comp, hp->loaded[k], 0));
+    NFFT_CUDA(cudaStreamWaitEvent(hp->comp, hp->drained[k], 0));
+    const double* bi = reinterpret_cast<const double*>(hp->bin[k]);
+    double* bo = reinterpret_cast<double*>(hp->bout[k]);
+    if (check_finite) {
+      const int64_t nd = 2 * m * P;
+      LAUNCH(k_nonfinite, (unsigned)std::min<int64_t>(ceil_div(nd, 256), 2 * 148 * 8), 256, 0, hp->comp, bi, nd,
+             hp->d_flag);
+    }
+    if (passes < 0)
+      status = kind == 5 ? nfft45_type5(p, bi, m, bo, hp->comp) : nfft45_type4(p, bi, m, bo, hp->comp);
+    else
+      status = kind == 5 ? nfft45_refine_type5(p, bi, m, passes, bo, hp->comp)
+                         : nfft45_refine_type4(p, bi, m, passes, bo, hp->comp);
+    NFFT_CUDA(cudaEventRecord(hp->done[k], hp->comp));
+    if (status != NFFT45_OK) break;
+    NFFT_CUDA(cudaStreamWaitEvent(hp->d2h, hp->done[k], 0));
+    NFFT_CUDA(cudaMemcpyAsync(hp->hout[k], hp->bout[k], bytes, cudaMemcpyDeviceToHost, hp->d2h));
+    NFFT_CUDA(cudaEventRecord(hp->drained[k], hp->d2h));
+    NFFT_CHECK(drain());
+    prev_lo = lo;
+    prev_m = m;
+    prev_k = k;
+  }
+  if (status != NFFT45_OK) {
+    cudaStreamSynchronize(hp->comp);
+    return status;
+  }
+  NFFT_CHECK(drain());
+  if (check_finite) {
+    int flag = 0;
+    NFFT_CUDA(cudaMemcpyAsync(&flag, hp->d_flag, sizeof(int), cudaMemcpyDeviceToHost, hp->comp));
+    NFFT_CUDA(cudaStreamSynchronize(hp->comp));
+    if (flag) return fail(NFFT45_ERR_INVALID_ARGUMENT, "operand contains NaN or Inf entries");
+  }
+  return NFFT45_OK;
+}
+}  // namespace nfft45
+
 extern "C" int nfft45_solve_host(const nfft45_plan* p, int kind, int passes, const double* in_host,
                                  int64_t batch, double* out_host, int64_t chunk, int blocking, void* stream) {
+  return nfft45_solve_host_ex(p, kind, passes, in_host, batch, out_host, chunk, blocking, 0, stream);
+}
+
+extern "C" int nfft45_solve_host_ex(const nfft45_plan* p, int kind, int passes, const double* in_host,
+                                    int64_t batch, double* out_host, int64_t chunk, int blocking, int flags,
+                                    void* stream) {
   using namespace nfft45;
   if (!p || (kind != 4 && kind != 5) || batch < 1 || !in_host || !out_host || passes < -1)
     return fail(NFFT45_ERR_INVALID_ARGUMENT, "invalid host solve arguments");
@@ -1311,6 +1513,7 @@ extern "C" int nfft45_solve_host(const nfft45_plan* p, int kind, int passes, con
   NFFT_CHECK(pipe_get(p->g->d.device, user, &hp));
   std::lock_guard<std::mutex> lk(hp->mu);
   NFFT_CHECK(pipe_reserve(hp, chunk * P));
+  const bool pageable = !(flags & NFFT45_HOST_NO_STAGING) && (is_pageable(in_host) || is_pageable(out_host));
   cudaEvent_t entry = nullptr, fin = nullptr;
   NFFT_CUDA(cudaEventCreateWithFlags(&entry, cudaEventDisableTiming));
   NFFT_CUDA(cudaEventRecord(entry, user));
@@ -1333,6 +1536,21 @@ extern "C" int nfft45_solve_host(const nfft45_plan* p, int kind, int passes, con
   const double2* src = reinterpret_cast<const double2*>(in_host);
   double2* dst = reinterpret_cast<double2*>(out_host);
   int status = NFFT45_OK;
+  if (pageable) {
+    struct NoGraph {
+      bool prev;
+      explicit NoGraph(bool on) : prev(tl_host_pipe_no_graph) { tl_host_pipe_no_graph = on; }
+      ~NoGraph() { tl_host_pipe_no_graph = prev; }
+    } ng(chunk * P >= (int64_t(1) << 16));
+    status = solve_host_pageable(p, hp, kind, passes, src, batch, dst, chunk, (flags & NFFT45_HOST_CHECK_FINITE) != 0);
+    cudaEvent_t done_ev = nullptr;
+    NFFT_CUDA(cudaEventCreateWithFlags(&done_ev, cudaEventDisableTiming));
+    NFFT_CUDA(cudaEventRecord(done_ev, hp->d2h));
+    NFFT_CUDA(cudaStreamWaitEvent(user, done_ev, 0));
+    cudaEventDestroy(done_ev);
+    cudaEventDestroy(entry);
+    return status;
+  }
   // A call's first chunk takes the slot the previous call's last solve is not
   // using, so its upload overlaps that solve.  Chunks of at least 2^16 points
   // run without the CUDA-graph cache here: next to the pipeline's copies the

@@ -211,6 +211,9 @@ STREAM_CHUNK = int(os.environ.get("NFFT45_STREAM_CHUNK", "64"))
 # single chunk, so a call's upload overlaps the previous call's solve and
 # download (NFFT45_PIPE_MIN_BYTES overrides, for A/B runs).
 PIPE_MIN_BYTES = int(os.environ.get("NFFT45_PIPE_MIN_BYTES", "0"))
+# numpy operands: device-side finiteness check; NFFT45_NO_STAGING=1 copies
+# pageable memory directly instead of through the pinned staging slots (A/B)
+HOST_FLAGS = 1 | (2 if os.environ.get("NFFT45_NO_STAGING") else 0)
 
 
 def _solve_streamed(name: str, plan: InversePlan, host, passes, dest, non_blocking: bool = False):
@@ -242,11 +245,18 @@ def _solve(name: str, plan: InversePlan, data, label: str, passes: int | None, d
     if not isinstance(data, torch.Tensor) and dest is None:
         # the reference's convention (array-like in host memory -> numpy out):
         # validated here, solved through the native host pipeline
-        arr = _device.host_array(data, plan.size, label)
+        # (the finiteness check of as_complex_vector, grid.py:30-31, runs on the
+        # device over the staged chunks: no extra host pass over the operand)
+        arr = _device.host_array(data, plan.size, label, check_finite=False)
         res = np.empty_like(arr)
-        _lib.call("nfft45_solve_host", plan.handle, 5 if name == "type5" else 4, -1 if passes is None else int(passes),
-                  arr.ctypes.data, arr.size // plan.size, res.ctypes.data, STREAM_CHUNK, 1,
-                  _device.stream_handle(plan.device))
+        try:
+            _lib.call("nfft45_solve_host_ex", plan.handle, 5 if name == "type5" else 4,
+                      -1 if passes is None else int(passes), arr.ctypes.data, arr.size // plan.size,
+                      res.ctypes.data, STREAM_CHUNK, 1, HOST_FLAGS, _device.stream_handle(plan.device))
+        except ValueError as exc:
+            if "NaN or Inf" in str(exc):
+                raise ValueError(f"{label} contains NaN or Inf entries") from None
+            raise
         return res
     if (isinstance(data, torch.Tensor) and not data.is_cuda and data.dim() in (1, 2) and data.numel() > 0
             and data.shape[-1] == plan.size
