@@ -28,6 +28,7 @@
 
 #include "fft_fast.cuh"
 #include "ops.cuh"
+#include "tma.cuh"
 
 namespace nfft45 {
 
@@ -292,6 +293,145 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
   }
 }
 
+// First-pass hook of the TMA-staged kernels: wait for the cp.async table
+// copies before the barrier; after it (every thread has read the tile) thread
+// 0 refills the buffer with the CTA's next tile of ROWS rows.
+template <int ROWS, int SG>
+struct TmaNextTile {
+  static constexpr bool kActive = true;
+  static constexpr bool kOpaque = false;
+  const CUtensorMap* map;
+  double2* dst;
+  uint64_t* bar;
+  int tn, ntiles, groups;
+  __device__ __forceinline__ void operator()() const { asm volatile("cp.async.wait_all;\n" ::); }
+  __device__ __forceinline__ void after() const {
+    if (threadIdx.x == 0 && tn < ntiles) {
+      fence_proxy_async();  // the first pass's generic reads of the buffer precede the async refill
+      mbar_expect_tx(bar, (unsigned)(ROWS * SG * sizeof(double2)));
+      tma_load_2d(dst, map, 2 * SG * (tn % groups), ROWS * (tn / groups), bar);
+    }
+  }
+};
+
+// kbm_pad with a TMA-staged input tile: the tile's Z rows (C rows x 8
+// signals, 32 KB at C = 256) are brought into shared memory by ONE
+// cp.async.bulk.tensor issued by thread 0 (SASS UTMALDG, mbarrier
+// transaction count) instead of 16 LDGs per thread into registers; the
+// per-tile tables are staged with cp.async meanwhile.  Tile order as the
+// one-shot kernels (signal groups fastest).  Arithmetic and store order are
+// those of kbm_pad (bitwise identical results).
+//
+// A persistent variant that refills the buffer with the CTA's next tile
+// right after the first pass (so its DRAM latency hides under the current
+// tile) is possible with the TmaNextTile hook, but nvcc then spills
+// 1.2 KB/thread at the 128-register budget (the second tile's FFT keeps
+// values of the first live: measured with a runtime loop, `#pragma unroll 1`,
+// a two-tile unroll, laundered pointers and thread indices alike), so each
+// CTA handles one tile.
+struct PadTileArgs {
+  double2* Y;
+  int64_t Bp;
+  const double2 *twR, *twC, *loN, *hiN;
+  int sN;
+  const double2* twQ;
+  int Q;
+  const double *coef, *deconv, *cd;
+  double2* xout;
+  int ntiles, groups;
+};
+
+template <int R, int C, int SG>
+__device__ __forceinline__ void pad_tile(const PadTileArgs& a, const CUtensorMap* tmZ, double2* sm, double2* inb,
+                                      uint64_t* bar, int t) {
+  constexpr int NC = 2 * C;
+  constexpr bool kLead2 = FastTraits<NC>::radix(0) == 2;
+  double* s_t0 = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + fast_smem<NC, SG>());
+  double* s_t1 = s_t0 + C;
+  const int r = t / a.groups;
+  const int64_t b0 = (int64_t)(t % a.groups) * SG;
+  const unsigned ub = (unsigned)a.Bp;
+  double2* __restrict__ Yt = a.Y + (int64_t)r * a.Bp + b0;
+  double2* __restrict__ Xt = a.xout ? a.xout + (int64_t)r * a.Bp + b0 : nullptr;
+  const bool xo = a.xout != nullptr;
+  int tid0 = threadIdx.x;
+  asm volatile("" : "+r"(tid0));
+  for (int k2 = tid0; k2 < C; k2 += blockDim.x) {
+    const int64_t p = (int64_t)r + (int64_t)R * k2;
+    if (xo) {
+      cpa8(&s_t0[k2], &a.coef[p]);
+      cpa8(&s_t1[k2], &a.deconv[p]);
+    } else {
+      cpa8(&s_t0[k2], &a.cd[p]);
+    }
+  }
+  cpa_commit();
+  const TmaNextTile<C, SG> hook{tmZ, inb, bar, a.ntiles, a.ntiles, a.groups};  // no refill (one tile per CTA)
+  auto ld1 = [&](int i, int c) -> double2 { return inb[i * SG + c]; };
+  auto st1 = [&](int k2, int c, double2 v) {
+    if (xo) {
+      v = rsc(v, s_t0[k2]);
+      Xt[(unsigned)(R * k2) * ub + c] = v;
+      v = rsc(v, s_t1[k2]);
+    } else {
+      v = rsc(v, s_t0[k2]);
+    }
+    const int n1 = (k2 - C / 2) & (NC - 1);
+    if constexpr (kLead2) {
+      if (n1 < C) {
+        sm[sidx<NC, SG, true>(2 * n1, c)] = v;
+        sm[sidx<NC, SG, true>(2 * n1 + 1, c)] = v;
+      } else {
+        const int j = n1 - C;
+        sm[sidx<NC, SG, true>(2 * j, c)] = v;
+        sm[sidx<NC, SG, true>(2 * j + 1, c)] = make_double2(-v.x, -v.y);
+      }
+    } else {
+      sm[sidx<NC, SG, true>(n1, c)] = v;
+      sm[sidx<NC, SG, true>((n1 + C) & (NC - 1), c)] = make_double2(0.0, 0.0);
+    }
+  };
+  fast_tile_fft<C, SG, -1, true, HalfTr<C>>(sm, ld1, st1, a.twR, NoPostTw(), hook);
+  __syncthreads();
+  auto st2 = [&](int k, int c, double2 v) { Yt[(unsigned)(k * R) * ub + c] = v; };
+  const FourStepTw<+1> pt{a.loN, a.hiN, a.sN, a.twQ, a.Q, r, 0};
+  if constexpr (kLead2) {
+    fast_tile_fft_from<NC, SG, +1, true, 1, 2>(sm, st2, a.twC, pt, NoHookT<false>());
+  } else {
+    auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, SG, true>(i, c)]; };
+    fast_tile_fft_smem<NC, SG, +1, true>(sm, ld2, st2, a.twC, pt, NoHookT<false>());
+  }
+}
+
+template <int R, int C, int SG>
+__global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_threads<2 * C, SG>())) kbm_pad_t(
+    const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ PadTileArgs a) {
+  constexpr int NC = 2 * C;
+  constexpr unsigned kTileBytes = (unsigned)(C * SG * sizeof(double2));
+  extern __shared__ __align__(128) unsigned char smraw_t[];
+  double2* sm = reinterpret_cast<double2*>(smraw_t);
+  double* s_t1 = reinterpret_cast<double*>(smraw_t + fast_smem<NC, SG>()) + C;
+  double2* inb = reinterpret_cast<double2*>(
+      (reinterpret_cast<uintptr_t>(s_t1 + C) + 127) & ~uintptr_t(127));  // [C][SG] dense (TMA box)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(inb + C * SG);
+  int t = blockIdx.x;
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmZ);
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  pdl_enter();  // programmatic dependent launch: Z is the producer's output
+  if (threadIdx.x == 0 && t < a.ntiles) {
+    mbar_expect_tx(bar, kTileBytes);
+    tma_load_2d(inb, &tmZ, 2 * SG * (t % a.groups), C * (t / a.groups), bar);
+  }
+  if (t < a.ntiles) {
+    mbar_wait(bar, 0);
+    pad_tile<R, C, SG>(a, &tmZ, sm, inb, bar, t);
+  }
+}
+
 // row pass: row r = blockIdx.x (length L), output index r + R1 k.
 template <int L, int S>
 __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<L, kSig>())) kbm_row(const double2* __restrict__ in,
@@ -365,6 +505,36 @@ __global__ void __launch_bounds__(fast_threads<C, 4 * RW>(), bm_minb(fast_thread
 }
 
 // ------------------------------------------------------------ host side
+
+int tma_map_rows(CUtensorMap* map, const void* base, int64_t rows, int64_t Bp, int box_rows, int box_sig) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<Encode>(fn);
+  }();
+  if (!encode) {
+    set_error(NFFT45_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return NFFT45_ERR_CUDA;
+  }
+  const cuuint64_t gdim[2] = {(cuuint64_t)(2 * Bp), (cuuint64_t)rows};
+  const cuuint64_t gstride[1] = {(cuuint64_t)(Bp * sizeof(double2))};
+  const cuuint32_t box[2] = {(cuuint32_t)(2 * box_sig), (cuuint32_t)box_rows};
+  const cuuint32_t estride[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), gdim, gstride, box, estride,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error(NFFT45_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return NFFT45_ERR_CUDA;
+  }
+  return NFFT45_OK;
+}
 
 template <typename K>
 static int bm_attr(K kernel, size_t bytes) {
@@ -459,7 +629,39 @@ struct ChainBM {
            (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout, (int)sw, pf);
     return NFFT45_OK;
   }
+  // TMA-staged pad (C <= 256 with 8-signal tiles, no subtrahend tile: two
+  // CTAs per SM fit).  Opt-in (NFFT45_TMA=1): bitwise identical to kbm_pad
+  // but measured 1.5-2 % slower on the C4 step (bm_pad 3.82 -> 3.88 ms per
+  // step): one CTA per tile still waits for its own tile, and the persistent
+  // form that would hide that wait spills (see kbm_pad_t).
+  int pad_tma(const double2* Z, double2* Y, const ChainPlanView& pv, double2* xout) {
+    auto bm_pad = kbm_pad_t<R, C, kSig>;
+    const size_t smem = fast_smem<2 * C, kSig>() + 2 * sizeof(double) * C + 128 + sizeof(double2) * C * kSig + 16;
+    NFFT_CHECK(bm_attr(bm_pad, smem));
+    constexpr int T = fast_threads<2 * C, kSig>();
+    const int64_t Q = n / last_stride<2 * C>();
+    const double2* twQ = nullptr;
+    NFFT_CHECK(qtab(Q, &twQ));
+    CUtensorMap tm;
+    NFFT_CHECK(tma_map_rows(&tm, Z, P, Bp, C, kSig));
+    const int ntiles = (int)(R * groups);
+    static const int sms = [] {
+      int dev = 0, v = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+      return v;
+    }();
+    const int grid = ntiles;
+    (void)sms;
+    const PadTileArgs args{Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q,
+                           pv.coef, pv.deconv, pv.cd, xout, ntiles, (int)groups};
+    LAUNCH_PDL(bm_pad, grid, T, smem, st, tm, args);
+    return NFFT45_OK;
+  }
   int pad(const double2* Z, double2* Y, const ChainPlanView& pv, const double2* xsub, double2* xout) {
+    static const bool tma = getenv("NFFT45_TMA") != nullptr;
+    if constexpr (C <= 256 && SG == kSig)
+      if (tma && !small_tiles && !(xout && xsub)) return pad_tma(Z, Y, pv, xout);
     if (small_tiles || SG < kSig) return pad_g<kSig / 2>(Z, Y, pv, xsub, xout);  // always for C = 1024
     return pad_g<kSig>(Z, Y, pv, xsub, xout);
   }

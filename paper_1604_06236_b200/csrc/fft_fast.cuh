@@ -200,13 +200,26 @@ struct FourStepTw {
 // barrier: kernels that stage per-tile tables with cp.async at entry wait for
 // them here, so the copies overlap the first pass and are visible to the
 // last pass's storer.
-struct NoHook {
+// `after()` runs once more right after the first pass's barrier (every thread
+// has read its first-pass inputs): the TMA-staged kernels refill their input
+// buffer with the next tile there.
+// kOpaque: the tile FFT runs inside a persistent tile loop — every pass
+// launders the thread index through an empty asm, so nvcc cannot hoist the
+// per-pass thread-derived addresses out of the loop (live across tiles, they
+// spill).
+template <bool OPQ>
+struct NoHookT {
   static constexpr bool kActive = false;
+  static constexpr bool kOpaque = OPQ;
   __device__ __forceinline__ void operator()() const {}
+  __device__ __forceinline__ void after() const {}
 };
+using NoHook = NoHookT<false>;
 struct CpAsyncWaitHook {
   static constexpr bool kActive = true;
+  static constexpr bool kOpaque = false;
   __device__ __forceinline__ void operator()() const { asm volatile("cp.async.wait_all;\n" ::); }
+  __device__ __forceinline__ void after() const {}
 };
 
 // One pass; FIRST reads through `ld`, LAST writes through `st`.  Threads
@@ -224,7 +237,8 @@ __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St&
   constexpr int stride = N / R;
   constexpr bool FIRST = (P == 0);
   constexpr bool LAST = (P == Tr::np - 1);
-  const int tid = threadIdx.x;
+  int tid = threadIdx.x;
+  if constexpr (Hk::kOpaque) asm volatile("" : "+r"(tid));
   const bool active = tid < T;
   double2 v[MB][R];
   if (active) {
@@ -270,7 +284,8 @@ __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St&
   if constexpr (!LAST) {
     if constexpr (FIRST && Hk::kActive) hook();
     __syncthreads();
-    fast_passes<N, C, S, CF, SYNC0, P + 1, Ns * R, Tr>(sm, ld, st, tw, pt);
+    if constexpr (FIRST && Hk::kActive) hook.after();
+    fast_passes<N, C, S, CF, SYNC0, P + 1, Ns * R, Tr>(sm, ld, st, tw, pt, NoHookT<Hk::kOpaque>());
   }
 }
 
@@ -283,19 +298,21 @@ __device__ __forceinline__ void fast_tile_fft(double2* sm, const Ld& ld, const S
 
 // Variant whose first pass reads the tile from shared memory (via `ld`)
 // that later passes overwrite.
-template <int N, int C, int S, bool CF, class Tr = FastTraits<N>, class Ld, class St, class PT = NoPostTw>
+template <int N, int C, int S, bool CF, class Tr = FastTraits<N>, class Ld, class St, class PT = NoPostTw,
+          class Hk = NoHook>
 __device__ __forceinline__ void fast_tile_fft_smem(double2* sm, const Ld& ld, const St& st,
-                                                   const double2* __restrict__ tw, const PT& pt = PT()) {
-  fast_passes<N, C, S, CF, true, 0, 1, Tr>(sm, ld, st, tw, pt);
+                                                   const double2* __restrict__ tw, const PT& pt = PT(),
+                                                   const Hk& hook = Hk()) {
+  fast_passes<N, C, S, CF, true, 0, 1, Tr>(sm, ld, st, tw, pt, hook);
 }
 
 // Run passes P0.. of a tile FFT whose earlier passes were produced directly
 // in shared memory (Stockham layout after pass P0-1, Ns = NS0).
-template <int N, int C, int S, bool CF, int P0, int NS0, class St, class PT = NoPostTw>
+template <int N, int C, int S, bool CF, int P0, int NS0, class St, class PT = NoPostTw, class Hk = NoHook>
 __device__ __forceinline__ void fast_tile_fft_from(double2* sm, const St& st, const double2* __restrict__ tw,
-                                                   const PT& pt = PT()) {
+                                                   const PT& pt = PT(), const Hk& hook = Hk()) {
   auto no_ld = [](int, int) -> double2 { return make_double2(0.0, 0.0); };
-  fast_passes<N, C, S, CF, false, P0, NS0, FastTraits<N>>(sm, no_ld, st, tw, pt);
+  fast_passes<N, C, S, CF, false, P0, NS0, FastTraits<N>>(sm, no_ld, st, tw, pt, hook);
 }
 
 // the last-pass stride (= N / radix of the last pass) of a fast tile FFT

@@ -548,7 +548,8 @@ import numpy as np
 sys.path.insert(0, sys.argv[2])
 import paper_1604_06236_b200 as nf
 out = {}
-for P, B, J in [(1000, 1, 0.3), (4096, 1, 0.45), (4096, 4, 0.3), (1 << 16, 1, 0.3), (1 << 18, 1, 0.4)]:
+for P, B, J in [(1000, 1, 0.3), (4096, 1, 0.45), (4096, 4, 0.3), (1 << 16, 1, 0.3), (1 << 18, 1, 0.4),
+                (4096, 32, 0.3), (1 << 16, 16, 0.3), (1 << 15, 24, 0.3), (12288, 16, 0.3)]:
     rng = np.random.default_rng(P + B)
     t = np.mod((np.arange(P) + rng.uniform(-J, J, P)) / P, 1.0)
     plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-15, P, 2))
@@ -565,16 +566,17 @@ def test_kernel_variants_bitwise(tmp_path):
     in the same order: programmatic dependent launch off (NFFT45_NO_PDL),
     warp-tiled single-signal spreading forced on / off (NFFT45_SPREAD_WARP),
     256-cell spreading tiles (NFFT45_STILE) and 256-node interpolation CTAs
-    (NFFT45_GNODES) must all give bitwise the outputs of the default build,
-    for single signals on both sides of the warp-tile threshold, a 4-signal
-    batch and a non-chain size."""
+    (NFFT45_GNODES) and the TMA-staged pad kernel instead of the LDG-staged
+    one (NFFT45_TMA) must all give bitwise the outputs of the
+    default build, for single signals on both sides of the warp-tile
+    threshold, a 4-signal batch, batch-minor chains and a non-chain size."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     variants = ({}, {"NFFT45_NO_PDL": "1"}, {"NFFT45_SPREAD_WARP": "1"}, {"NFFT45_SPREAD_WARP": "0"},
-                {"NFFT45_STILE": "256", "NFFT45_GNODES": "256"})
+                {"NFFT45_STILE": "256", "NFFT45_GNODES": "256"}, {"NFFT45_TMA": "1"})
     outs = []
     for i, extra in enumerate(variants):
         f = tmp_path / f"v{i}.npz"
