@@ -58,6 +58,9 @@ def full(path):
             "smem_wf": g("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
             "smem_conf": g("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
             "cycles": g("sm__cycles_active.avg"),
+            "l2_bytes": g("lts__t_bytes.sum"),
+            "l2_pct": g("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "l2_hit": g("lts__t_sector_hit_rate.pct"),
             "stalls": sorted(((g(k) or 0.0, k.replace("smsp__average_warps_issue_stalled_", "").replace(
                 "_per_issue_active.ratio", "")) for k in d if k.startswith("smsp__average_warps_issue_stalled_")
                 and k.endswith("_per_issue_active.ratio") and "selected" not in k), reverse=True)[:3],
@@ -82,24 +85,30 @@ def main(lpath, fpath, tag, steps, config="c4"):
     res, units = full(fpath)
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     ur, uw = scale.get(units.get("dram__bytes_read.sum", "byte"), 1), scale.get(units.get("dram__bytes_write.sum", "byte"), 1)
+    ul = scale.get(units.get("lts__t_bytes.sum", "byte"), 1)
     traffic = collections.defaultdict(list)
     tunit = units.get("gpu__time_duration.sum", "msecond")
     tscale = {"msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "us": 1e-3, "ns": 1e-6}.get(tunit, 1.0)
     with open(os.path.join(REPO, "profiles", f"{tag}_{config}_kernels.md"), "w") as f:
         f.write(f"# {tag}: ncu --set full captures ({config}, one bench step)\n\n")
-        f.write("Shared-memory busy = LSU shared wavefronts / (SMs x active cycles); stalls = top three "
+        f.write("Shared-memory busy = LSU shared wavefronts / (SMs x active cycles); L2 = `lts__t_bytes.sum` "
+                "(all L2 slice traffic), `lts__throughput` % of peak and sector hit rate; stalls = top three "
                 "`smsp__average_warps_issue_stalled_*` per issued instruction.\n\n")
-        f.write("| kernel | grid | ms | DRAM read GB | DRAM write GB | DRAM % peak | fp64 pipe % | L1 % | SMEM busy % "
-                "| bank conflicts % | issue % | warps active % | regs | top stalls |\n")
-        f.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
+        f.write("| kernel | grid | ms | DRAM read GB | DRAM write GB | DRAM % peak | L2 GB | L2 GB/s | L2 % peak | L2 hit % "
+                "| fp64 pipe % | L1 % | SMEM busy % | bank conflicts % | issue % | warps active % | regs | top stalls |\n")
+        f.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
         for r in res:
             rb, wb = (r["dram_bytes_read"] or 0) * ur, (r["dram_bytes_write"] or 0) * uw
             traffic[r["kernel"]].append(rb + wb)
             smem = 100.0 * (r["smem_wf"] or 0) / 148 / r["cycles"] if r["cycles"] else 0.0
             conf = 100.0 * (r["smem_conf"] or 0) / r["smem_wf"] if r["smem_wf"] else 0.0
             st = ", ".join(f"{n} {v:.2f}" for v, n in r["stalls"])
-            f.write(f"| `{r['kernel']}` | {r['grid']} | {r['time_ms'] * tscale:.3f} | {rb / 1e9:.3f} | {wb / 1e9:.3f} | "
-                    f"{r['dram_pct']:.1f} | {r['fp64_pct']:.1f} | {r['l1_pct']:.1f} | {smem:.1f} | {conf:.1f} | "
+            lb = (r["l2_bytes"] or 0) * ul
+            ms = r["time_ms"] * tscale
+            l2 = (f"{lb / 1e9:.3f} | {lb / (ms / 1e3) / 1e9:.0f} | {r['l2_pct'] or 0:.1f} | {r['l2_hit'] or 0:.1f}"
+                  if r["l2_bytes"] is not None else "— | — | — | —")
+            f.write(f"| `{r['kernel']}` | {r['grid']} | {ms:.3f} | {rb / 1e9:.3f} | {wb / 1e9:.3f} | "
+                    f"{r['dram_pct']:.1f} | {l2} | {r['fp64_pct']:.1f} | {r['l1_pct']:.1f} | {smem:.1f} | {conf:.1f} | "
                     f"{r['issue_pct']:.1f} | {r['warps_active_pct']:.1f} | {r['regs']:.0f} | {st} |\n")
     short = {}
     for k, v in traffic.items():
