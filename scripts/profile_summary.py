@@ -42,7 +42,10 @@ def full(path):
     res = []
     for r in rows[2:]:
         d = dict(zip(h, r))
-        g = lambda k: float(d[k].replace(",", "")) if k in d and d[k] not in ("", "n/a") else None
+        def g(k):
+            # section-prefixed names (e.g. "LTS.TriageCompute.lts__throughput...") are accepted too
+            key = k if k in d else next((h_ for h_ in d if h_.endswith("." + k)), None)
+            return float(d[key].replace(",", "")) if key and d[key] not in ("", "n/a") else None
         res.append({
             "kernel": d["Kernel Name"].split("(")[0].replace("void ", "").strip(),
             "grid": d.get("Grid Size"), "block": d.get("Block Size"),
@@ -58,9 +61,10 @@ def full(path):
             "smem_wf": g("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
             "smem_conf": g("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
             "cycles": g("sm__cycles_active.avg"),
-            "l2_bytes": g("lts__t_bytes.sum"),
+            "l2_bytes": g("l1tex__m_xbar2l1tex_read_bytes.sum"),
             "l2_pct": g("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
-            "l2_hit": g("lts__t_sector_hit_rate.pct"),
+            "l2_hit": g("lts__t_sector_op_read_hit_rate.pct"),
+            "l2x_bps": g("derived__lts__lts2xbar_bytes.sum.per_second"),
             "stalls": sorted(((g(k) or 0.0, k.replace("smsp__average_warps_issue_stalled_", "").replace(
                 "_per_issue_active.ratio", "")) for k in d if k.startswith("smsp__average_warps_issue_stalled_")
                 and k.endswith("_per_issue_active.ratio") and "selected" not in k), reverse=True)[:3],
@@ -85,16 +89,18 @@ def main(lpath, fpath, tag, steps, config="c4"):
     res, units = full(fpath)
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     ur, uw = scale.get(units.get("dram__bytes_read.sum", "byte"), 1), scale.get(units.get("dram__bytes_write.sum", "byte"), 1)
-    ul = scale.get(units.get("lts__t_bytes.sum", "byte"), 1)
+    ul = scale.get(units.get("l1tex__m_xbar2l1tex_read_bytes.sum", "byte"), 1)
     traffic = collections.defaultdict(list)
     tunit = units.get("gpu__time_duration.sum", "msecond")
     tscale = {"msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "us": 1e-3, "ns": 1e-6}.get(tunit, 1.0)
     with open(os.path.join(REPO, "profiles", f"{tag}_{config}_kernels.md"), "w") as f:
         f.write(f"# {tag}: ncu --set full captures ({config}, one bench step)\n\n")
-        f.write("Shared-memory busy = LSU shared wavefronts / (SMs x active cycles); L2 = `lts__t_bytes.sum` "
-                "(all L2 slice traffic), `lts__throughput` % of peak and sector hit rate; stalls = top three "
-                "`smsp__average_warps_issue_stalled_*` per issued instruction.\n\n")
-        f.write("| kernel | grid | ms | DRAM read GB | DRAM write GB | DRAM % peak | L2 GB | L2 GB/s | L2 % peak | L2 hit % "
+        f.write("Shared-memory busy = LSU shared wavefronts / (SMs x active cycles); L2->SM GB = "
+                "`l1tex__m_xbar2l1tex_read_bytes.sum` (bytes the SMs read from L2; writes go through to L2 as "
+                "well), its rate over the kernel time, `lts__throughput` % of peak (the busiest L2 sub-unit) and "
+                "the L2 read-sector hit rate; stalls = top three `smsp__average_warps_issue_stalled_*` per issued "
+                "instruction.\n\n")
+        f.write("| kernel | grid | ms | DRAM read GB | DRAM write GB | DRAM % peak | L2->SM GB | L2->SM GB/s | L2 % peak | L2 read hit % "
                 "| fp64 pipe % | L1 % | SMEM busy % | bank conflicts % | issue % | warps active % | regs | top stalls |\n")
         f.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
         for r in res:
