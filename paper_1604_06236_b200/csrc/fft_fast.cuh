@@ -136,8 +136,14 @@ __device__ __forceinline__ void twiddles(const double2* __restrict__ tw, int e, 
   }
 }
 
+// For column-fast tiles the padding term is split so the index stays linear
+// in i (c < C, C a power of two): tpad(i C + c) = i C + (i C >> 3) + c + (c >> 3)
+// when 8 | C, and i C + c + i / (8 / C) when C < 8 — the same slots, but the
+// per-element offsets of a butterfly fold into immediate offsets.
 template <int N, int C, bool CF>
 __device__ __forceinline__ int sidx(int i, int c) {
+  if constexpr (CF && is_pow2_c(C) && C >= 8) return i * (C + C / 8) + c + (c >> 3);
+  if constexpr (CF && is_pow2_c(C) && C < 8) return i * C + c + i / (8 / C);
   return CF ? tpad(i * C + c) : tpad(c * N + i);
 }
 
