@@ -98,13 +98,17 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<
       pf_rows(in + (int64_t)(sw ? ay : ax) * Bp + (int64_t)(sw ? ax : ay) * kSig, (int64_t)L2 * Bp, L,
               kSig * sizeof(double2));
   }
+  // tile base pointers + 32-bit in-tile offsets (n * Bp < 2^31, guarded on the
+  // host): the per-element address math stays out of 64-bit registers
+  const unsigned ub = (unsigned)Bp;
+  const double2* __restrict__ it = in + (int64_t)n2 * Bp + b0;
+  double2* __restrict__ ot = out + (int64_t)n2 * Bp + b0;
   auto ld = [&](int i, int c) -> double2 {
-    const int64_t idx = (int64_t)i * L2 + n2;
-    double2 v = in[idx * Bp + b0 + c];
-    if (pre) v = rsc(v, __ldg(&pre[idx]));
+    double2 v = it[(unsigned)(i * L2) * ub + c];
+    if (pre) v = rsc(v, __ldg(&pre[(int64_t)i * L2 + n2]));
     return v;
   };
-  auto st = [&](int k1, int c, double2 v) { out[((int64_t)k1 * L2 + n2) * Bp + b0 + c] = v; };
+  auto st = [&](int k1, int c, double2 v) { ot[(unsigned)(k1 * L2) * ub + c] = v; };
   const FourStepTw<S> pt{lo, hi, sh, twQ, Q, n2, 0};
   fast_tile_fft<L, kSig, S, true>(sm, ld, st, tw, pt);
 }
@@ -151,7 +155,10 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
     for (int e = threadIdx.x; e < C * SG; e += blockDim.x)
       cpa16(&s_sb[e], &sub[((int64_t)k1 + (int64_t)R * (e / SG)) * Bp + b0 + e % SG]);
   cpa_commit();
-  auto ld1 = [&](int i, int c) -> double2 { return T[((int64_t)k1 * NR + i) * Bp + b0 + c]; };
+  const unsigned ub = (unsigned)Bp;  // 32-bit in-tile offsets (see kbm_col)
+  const double2* __restrict__ Tt = T + (int64_t)k1 * NR * Bp + b0;
+  double2* __restrict__ Ut = U + (int64_t)k1 * Bp + b0;
+  auto ld1 = [&](int i, int c) -> double2 { return Tt[(unsigned)i * ub + c]; };
   auto st1 = [&](int k2, int c, double2 v) {
     const int m1 = (k2 + C / 2) & (NR - 1);  // (k2 + K/R) mod 2C, K/R = C/2
     if (m1 < C) {
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
   fast_tile_fft<NR, SG, -1, true>(sm, ld1, st1, twR, NoPostTw(), CpAsyncWaitHook());
   __syncthreads();
   auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<C, SG, true>(i, c)]; };
-  auto st2 = [&](int k1p, int c, double2 v) { U[((int64_t)k1p * R + k1) * Bp + b0 + c] = v; };
+  auto st2 = [&](int k1p, int c, double2 v) { Ut[(unsigned)(k1p * R) * ub + c] = v; };
   const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, k1, 0};
   fast_tile_fft_smem<C, SG, +1, true, HalfTr<C>>(sm, ld2, st2, twC, pt);
 }
@@ -193,12 +200,15 @@ __global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<
   }
   for (int k2 = threadIdx.x; k2 < R; k2 += blockDim.x) cpa16(&s_ks[k2], &ks[(int64_t)r + (int64_t)C * k2]);
   cpa_commit();
-  auto ld1 = [&](int i, int c) -> double2 { return U[((int64_t)r * R + i) * Bp + b0 + c]; };
+  const unsigned ub = (unsigned)Bp;  // 32-bit in-tile offsets (see kbm_col)
+  const double2* __restrict__ Ut = U + (int64_t)r * R * Bp + b0;
+  double2* __restrict__ Zt = Z + (int64_t)r * Bp + b0;
+  auto ld1 = [&](int i, int c) -> double2 { return Ut[(unsigned)i * ub + c]; };
   auto st1 = [&](int k2, int c, double2 v) { sm[sidx<R, kSig, true>(k2, c)] = cmul(v, s_ks[k2]); };
   fast_tile_fft<R, kSig, +1, true>(sm, ld1, st1, tw, NoPostTw(), CpAsyncWaitHook());
   __syncthreads();
   auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<R, kSig, true>(i, c)]; };
-  auto st2 = [&](int k, int c, double2 v) { Z[((int64_t)k * C + r) * Bp + b0 + c] = v; };
+  auto st2 = [&](int k, int c, double2 v) { Zt[(unsigned)(k * C) * ub + c] = v; };
   const FourStepTw<-1> pt{loP, hiP, sP, twQ, Q, r, 0};
   fast_tile_fft_smem<R, kSig, -1, true>(sm, ld2, st2, tw, pt);
 }
@@ -827,6 +837,25 @@ bool chain_bm_supported(int64_t P) {
 
 int chain_run_bm(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes, double2* out,
                  double* norms, cudaStream_t st) {
+  // the kernels address a tile's rows with 32-bit offsets: keep n * Bp below
+  // 2^31 by solving large batches in independent slices (rows are independent)
+  const int64_t max_rows = ((int64_t(1) << 31) / (2 * pv.P)) / kSig * kSig;
+  if (batch > max_rows && max_rows >= 16) {
+    double* sn = nullptr;  // per-slice [passes][nb] norms, scattered into [passes][batch]
+    if (norms && passes > 0) NFFT_CUDA(cudaMallocAsync(&sn, sizeof(double) * passes * max_rows, st));
+    int status = NFFT45_OK;
+    for (int64_t b0 = 0; b0 < batch && status == NFFT45_OK; b0 += max_rows) {
+      const int64_t nb = std::min(max_rows, batch - b0);
+      status = chain_run_bm(pv, kind, data + b0 * pv.P, nb, passes, out + b0 * pv.P, sn, st);
+      if (status == NFFT45_OK && sn) {
+        const cudaError_t e = cudaMemcpy2DAsync(norms + b0, sizeof(double) * batch, sn, sizeof(double) * nb,
+                                                sizeof(double) * nb, passes, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) status = cuda_fail(e, "norms slice copy");
+      }
+    }
+    if (sn) cudaFreeAsync(sn, st);
+    return status;
+  }
   switch (pv.P) {
     case 1024: return chain_solve_bm<32, 32>(pv, kind, data, batch, passes, out, norms, st);
     case 2048: return chain_solve_bm<64, 32>(pv, kind, data, batch, passes, out, norms, st);
