@@ -303,20 +303,196 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
   }
 }
 
+// ------------------------------------------------------------------------
+// Hybrid variants of the two-FFT kernels (see hyb_passes in fft_fast.cuh):
+// the first pass (from global memory) and the last pass (to global memory)
+// keep the column-fast mapping, every pass in between is warp-local on an
+// unpadded XOR-swizzled tile, so a tile costs 2 CTA barriers instead of 9-10.
+// Same arithmetic per element as kbm_band / kbm_mid / kbm_pad (bitwise
+// identical results).  Used when both tile FFTs satisfy hyb_ok (powers of two
+// with at most 32 threads per signal: every R = C and R = 2C chain up to
+// P = 2^17).
+template <int R, int C>
+__host__ __device__ constexpr bool bm_hyb() {
+  return bm_sg<C>() == kSig && hyb_ok<2 * C>() && hyb_ok<C, HalfTr<C>>() && hyb_ok<R>();
+}
+
+template <int R, int C>
+__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_band_h(
+    const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
+    const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
+    const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
+    const double* __restrict__ dd, const double2* __restrict__ sub, double2* __restrict__ rsave) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
+  constexpr int NR = 2 * C;
+  constexpr int SG = kSig;
+  using TrA = FastTraits<NR>;
+  using TrB = HalfTr<C>;
+  extern __shared__ double2 sm[];
+  double* s_t0 = reinterpret_cast<double*>(sm + NR * SG);
+  double* s_t1 = s_t0 + C;
+  double2* s_sb = reinterpret_cast<double2*>(s_t1 + C);
+  const int k1 = blockIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * SG;
+  for (int m1 = threadIdx.x; m1 < C; m1 += blockDim.x) {
+    const int64_t p = (int64_t)k1 + (int64_t)R * m1;
+    if (sub) {
+      cpa8(&s_t0[m1], &deconv[p]);
+      cpa8(&s_t1[m1], &decay[p]);
+    } else {
+      cpa8(&s_t0[m1], &dd[p]);
+    }
+  }
+  if (sub)  // subtrahend tile, swizzled like the data tile (it is read by warp-local lanes)
+    for (int e = threadIdx.x; e < C * SG; e += blockDim.x)
+      cpa16(&s_sb[hidx(e / SG, e % SG)], &sub[((int64_t)k1 + (int64_t)R * (e / SG)) * Bp + b0 + e % SG]);
+  cpa_commit();
+  const unsigned ub = (unsigned)Bp;  // 32-bit in-tile offsets (see kbm_col)
+  const double2* __restrict__ Tt = T + (int64_t)k1 * NR * Bp + b0;
+  double2* __restrict__ Ut = U + (int64_t)k1 * Bp + b0;
+  auto ld1 = [&](int i, int c) -> double2 { return Tt[(unsigned)i * ub + c]; };
+  auto st1 = [&](int k2, int c, double2 v) {
+    const int m1 = (k2 + C / 2) & (NR - 1);  // (k2 + K/R) mod 2C, K/R = C/2
+    if (m1 < C) {
+      if (sub) {
+        v = rsc(v, s_t0[m1]);
+        v = csub(v, s_sb[hidx(m1, c)]);
+        if (rsave) rsave[((int64_t)k1 + (int64_t)R * m1) * Bp + b0 + c] = v;  // r itself (norms, passes >= 2)
+        v = rsc(v, s_t1[m1]);
+      } else {
+        v = rsc(v, s_t0[m1]);
+      }
+      sm[hidx(m1, c)] = v;
+    }
+  };
+  hyb_tile_fft<NR, -1, TrA, hyb_mask<TrA>(true, false), false, true>(sm, ld1, st1, twR, NoPostTw(),
+                                                                     CpAsyncWaitHook());
+  __syncwarp();  // the band of signal c was written by the warp that transforms it next
+  auto ld2 = [&](int i, int c) -> double2 { return sm[hidx(i, c)]; };
+  auto st2 = [&](int k1p, int c, double2 v) { Ut[(unsigned)(k1p * R) * ub + c] = v; };
+  const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, k1, 0};
+  hyb_tile_fft<C, +1, TrB, hyb_mask<TrB>(false, true), true, false>(sm, ld2, st2, twC, pt);
+}
+
+template <int R, int C>
+__global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<R, kSig>())) kbm_mid_h(
+    const double2* __restrict__ U, double2* __restrict__ Z, int64_t Bp, const double2* __restrict__ tw,
+    const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
+    const double2* __restrict__ ks) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
+  using Tr = FastTraits<R>;
+  extern __shared__ double2 sm[];
+  double2* s_ks = sm + R * kSig;
+  const int r = blockIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * kSig;
+  for (int k2 = threadIdx.x; k2 < R; k2 += blockDim.x) cpa16(&s_ks[k2], &ks[(int64_t)r + (int64_t)C * k2]);
+  cpa_commit();
+  const unsigned ub = (unsigned)Bp;  // 32-bit in-tile offsets (see kbm_col)
+  const double2* __restrict__ Ut = U + (int64_t)r * R * Bp + b0;
+  double2* __restrict__ Zt = Z + (int64_t)r * Bp + b0;
+  auto ld1 = [&](int i, int c) -> double2 { return Ut[(unsigned)i * ub + c]; };
+  auto st1 = [&](int k2, int c, double2 v) { sm[hidx(k2, c)] = cmul(v, s_ks[k2]); };
+  hyb_tile_fft<R, +1, Tr, hyb_mask<Tr>(true, false), false, true>(sm, ld1, st1, tw, NoPostTw(), CpAsyncWaitHook());
+  __syncwarp();
+  auto ld2 = [&](int i, int c) -> double2 { return sm[hidx(i, c)]; };
+  auto st2 = [&](int k, int c, double2 v) { Zt[(unsigned)(k * C) * ub + c] = v; };
+  const FourStepTw<-1> pt{loP, hiP, sP, twQ, Q, r, 0};
+  hyb_tile_fft<R, -1, Tr, hyb_mask<Tr>(false, true), true, false>(sm, ld2, st2, tw, pt);
+}
+
+// XOUT: the tile also stores x (coalesced rows), so the last pass of the
+// C-point FFT keeps the column-fast mapping and is followed by a CTA barrier.
+template <int R, int C, bool XOUT>
+__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_pad_h(
+    const double2* __restrict__ Z, double2* __restrict__ Y, int64_t Bp, const double2* __restrict__ twR,
+    const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
+    const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
+    const double* __restrict__ cd, const double2* __restrict__ xsub, double2* __restrict__ xout) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
+  constexpr int NC = 2 * C;
+  constexpr int SG = kSig;
+  using TrA = HalfTr<C>;
+  using TrB = FastTraits<NC>;
+  constexpr bool kLead2 = TrB::radix(0) == 2;
+  extern __shared__ double2 sm[];
+  double* s_t0 = reinterpret_cast<double*>(sm + NC * SG);
+  double* s_t1 = s_t0 + C;
+  double2* s_xs = reinterpret_cast<double2*>(s_t1 + C);
+  const int r = blockIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * SG;
+  const unsigned ub = (unsigned)Bp;
+  const double2* __restrict__ Zt = Z + (int64_t)r * C * Bp + b0;
+  double2* __restrict__ Yt = Y + (int64_t)r * Bp + b0;
+  double2* __restrict__ Xt = XOUT ? xout + (int64_t)r * Bp + b0 : nullptr;
+  const double2* __restrict__ XSt = (XOUT && xsub) ? xsub + (int64_t)r * Bp + b0 : nullptr;
+  for (int k2 = threadIdx.x; k2 < C; k2 += blockDim.x) {
+    const int64_t p = (int64_t)r + (int64_t)R * k2;
+    if (XOUT) {
+      cpa8(&s_t0[k2], &coef[p]);
+      cpa8(&s_t1[k2], &deconv[p]);
+    } else {
+      cpa8(&s_t0[k2], &cd[p]);
+    }
+  }
+  if (XOUT && xsub)
+    for (int e = threadIdx.x; e < C * SG; e += blockDim.x)
+      cpa16(&s_xs[e], &XSt[(unsigned)(R * (e / SG)) * ub + e % SG]);
+  cpa_commit();
+  auto ld1 = [&](int i, int c) -> double2 { return Zt[(unsigned)i * ub + c]; };
+  auto st1 = [&](int k2, int c, double2 v) {
+    if (XOUT) {
+      v = rsc(v, s_t0[k2]);
+      if (xsub) v = csub(s_xs[k2 * SG + c], v);
+      Xt[(unsigned)(R * k2) * ub + c] = v;
+      v = rsc(v, s_t1[k2]);
+    } else {
+      v = rsc(v, s_t0[k2]);
+    }
+    const int n1 = (k2 - C / 2) & (NC - 1);
+    if constexpr (kLead2) {
+      // first Stockham pass (radix 2) of the zero-padded column: a copy (see kbm_pad)
+      if (n1 < C) {
+        sm[hidx(2 * n1, c)] = v;
+        sm[hidx(2 * n1 + 1, c)] = v;
+      } else {
+        const int j = n1 - C;
+        sm[hidx(2 * j, c)] = v;
+        sm[hidx(2 * j + 1, c)] = make_double2(-v.x, -v.y);
+      }
+    } else {
+      sm[hidx(n1, c)] = v;
+      sm[hidx((n1 + C) & (NC - 1), c)] = make_double2(0.0, 0.0);
+    }
+  };
+  constexpr unsigned maskA = hyb_mask<TrA>(true, XOUT);
+  hyb_tile_fft<C, -1, TrA, maskA, false, true>(sm, ld1, st1, twR, NoPostTw(), CpAsyncWaitHook());
+  if constexpr (XOUT) __syncthreads();
+  else __syncwarp();
+  auto st2 = [&](int k, int c, double2 v) { Yt[(unsigned)(k * R) * ub + c] = v; };
+  const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r, 0};
+  if constexpr (kLead2) {
+    hyb_tile_fft_from<NC, +1, TrB, hyb_mask<TrB>(false, true), 1, 2>(sm, st2, twC, pt);
+  } else {
+    auto ld2 = [&](int i, int c) -> double2 { return sm[hidx(i, c)]; };
+    hyb_tile_fft<NC, +1, TrB, hyb_mask<TrB>(false, true), true, false>(sm, ld2, st2, twC, pt);
+  }
+}
+
 // First-pass hook of the TMA-staged kernels: wait for the cp.async table
 // copies before the barrier; after it (every thread has read the tile) thread
 // 0 refills the buffer with the CTA's next tile of ROWS rows.
-template <int ROWS, int SG>
+template <int ROWS, int SG, bool OPQ = false>
 struct TmaNextTile {
   static constexpr bool kActive = true;
-  static constexpr bool kOpaque = false;
+  static constexpr bool kOpaque = OPQ;
   const CUtensorMap* map;
   double2* dst;
   uint64_t* bar;
   int tn, ntiles, groups;
+  int tid;  // thread index within the CTA (or the CTA's tile group)
   __device__ __forceinline__ void operator()() const { asm volatile("cp.async.wait_all;\n" ::); }
   __device__ __forceinline__ void after() const {
-    if (threadIdx.x == 0 && tn < ntiles) {
+    if (tid == 0 && tn < ntiles) {
       fence_proxy_async();  // the first pass's generic reads of the buffer precede the async refill
       mbar_expect_tx(bar, (unsigned)(ROWS * SG * sizeof(double2)));
       tma_load_2d(dst, map, 2 * SG * (tn % groups), ROWS * (tn / groups), bar);
@@ -351,9 +527,9 @@ struct PadTileArgs {
   int ntiles, groups;
 };
 
-template <int R, int C, int SG>
+template <int R, int C, int SG, bool OPQ = false, class Sy = CtaSync>
 __device__ __forceinline__ void pad_tile(const PadTileArgs& a, const CUtensorMap* tmZ, double2* sm, double2* inb,
-                                      uint64_t* bar, int t) {
+                                      uint64_t* bar, int t, int tn, const Sy& sy = Sy()) {
   constexpr int NC = 2 * C;
   constexpr bool kLead2 = FastTraits<NC>::radix(0) == 2;
   double* s_t0 = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + fast_smem<NC, SG>());
@@ -364,9 +540,9 @@ __device__ __forceinline__ void pad_tile(const PadTileArgs& a, const CUtensorMap
   double2* __restrict__ Yt = a.Y + (int64_t)r * a.Bp + b0;
   double2* __restrict__ Xt = a.xout ? a.xout + (int64_t)r * a.Bp + b0 : nullptr;
   const bool xo = a.xout != nullptr;
-  int tid0 = threadIdx.x;
+  int tid0 = sy.tid();
   asm volatile("" : "+r"(tid0));
-  for (int k2 = tid0; k2 < C; k2 += blockDim.x) {
+  for (int k2 = tid0; k2 < C; k2 += fast_threads<NC, SG>()) {
     const int64_t p = (int64_t)r + (int64_t)R * k2;
     if (xo) {
       cpa8(&s_t0[k2], &a.coef[p]);
@@ -376,7 +552,7 @@ __device__ __forceinline__ void pad_tile(const PadTileArgs& a, const CUtensorMap
     }
   }
   cpa_commit();
-  const TmaNextTile<C, SG> hook{tmZ, inb, bar, a.ntiles, a.ntiles, a.groups};  // no refill (one tile per CTA)
+  const TmaNextTile<C, SG, OPQ> hook{tmZ, inb, bar, tn, a.ntiles, a.groups, sy.tid()};  // refill with tile tn
   auto ld1 = [&](int i, int c) -> double2 { return inb[i * SG + c]; };
   auto st1 = [&](int k2, int c, double2 v) {
     if (xo) {
@@ -401,15 +577,15 @@ __device__ __forceinline__ void pad_tile(const PadTileArgs& a, const CUtensorMap
       sm[sidx<NC, SG, true>((n1 + C) & (NC - 1), c)] = make_double2(0.0, 0.0);
     }
   };
-  fast_tile_fft<C, SG, -1, true, HalfTr<C>>(sm, ld1, st1, a.twR, NoPostTw(), hook);
-  __syncthreads();
+  fast_tile_fft<C, SG, -1, true, HalfTr<C>>(sm, ld1, st1, a.twR, NoPostTw(), hook, sy);
+  sy.sync();
   auto st2 = [&](int k, int c, double2 v) { Yt[(unsigned)(k * R) * ub + c] = v; };
   const FourStepTw<+1> pt{a.loN, a.hiN, a.sN, a.twQ, a.Q, r, 0};
   if constexpr (kLead2) {
-    fast_tile_fft_from<NC, SG, +1, true, 1, 2>(sm, st2, a.twC, pt, NoHookT<false>());
+    fast_tile_fft_from<NC, SG, +1, true, 1, 2>(sm, st2, a.twC, pt, NoHookT<OPQ>(), sy);
   } else {
     auto ld2 = [&](int i, int c) -> double2 { return sm[sidx<NC, SG, true>(i, c)]; };
-    fast_tile_fft_smem<NC, SG, +1, true>(sm, ld2, st2, a.twC, pt, NoHookT<false>());
+    fast_tile_fft_smem<NC, SG, +1, true>(sm, ld2, st2, a.twC, pt, NoHookT<OPQ>(), sy);
   }
 }
 
@@ -438,7 +614,80 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
   }
   if (t < a.ntiles) {
     mbar_wait(bar, 0);
-    pad_tile<R, C, SG>(a, &tmZ, sm, inb, bar, t);
+    pad_tile<R, C, SG>(a, &tmZ, sm, inb, bar, t, a.ntiles);  // no refill (one tile per CTA)
+  }
+}
+
+template <int R, int C, int SG>
+__device__ __noinline__ bool pad_p_body(const CUtensorMap* tmZ, const PadTileArgs* ap, unsigned char* smraw, int it) {
+  constexpr int NC = 2 * C;
+  constexpr int T = fast_threads<NC, SG>();
+  constexpr unsigned kTileBytes = (unsigned)(C * SG * sizeof(double2));
+  constexpr size_t kWork = (fast_smem<NC, SG>() + 2 * sizeof(double) * C + 127) / 128 * 128;
+  constexpr size_t kGroup = kWork + kTileBytes;
+  const PadTileArgs& a = *ap;
+  const int tx = threadIdx.x;
+  const int g = tx / T;
+  const GroupSync<T> sy{g, tx - g * T};
+  const int stride = 2 * gridDim.x;
+  const int t = 2 * blockIdx.x + g + it * stride;
+  if (t >= a.ntiles) return false;
+  double2* sm = reinterpret_cast<double2*>(smraw + g * kGroup);
+  double2* inb = reinterpret_cast<double2*>(smraw + g * kGroup + kWork);  // [C][SG] dense (TMA box)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * kGroup) + g;
+  mbar_wait(bar, it & 1);
+  pad_tile<R, C, SG, false>(a, tmZ, sm, inb, bar, t, t + stride, sy);
+  return true;
+}
+
+// Persistent, software-pipelined pad: ONE CTA per SM made of two independent
+// tile groups of T threads.  Each group owns a work buffer, its table slots,
+// a TMA staging buffer and an mbarrier, and walks the tiles
+// t = 2 blockIdx.x + group, + 2 gridDim.x, ... : right after the first pass
+// has pulled the staged tile into registers (its barrier), the group's thread
+// 0 refills the staging buffer with the group's NEXT tile, so that tile's
+// DRAM latency runs under the remaining five passes of the current one, and
+// the other group's arithmetic fills this group's barrier waits.  Registers
+// hold only tiles being computed (the one-shot kernels keep 2 x 32K registers
+// idle while their tiles are in flight).  Arithmetic and store order are those
+// of kbm_pad: bitwise identical results.
+template <int R, int C, int SG>
+__global__ void __launch_bounds__(2 * fast_threads<2 * C, SG>(), 1) kbm_pad_p(
+    const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ PadTileArgs a) {
+  constexpr int NC = 2 * C;
+  constexpr int T = fast_threads<NC, SG>();
+  constexpr unsigned kTileBytes = (unsigned)(C * SG * sizeof(double2));
+  constexpr size_t kWork = (fast_smem<NC, SG>() + 2 * sizeof(double) * C + 127) / 128 * 128;
+  constexpr size_t kGroup = kWork + kTileBytes;
+  extern __shared__ __align__(128) unsigned char smraw_p[];
+  {
+    const int g = threadIdx.x / T;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw_p + 2 * kGroup) + g;
+    if ((int)threadIdx.x - g * T == 0) {
+      if (g == 0) tma_prefetch_desc(&tmZ);
+      mbar_init(bar, 1);
+      mbar_fence_init();
+    }
+  }
+  __syncthreads();
+  pdl_enter();  // programmatic dependent launch: Z is the producer's output
+  {
+    const int g = threadIdx.x / T;
+    const int t = 2 * blockIdx.x + g;
+    if ((int)threadIdx.x - g * T == 0 && t < a.ntiles) {
+      uint64_t* bar = reinterpret_cast<uint64_t*>(smraw_p + 2 * kGroup) + g;
+      mbar_expect_tx(bar, kTileBytes);
+      tma_load_2d(smraw_p + g * kGroup + kWork, &tmZ, 2 * SG * (t % a.groups), C * (t / a.groups), bar);
+    }
+  }
+  // loop state: the iteration count only; everything else is re-derived from
+  // (laundered) special registers inside the body so that nothing thread- or
+  // tile-dependent stays live across the tile's barriers
+  // the tile body is a real call (see pad_p_body): inlined into this loop,
+  // ptxas keeps ~30 more registers live across the tile's barriers and spills
+  // 1.3 KB per thread; as a function with one integer argument it spills 80 B
+#pragma unroll 1
+  for (int it = 0; pad_p_body<R, C, SG>(&tmZ, &a, smraw_p, it); it++) {
   }
 }
 
@@ -514,6 +763,22 @@ __global__ void __launch_bounds__(fast_threads<C, 4 * RW>(), bm_minb(fast_thread
   fast_tile_fft<C, 4 * RW, -1, true>(sm, ld, st, tw);
 }
 
+// Kernel-only build for register / SASS experiments:
+//   nvcc ... -DNFFT45_EXP_ONLY -Xptxas -v -c csrc/chain_bm.cu
+#ifdef NFFT45_EXP_ONLY
+#define NFFT45_EXP_RC 256, 256
+template __global__ void kbm_band_h<NFFT45_EXP_RC>(const double2*, double2*, int64_t, const double2*, const double2*, const double2*,
+                                              const double2*, int, const double2*, int, const double*, const double*,
+                                              const double*, const double2*, double2*);
+template __global__ void kbm_mid_h<NFFT45_EXP_RC>(const double2*, double2*, int64_t, const double2*, const double2*, const double2*,
+                                             int, const double2*, int, const double2*);
+template __global__ void kbm_pad_h<NFFT45_EXP_RC, false>(const double2*, double2*, int64_t, const double2*, const double2*,
+                                                    const double2*, const double2*, int, const double2*, int,
+                                                    const double*, const double*, const double*, const double2*, double2*);
+template __global__ void kbm_pad_h<NFFT45_EXP_RC, true>(const double2*, double2*, int64_t, const double2*, const double2*,
+                                                   const double2*, const double2*, int, const double2*, int,
+                                                   const double*, const double*, const double*, const double2*, double2*);
+#else
 // ------------------------------------------------------------ host side
 
 int tma_map_rows(CUtensorMap* map, const void* base, int64_t rows, int64_t Bp, int box_rows, int box_sig) {
@@ -568,6 +833,7 @@ struct ChainBM {
   bool small_tiles = false;  // 4-signal tiles for the two-FFT kernels (A/B experiment)
   bool sw = false;           // grid order: signal groups fastest (blockIdx.x) instead of tile index
   int pf = 0;                // L2 prefetch distance in launch slots (0: off)
+  bool hyb = false;          // hybrid two-FFT kernels (warp-local middle passes), when bm_hyb<R, C>()
   // grid of (tiles x groups*mult); with sw the signal groups run fastest
   dim3 gdim(int tiles, int mult = 1) const {
     return sw ? dim3(groups * mult, (unsigned)tiles) : dim3((unsigned)tiles, groups * mult);
@@ -608,12 +874,42 @@ struct ChainBM {
            (int)Q, pv.deconv, pv.decay, pv.dd, sub, (int)sw, pf, rsave);
     return NFFT45_OK;
   }
+  int band_h(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub, double2* rsave) {
+    if constexpr (bm_hyb<R, C>()) {
+      auto bm_band = kbm_band_h<R, C>;
+      const size_t smem = sizeof(double2) * 2 * C * kSig + 2 * sizeof(double) * C + (sub ? sizeof(double2) * C * kSig : 0);
+      NFFT_CHECK(bm_attr(bm_band, smem));
+      constexpr int T = fast_threads<2 * C, kSig>();
+      const int64_t Q = P / last_stride<C, HalfTr<C>>();
+      const double2* twQ = nullptr;
+      NFFT_CHECK(qtab(Q, &twQ));
+      LAUNCH_PDL(bm_band, dim3(groups, (unsigned)R), T, smem, st, T_, U, Bp, t.tw2C, t.twC, t.tP->lo, t.tP->hi, t.tP->s,
+                 twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub, rsave);
+    }
+    return NFFT45_OK;
+  }
   int band(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub, double2* rsave = nullptr) {
+    if (hyb && !small_tiles) return band_h(T_, U, pv, sub, rsave);
     if (small_tiles || SG < kSig) return band_g<kSig / 2>(T_, U, pv, sub, rsave);  // always for C = 1024
     return band_g<kSig>(T_, U, pv, sub, rsave);
   }
 
+  int mid_h(const double2* U, double2* Z, const ChainPlanView& pv) {
+    if constexpr (bm_hyb<R, C>()) {
+      auto bm_mid = kbm_mid_h<R, C>;
+      constexpr size_t smem = sizeof(double2) * R * kSig + sizeof(double2) * R;
+      NFFT_CHECK(bm_attr(bm_mid, smem));
+      constexpr int T = fast_threads<R, kSig>();
+      const int64_t Q = P / last_stride<R>();
+      const double2* twQ = nullptr;
+      NFFT_CHECK(qtab(Q, &twQ));
+      LAUNCH_PDL(bm_mid, dim3(groups, (unsigned)C), T, smem, st, U, Z, Bp, t.twR, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q,
+                 pv.ks);
+    }
+    return NFFT45_OK;
+  }
   int mid(const double2* U, double2* Z, const ChainPlanView& pv) {
+    if (hyb) return mid_h(U, Z, pv);
     auto bm_mid = kbm_mid<R, C>;
     constexpr size_t smem = fast_smem<R, kSig>() + sizeof(double2) * R;
     NFFT_CHECK(bm_attr(bm_mid, smem));
@@ -668,8 +964,54 @@ struct ChainBM {
     LAUNCH_PDL(bm_pad, grid, T, smem, st, tm, args);
     return NFFT45_OK;
   }
+  // Persistent two-group pad (kbm_pad_p): one CTA per SM, TMA-prefetched tiles.
+  int pad_persist(const double2* Z, double2* Y, const ChainPlanView& pv, double2* xout) {
+    auto bm_pad = kbm_pad_p<R, C, kSig>;
+    constexpr size_t kWork = (fast_smem<2 * C, kSig>() + 2 * sizeof(double) * C + 127) / 128 * 128;
+    constexpr size_t smem = 2 * (kWork + sizeof(double2) * C * kSig) + 16;
+    NFFT_CHECK(bm_attr(bm_pad, smem));
+    constexpr int T = 2 * fast_threads<2 * C, kSig>();
+    const int64_t Q = n / last_stride<2 * C>();
+    const double2* twQ = nullptr;
+    NFFT_CHECK(qtab(Q, &twQ));
+    CUtensorMap tm;
+    NFFT_CHECK(tma_map_rows(&tm, Z, P, Bp, C, kSig));
+    const int ntiles = (int)(R * groups);
+    static const int sms = [] {
+      int dev = 0, v = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+      return v;
+    }();
+    const int grid = std::min(sms, (ntiles + 1) / 2);
+    const PadTileArgs args{Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q,
+                           pv.coef, pv.deconv, pv.cd, xout, ntiles, (int)groups};
+    LAUNCH_PDL(bm_pad, grid, T, smem, st, tm, args);
+    return NFFT45_OK;
+  }
+  template <bool XOUT>
+  int pad_h(const double2* Z, double2* Y, const ChainPlanView& pv, const double2* xsub, double2* xout) {
+    if constexpr (bm_hyb<R, C>()) {
+      auto bm_pad = kbm_pad_h<R, C, XOUT>;
+      const size_t smem =
+          sizeof(double2) * 2 * C * kSig + 2 * sizeof(double) * C + (XOUT && xsub ? sizeof(double2) * C * kSig : 0);
+      NFFT_CHECK(bm_attr(bm_pad, smem));
+      constexpr int T = fast_threads<2 * C, kSig>();
+      const int64_t Q = n / last_stride<2 * C>();
+      const double2* twQ = nullptr;
+      NFFT_CHECK(qtab(Q, &twQ));
+      LAUNCH_PDL(bm_pad, dim3(groups, (unsigned)R), T, smem, st, Z, Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s,
+                 twQ, (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout);
+    }
+    return NFFT45_OK;
+  }
   int pad(const double2* Z, double2* Y, const ChainPlanView& pv, const double2* xsub, double2* xout) {
     static const bool tma = getenv("NFFT45_TMA") != nullptr;
+    if (hyb && !small_tiles && !tma && !getenv("NFFT45_PADP"))
+      return xout ? pad_h<true>(Z, Y, pv, xsub, xout) : pad_h<false>(Z, Y, pv, xsub, xout);
+    static const bool padp = getenv("NFFT45_PADP") != nullptr;
+    if constexpr (C <= 256 && SG == kSig)
+      if (padp && !small_tiles && !(xout && xsub)) return pad_persist(Z, Y, pv, xout);
     if constexpr (C <= 256 && SG == kSig)
       if (tma && !small_tiles && !(xout && xsub)) return pad_tma(Z, Y, pv, xout);
     if (small_tiles || SG < kSig) return pad_g<kSig / 2>(Z, Y, pv, xsub, xout);  // always for C = 1024
@@ -739,6 +1081,10 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
     // kept as an opt-in A/B switch, off by default
     static const int pf_env = getenv("NFFT45_PREFETCH") ? atoi(getenv("NFFT45_PREFETCH")) : 0;
     ch.pf = pf_env;
+    // hybrid two-FFT kernels (2 CTA barriers per tile, warp-local middle
+    // passes); NFFT45_HYB=0 restores the all-column-fast kernels for A/B runs
+    static const bool hyb_on = !(getenv("NFFT45_HYB") && atoi(getenv("NFFT45_HYB")) == 0);
+    ch.hyb = hyb_on && bm_hyb<R, C>() && !ch.small_tiles;
   }
   int status = NFFT45_OK;
   {
@@ -876,5 +1222,6 @@ int chain_run_bm(const ChainPlanView& pv, int kind, const double2* data, int64_t
   }
   return NFFT45_ERR_INVALID_ARGUMENT;
 }
+#endif  // NFFT45_EXP_ONLY
 
 }  // namespace nfft45

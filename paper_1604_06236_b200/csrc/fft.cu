@@ -72,6 +72,15 @@ __global__ void k_twiddle_fill(double2* out, int64_t count, int64_t N, int64_t s
 static std::mutex g_tw_mu;
 static std::map<std::pair<int, int64_t>, FftTables*> g_tw;
 
+#define NFFT_CUDA_P(call)                                  \
+  do {                                                     \
+    cudaError_t _e = (call);                               \
+    if (_e != cudaSuccess) {                               \
+      *status = cuda_fail(_e, #call);                      \
+      return nullptr;                                      \
+    }                                                      \
+  } while (0)
+
 const FftTables* fft_tables(int64_t N, cudaStream_t st, int* status) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -89,7 +98,16 @@ const FftTables* fft_tables(int64_t N, cudaStream_t st, int* status) {
     return NFFT45_OK;
   };
   int s = NFFT45_OK;
-  if (N <= 65536 || !fft_smooth(N)) s = fill(&t->tw, N, 1);
+  if (N <= kTileMax && is_pow2(N)) {
+    // [4][N]: section q = W_N^{k 2^q} (the same sincospi values as tw[(k << q) mod N])
+    NFFT_CUDA_P(cudaMalloc(&t->tw, sizeof(double2) * 4 * N));
+    for (int q = 0; q < 4 && s == NFFT45_OK; q++) {
+      k_twiddle_fill<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(t->tw + q * N, N, N, int64_t(1) << q);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      cudaError_t le = cudaGetLastError();
+      if (le != cudaSuccess) s = cuda_fail(le, "k_twiddle_fill");
+    }
+  } else if (N <= 65536 || !fft_smooth(N)) s = fill(&t->tw, N, 1);
   if (s == NFFT45_OK && N > 1 && fft_smooth(N)) {
     int bits = 0;
     while ((int64_t(1) << (2 * bits)) < N) bits++;

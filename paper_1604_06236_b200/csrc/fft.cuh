@@ -35,6 +35,8 @@ FftSeq fft_seq(int N);
 struct FftTables {
   int64_t N;
   double2* tw;   // W_N^k = e^{-2 pi i k / N}, k < N (only when N <= kTileMax or non-smooth)
+                 // powers of two up to kTileMax: [4][N], section q holds W_N^{k 2^q} (section 0 = the
+                 // plain table), so warp-local passes read their 2^q-th powers as contiguous runs
   double2* lo;   // four-step twiddles: W_N^k, k < 2^s
   double2* hi;   // W_N^{k 2^s}, k < ceil(N / 2^s)
   int s;

@@ -136,6 +136,30 @@ __device__ __forceinline__ void twiddles(const double2* __restrict__ tw, int e, 
   }
 }
 
+// The same twiddles from the [4][N] power table of FftTables (section q =
+// W_N^{k 2^q}): bitwise the values twiddles<R> loads, but lanes with
+// consecutive e read consecutive words of every section.
+template <int R, int N>
+__device__ __forceinline__ void twiddles_pw(const double2* __restrict__ tw, int e, double2* w) {
+  static_assert(R == 2 || R == 4 || R == 8 || R == 16, "power-table twiddles: radix 2/4/8/16");
+  w[1] = __ldg(&tw[e]);
+  if constexpr (R >= 4) {
+    w[2] = __ldg(&tw[N + e]);
+    w[3] = cmul(w[1], w[2]);
+  }
+  if constexpr (R >= 8) {
+    w[4] = __ldg(&tw[2 * N + e]);
+    w[5] = cmul(w[1], w[4]);
+    w[6] = cmul(w[2], w[4]);
+    w[7] = cmul(w[3], w[4]);
+  }
+  if constexpr (R >= 16) {
+    w[8] = __ldg(&tw[3 * N + e]);
+#pragma unroll
+    for (int r = 1; r < 8; r++) w[8 + r] = cmul(w[r], w[8]);
+  }
+}
+
 // For column-fast tiles the padding term is split so the index stays linear
 // in i (c < C, C a power of two): tpad(i C + c) = i C + (i C >> 3) + c + (c >> 3)
 // when 8 | C, and i C + c + i / (8 / C) when C < 8 — the same slots, but the
@@ -228,14 +252,29 @@ struct CpAsyncWaitHook {
   __device__ __forceinline__ void after() const {}
 };
 
+// Synchronisation policy of a tile FFT: the whole CTA (default), or one
+// GROUP of T threads of a persistent CTA whose groups work on different tiles
+// (named barrier 1 + group id; thread index within the group).
+struct CtaSync {
+  __device__ __forceinline__ int tid() const { return threadIdx.x; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+template <int T>
+struct GroupSync {
+  int id;  // group index (named barrier id - 1)
+  int t;   // thread index within the group
+  __device__ __forceinline__ int tid() const { return t; }
+  __device__ __forceinline__ void sync() const { asm volatile("bar.sync %0, %1;\n" ::"r"(id + 1), "n"(T) : "memory"); }
+};
+
 // One pass; FIRST reads through `ld`, LAST writes through `st`.  Threads
 // with threadIdx.x >= T (a CTA sized for a bigger FFT of a chain) idle but
 // still meet every barrier.  SYNC0: the first pass reads shared memory that
 // its own stores overwrite (chain kernels), so it needs a barrier too.
 template <int N, int C, int S, bool CF, bool SYNC0, int P, int Ns, class Tr, class Ld, class St, class PT,
-          class Hk = NoHook>
+          class Hk = NoHook, class Sy = CtaSync>
 __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
-                                            const PT& pt, const Hk& hook = Hk()) {
+                                            const PT& pt, const Hk& hook = Hk(), const Sy& sy = Sy()) {
   constexpr int E = Tr::E;
   constexpr int R = Tr::radix(P);
   constexpr int T = N * C / E;
@@ -243,7 +282,7 @@ __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St&
   constexpr int stride = N / R;
   constexpr bool FIRST = (P == 0);
   constexpr bool LAST = (P == Tr::np - 1);
-  int tid = threadIdx.x;
+  int tid = sy.tid();
   if constexpr (Hk::kOpaque) asm volatile("" : "+r"(tid));
   const bool active = tid < T;
   double2 v[MB][R];
@@ -262,7 +301,7 @@ __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St&
   }
   }
   if constexpr (FIRST && LAST && Hk::kActive) hook();
-  if constexpr (!FIRST || SYNC0 || (LAST && Hk::kActive)) __syncthreads();  // everyone has read before anyone overwrites
+  if constexpr (!FIRST || SYNC0 || (LAST && Hk::kActive)) sy.sync();  // everyone has read before anyone overwrites
   if (active) {
 #pragma unroll
   for (int u = 0; u < MB; u++) {
@@ -289,36 +328,175 @@ __device__ __forceinline__ void fast_passes(double2* sm, const Ld& ld, const St&
   }
   if constexpr (!LAST) {
     if constexpr (FIRST && Hk::kActive) hook();
-    __syncthreads();
+    sy.sync();
     if constexpr (FIRST && Hk::kActive) hook.after();
-    fast_passes<N, C, S, CF, SYNC0, P + 1, Ns * R, Tr>(sm, ld, st, tw, pt, NoHookT<Hk::kOpaque>());
+    fast_passes<N, C, S, CF, SYNC0, P + 1, Ns * R, Tr>(sm, ld, st, tw, pt, NoHookT<Hk::kOpaque>(), sy);
   }
 }
 
 template <int N, int C, int S, bool CF, class Tr = FastTraits<N>, class Ld, class St, class PT = NoPostTw,
-          class Hk = NoHook>
+          class Hk = NoHook, class Sy = CtaSync>
 __device__ __forceinline__ void fast_tile_fft(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
-                                              const PT& pt = PT(), const Hk& hook = Hk()) {
-  fast_passes<N, C, S, CF, false, 0, 1, Tr>(sm, ld, st, tw, pt, hook);
+                                              const PT& pt = PT(), const Hk& hook = Hk(), const Sy& sy = Sy()) {
+  fast_passes<N, C, S, CF, false, 0, 1, Tr>(sm, ld, st, tw, pt, hook, sy);
 }
 
 // Variant whose first pass reads the tile from shared memory (via `ld`)
 // that later passes overwrite.
 template <int N, int C, int S, bool CF, class Tr = FastTraits<N>, class Ld, class St, class PT = NoPostTw,
-          class Hk = NoHook>
+          class Hk = NoHook, class Sy = CtaSync>
 __device__ __forceinline__ void fast_tile_fft_smem(double2* sm, const Ld& ld, const St& st,
                                                    const double2* __restrict__ tw, const PT& pt = PT(),
-                                                   const Hk& hook = Hk()) {
-  fast_passes<N, C, S, CF, true, 0, 1, Tr>(sm, ld, st, tw, pt, hook);
+                                                   const Hk& hook = Hk(), const Sy& sy = Sy()) {
+  fast_passes<N, C, S, CF, true, 0, 1, Tr>(sm, ld, st, tw, pt, hook, sy);
 }
 
 // Run passes P0.. of a tile FFT whose earlier passes were produced directly
 // in shared memory (Stockham layout after pass P0-1, Ns = NS0).
-template <int N, int C, int S, bool CF, int P0, int NS0, class St, class PT = NoPostTw, class Hk = NoHook>
+template <int N, int C, int S, bool CF, int P0, int NS0, class St, class PT = NoPostTw, class Hk = NoHook,
+          class Sy = CtaSync>
 __device__ __forceinline__ void fast_tile_fft_from(double2* sm, const St& st, const double2* __restrict__ tw,
-                                                   const PT& pt = PT(), const Hk& hook = Hk()) {
+                                                   const PT& pt = PT(), const Hk& hook = Hk(), const Sy& sy = Sy()) {
   auto no_ld = [](int, int) -> double2 { return make_double2(0.0, 0.0); };
-  fast_passes<N, C, S, CF, false, P0, NS0, FastTraits<N>>(sm, no_ld, st, tw, pt, hook);
+  fast_passes<N, C, S, CF, false, P0, NS0, FastTraits<N>>(sm, no_ld, st, tw, pt, hook, sy);
+}
+
+
+// ------------------------------------------------------------------------
+// Hybrid tile FFT for batch-minor tiles of 8 signals ([N][8] in shared
+// memory).  The passes that touch global memory (first / last) keep the
+// column-fast mapping (a warp = 4 consecutive indices x 8 signals: 128-byte
+// global runs); the passes in between use a WARP-LOCAL mapping: the N / E
+// threads that own one signal sit in one warp (E = 16, N = 512: warp w is
+// signal w), so their exchanges through shared memory need only __syncwarp.
+// A two-FFT chain kernel then has 2 CTA barriers per tile instead of 9-10,
+// and its 8 warps drift apart between them: one warp's shared-memory phase
+// overlaps another's fp64 phase instead of every warp of the CTA hitting the
+// same pipe at once.  Every element sees the same butterflies and twiddles as
+// in fast_passes (same radix schedule): results are bitwise identical.
+//
+// Layout: unpadded, XOR-swizzled.  Element (i, c) lives in 16-byte slot
+// 8 i + (c ^ h(i)), h(i) = XOR of the base-8 digits of i: a row's 8 signals
+// are 8 different bank groups (column-fast accesses), and so are 8 aligned
+// consecutive indices of one signal, also at any power-of-two stride
+// (warp-local accesses).  h is linear over disjoint bit fields, so for
+// i = j + r * stride the per-element part is a compile-time XOR constant.
+//
+// h is a GF(2)-linear map of the index bits onto 3 bank-group bits, chosen so
+// that every access pattern of the warp-local passes (8 aligned consecutive
+// indices; strides 2 ... 256; the mixed patterns of the Stockham stores with
+// Ns = 2 and 4) touches 8 distinct bank groups — checked exhaustively over
+// all radix schedules of N = 64 ... 512:
+//   h0 = i0 ^ i3 ^ i4 ^ i7,  h1 = i1 ^ i4 ^ i6 ^ i8,  h2 = i2 ^ i5 ^ i6.
+__host__ __device__ constexpr int hsw8(int i) {
+  return ((i & 7) ^ ((i >> 3) & 1) ^ ((i >> 4) & 1) * 3 ^ ((i >> 5) & 1) * 4 ^ ((i >> 6) & 1) * 6 ^ ((i >> 7) & 1) ^
+          ((i >> 8) & 1) * 2);
+}
+__device__ __forceinline__ int hidx(int i, int c) { return (i << 3) + ((c ^ hsw8(i)) & 7); }
+
+// lanes per signal of the warp-local mapping
+template <int N, class Tr>
+__host__ __device__ constexpr int hyb_lps() { return N / Tr::E; }
+// a tile FFT can run hybrid: power of two, at most 32 threads per signal
+template <int N, class Tr = FastTraits<N>>
+__host__ __device__ constexpr bool hyb_ok() {
+  return is_pow2_c(N) && N <= 512 && Tr::np >= 2 && hyb_lps<N, Tr>() <= 32 && hyb_lps<N, Tr>() >= 1;
+}
+
+// Passes P.. of the hybrid schedule.  WLMASK bit p: pass p is warp-local.
+// SRC_SMEM: the first pass's `ld` reads this tile's shared memory (in-place
+// hazard); DST_SMEM: the last pass's `st` writes shared memory.
+template <int N, int S, int P, int Ns, class Tr, unsigned WLMASK, bool SRC_SMEM, bool DST_SMEM, int P0, class Ld,
+          class St, class PT, class Hk>
+__device__ __forceinline__ void hyb_passes(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
+                                           const PT& pt, const Hk& hook) {
+  constexpr int C = 8;
+  constexpr int E = Tr::E;
+  constexpr int R = Tr::radix(P);
+  constexpr int T = N * C / E;
+  constexpr int MB = E / R;
+  constexpr int stride = N / R;
+  constexpr int LPS = N / E;
+  constexpr bool FIRST = (P == P0);
+  constexpr bool LAST = (P == Tr::np - 1);
+  constexpr bool WL = (WLMASK >> P) & 1u;
+  constexpr bool LD_FN = FIRST && P0 == 0;  // the very first pass reads through `ld`
+  const int tid = threadIdx.x;
+  double2 v[MB][R];
+#pragma unroll
+  for (int u = 0; u < MB; u++) {
+    const int c = WL ? tid / LPS : tid % C;
+    const int j = WL ? (tid % LPS) + u * LPS : tid / C + u * (T / C);
+    const int hj = (c ^ hsw8(j)) & 7;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      if constexpr (LD_FN) v[u][r] = ld(j + r * stride, c);
+      else v[u][r] = sm[((j + r * stride) << 3) + (hj ^ hsw8(r * stride))];
+    }
+  }
+  // in place: every read of the pass precedes every write of its sync domain
+  if constexpr ((!LD_FN || SRC_SMEM) && (!LAST || DST_SMEM)) {
+    if constexpr (WL) __syncwarp();
+    else __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < MB; u++) {
+    const int c = WL ? tid / LPS : tid % C;
+    const int j = WL ? (tid % LPS) + u * LPS : tid / C + u * (T / C);
+    const int k = j % Ns;
+    if constexpr (Ns > 1) {
+      constexpr int tstep = N / (Ns * R);
+      double2 w[R];
+      if constexpr (WL) twiddles_pw<R, N>(tw, k * tstep, w);  // lanes = consecutive k: contiguous runs
+      else twiddles<R>(tw, k * tstep, w);
+#pragma unroll
+      for (int r = 1; r < R; r++) v[u][r] = S < 0 ? cmul(v[u][r], w[r]) : cmulc(v[u][r], w[r]);
+    }
+    bfly_fast<R, S>(v[u]);
+    if constexpr (LAST) pt.template apply<R, stride>(c, j, v[u]);  // outputs k = j + r*stride
+    const int d = (j - k) * R + k;
+    if constexpr (LAST) {
+#pragma unroll
+      for (int r = 0; r < R; r++) st(d + r * Ns, c, v[u][r]);
+    } else {
+      const int hd = (c ^ hsw8(d)) & 7;
+#pragma unroll
+      for (int r = 0; r < R; r++) sm[((d + r * Ns) << 3) + (hd ^ hsw8(r * Ns))] = v[u][r];
+    }
+  }
+  if constexpr (!LAST) {
+    constexpr bool WLN = (WLMASK >> (P + 1)) & 1u;
+    if constexpr (FIRST && Hk::kActive) hook();
+    if constexpr (WL && WLN) __syncwarp();
+    else __syncthreads();
+    if constexpr (FIRST && Hk::kActive) hook.after();
+    hyb_passes<N, S, P + 1, Ns * R, Tr, WLMASK, SRC_SMEM, DST_SMEM, P0>(sm, ld, st, tw, pt, NoHook());
+  }
+}
+
+// whole tile FFT, first pass through `ld`
+template <int N, int S, class Tr, unsigned WLMASK, bool SRC_SMEM, bool DST_SMEM, class Ld, class St,
+          class PT = NoPostTw, class Hk = NoHook>
+__device__ __forceinline__ void hyb_tile_fft(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
+                                             const PT& pt = PT(), const Hk& hook = Hk()) {
+  hyb_passes<N, S, 0, 1, Tr, WLMASK, SRC_SMEM, DST_SMEM, 0>(sm, ld, st, tw, pt, hook);
+}
+// passes P0.. of a tile FFT whose earlier passes were produced directly in
+// shared memory (swizzled Stockham layout after pass P0 - 1, Ns = NS0)
+template <int N, int S, class Tr, unsigned WLMASK, int P0, int NS0, class St, class PT = NoPostTw>
+__device__ __forceinline__ void hyb_tile_fft_from(double2* sm, const St& st, const double2* __restrict__ tw,
+                                                  const PT& pt = PT()) {
+  auto no_ld = [](int, int) -> double2 { return make_double2(0.0, 0.0); };
+  hyb_passes<N, S, P0, NS0, Tr, WLMASK, true, false, P0>(sm, no_ld, st, tw, pt, NoHook());
+}
+// warp-local mask: every pass but the first (when it reads global memory)
+// and the last (when it writes global memory)
+template <class Tr>
+__host__ __device__ constexpr unsigned hyb_mask(bool first_global, bool last_global) {
+  unsigned m = (1u << Tr::np) - 1u;
+  if (first_global) m &= ~1u;
+  if (last_global) m &= ~(1u << (Tr::np - 1));
+  return m;
 }
 
 // the last-pass stride (= N / radix of the last pass) of a fast tile FFT

@@ -504,9 +504,17 @@ def test_one_cta_small_solves(P):
     plan = nf.build_plan(grid, prm)
     oplan = O.Plan.build(t, prm.damping_a, 2)
     L = _lib.load()
+    import torch
+
+    xdev = torch.from_numpy(data[1]).to("cuda")
+    before = L.nfft45_launch_count()
+    got5_dev = nf.refine_type5(plan, xdev, passes=1)
+    assert L.nfft45_launch_count() - before == 1  # device operand: the whole solve is ONE kernel
     before = L.nfft45_launch_count()
     got5 = nf.refine_type5(plan, data[1], passes=1)
-    assert L.nfft45_launch_count() - before == 1
+    # numpy operand (host pipeline): the same kernel plus the device-side finiteness check
+    assert L.nfft45_launch_count() - before == 2
+    assert np.array_equal(got5_dev.cpu().numpy(), got5)
     got4 = nf.refine_type4(plan, data[1], passes=1)
     assert rel(O.refine5(oplan, data[1], 1), got5) <= G1 and rel(O.refine4(oplan, data[1], 1), got4) <= G1
     assert rel(data[1], O.type2(got5, t)) <= G1 and rel(data[1], O.type1(t, got4, P)) <= G1
