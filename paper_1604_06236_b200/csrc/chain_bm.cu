@@ -400,6 +400,163 @@ __global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<
   hyb_tile_fft<R, -1, Tr, hyb_mask<Tr>(false, true), true, false>(sm, ld2, st2, tw, pt);
 }
 
+// kbm_mid_h with the handoff between the two transforms kept in REGISTERS:
+// for an all-radix-16 schedule (R = 256) the last pass of the IFFT leaves
+// thread (signal c, j) with X[j + 16 r], r < 16 -- exactly the inputs of
+// butterfly j of the FFT's first pass -- so IFFT pass 1, the ks product and
+// FFT pass 0 run back to back on one register tile: 2 shared-memory round
+// trips per tile instead of 3, same arithmetic per element (bitwise identical).
+template <int R, int C>
+__host__ __device__ constexpr bool bm_mid_fused() {
+  return bm_hyb<R, C>() && FastTraits<R>::rem == 0 && FastTraits<R>::np == 2;
+}
+
+template <int R, int C>
+__global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<R, kSig>())) kbm_mid_hf(
+    const double2* __restrict__ U, double2* __restrict__ Z, int64_t Bp, const double2* __restrict__ tw,
+    const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
+    const double2* __restrict__ ks) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
+  using Tr = FastTraits<R>;
+  static_assert(Tr::np == 2 && Tr::rem == 0, "fused handoff: schedule 16 x 16");
+  constexpr int LPS = R / 16;  // lanes per signal = stride of the radix-16 passes
+  extern __shared__ double2 sm[];
+  double2* s_ks = sm + R * kSig;
+  const int r = blockIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * kSig;
+  for (int k2 = threadIdx.x; k2 < R; k2 += blockDim.x) cpa16(&s_ks[k2], &ks[(int64_t)r + (int64_t)C * k2]);
+  cpa_commit();
+  const unsigned ub = (unsigned)Bp;  // 32-bit in-tile offsets (see kbm_col)
+  const double2* __restrict__ Ut = U + (int64_t)r * R * Bp + b0;
+  double2* __restrict__ Zt = Z + (int64_t)r * Bp + b0;
+  auto ld1 = [&](int i, int c) -> double2 { return Ut[(unsigned)i * ub + c]; };
+  constexpr unsigned mask = 0x2u;  // pass 0 column-fast (global), pass 1 warp-local
+  hyb_tile_fft_head<R, +1, Tr, mask, 1>(sm, ld1, tw, CpAsyncWaitHook());  // ends with a CTA barrier
+  {
+    const int tid = threadIdx.x;
+    const int c = tid / LPS, j = tid % LPS;
+    const int hj = (c ^ hsw8(j)) & 7;
+    double2 v[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) v[q] = sm[((j + q * LPS) << 3) + (hj ^ hsw8(q * LPS))];
+    __syncwarp();  // the signal's lanes have read before any of them overwrites
+    {  // IFFT pass 1: Ns = R / 16 (k = j), twiddle step 1
+      double2 w[16];
+      twiddles_pw<16, R>(tw, j, w);
+#pragma unroll
+      for (int q = 1; q < 16; q++) v[q] = cmulc(v[q], w[q]);
+    }
+    bfly_fast<16, +1>(v);  // v[q] = X[j + q LPS]
+#pragma unroll
+    for (int q = 0; q < 16; q++) v[q] = cmul(v[q], s_ks[j + q * LPS]);
+    bfly_fast<16, -1>(v);  // FFT pass 0 (no twiddles): outputs at 16 j + q
+    const int d = j * 16;
+    const int hd = (c ^ hsw8(d)) & 7;
+#pragma unroll
+    for (int q = 0; q < 16; q++) sm[((d + q) << 3) + (hd ^ hsw8(q))] = v[q];
+  }
+  __syncthreads();  // the last pass is column-fast
+  auto st2 = [&](int k, int c, double2 v) { Zt[(unsigned)(k * C) * ub + c] = v; };
+  const FourStepTw<-1> pt{loP, hiP, sP, twQ, Q, r, 0};
+  hyb_tile_fft_from<R, -1, Tr, 0x0u, 1, 16>(sm, st2, tw, pt);
+}
+
+// kbm_band_h with the band handoff in registers: after the last (radix-16)
+// pass of the row FFT_2P (2C = 512) thread (signal c, j < 32) holds
+// X[j + 32 r]; the in-band half, m1 = j + 32 s (s < 8), is exactly the input
+// of butterflies j and j + 32 of the column IFFT_P's first (radix-4) pass.
+template <int R, int C>
+__host__ __device__ constexpr bool bm_band_fused() {
+  return bm_hyb<R, C>() && C == 256;  // FFT_512 = 2 x 16 x 16, IFFT_256 = 4 x 8 x 8
+}
+
+template <int R, int C>
+__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_band_hf(
+    const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
+    const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
+    const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
+    const double* __restrict__ dd, const double2* __restrict__ sub, double2* __restrict__ rsave) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
+  constexpr int NR = 2 * C;
+  constexpr int SG = kSig;
+  using TrA = FastTraits<NR>;
+  using TrB = HalfTr<C>;
+  static_assert(NR == 512 && TrA::np == 3 && TrB::np == 3 && TrB::radix(0) == 4, "fused band handoff: 512 / 256");
+  extern __shared__ double2 sm[];
+  double* s_t0 = reinterpret_cast<double*>(sm + NR * SG);
+  double* s_t1 = s_t0 + C;
+  double2* s_sb = reinterpret_cast<double2*>(s_t1 + C);
+  const int k1 = blockIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * SG;
+  for (int m1 = threadIdx.x; m1 < C; m1 += blockDim.x) {
+    const int64_t p = (int64_t)k1 + (int64_t)R * m1;
+    if (sub) {
+      cpa8(&s_t0[m1], &deconv[p]);
+      cpa8(&s_t1[m1], &decay[p]);
+    } else {
+      cpa8(&s_t0[m1], &dd[p]);
+    }
+  }
+  if (sub)  // subtrahend tile, swizzled like the data tile (it is read by warp-local lanes)
+    for (int e = threadIdx.x; e < C * SG; e += blockDim.x)
+      cpa16(&s_sb[hidx(e / SG, e % SG)], &sub[((int64_t)k1 + (int64_t)R * (e / SG)) * Bp + b0 + e % SG]);
+  cpa_commit();
+  const unsigned ub = (unsigned)Bp;  // 32-bit in-tile offsets (see kbm_col)
+  const double2* __restrict__ Tt = T + (int64_t)k1 * NR * Bp + b0;
+  double2* __restrict__ Ut = U + (int64_t)k1 * Bp + b0;
+  auto ld1 = [&](int i, int c) -> double2 { return Tt[(unsigned)i * ub + c]; };
+  constexpr unsigned maskA = 0x6u;  // pass 0 column-fast (global), passes 1, 2 warp-local
+  hyb_tile_fft_head<NR, -1, TrA, maskA, 2>(sm, ld1, twR, CpAsyncWaitHook());  // passes 0, 1 (+ warp sync)
+  {
+    const int tid = threadIdx.x;
+    const int c = tid >> 5, j = tid & 31;  // warp = signal
+    const int hj = (c ^ hsw8(j)) & 7;
+    double2 v[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) v[q] = sm[((j + q * 32) << 3) + (hj ^ hsw8(q * 32))];
+    __syncwarp();
+    {  // FFT_512 pass 2: Ns = 32 (k = j), twiddle step 1
+      double2 w[16];
+      twiddles_pw<16, NR>(twR, j, w);
+#pragma unroll
+      for (int q = 1; q < 16; q++) v[q] = cmul(v[q], w[q]);
+    }
+    bfly_fast<16, -1>(v);  // v[q] = X[k2 = j + 32 q]
+    // band: m1 = (k2 + C/2) mod 2C = j + 32 s with s = (q + 4) mod 16 < 8
+    double2 u[8];
+#pragma unroll
+    for (int s8 = 0; s8 < 8; s8++) {
+      const int m1 = j + 32 * s8;
+      double2 x = v[(s8 + 12) & 15];
+      if (sub) {
+        x = rsc(x, s_t0[m1]);
+        x = csub(x, s_sb[hidx(m1, c)]);
+        if (rsave) rsave[((int64_t)k1 + (int64_t)R * m1) * Bp + b0 + c] = x;  // r itself (norms, passes >= 2)
+        x = rsc(x, s_t1[m1]);
+      } else {
+        x = rsc(x, s_t0[m1]);
+      }
+      u[s8] = x;
+    }
+    // column IFFT_P pass 0 (radix 4, stride 64): butterflies j (s = 0, 2, 4, 6) and j + 32 (s = 1, 3, 5, 7)
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      double2 x0 = u[h], x1 = u[2 + h], x2 = u[4 + h], x3 = u[6 + h];
+      bfly4<+1>(x0, x1, x2, x3);
+      const int d = (j + 32 * h) * 4;
+      const int hd = (c ^ hsw8(d)) & 7;
+      sm[((d + 0) << 3) + (hd ^ hsw8(0))] = x0;
+      sm[((d + 1) << 3) + (hd ^ hsw8(1))] = x1;
+      sm[((d + 2) << 3) + (hd ^ hsw8(2))] = x2;
+      sm[((d + 3) << 3) + (hd ^ hsw8(3))] = x3;
+    }
+  }
+  __syncwarp();  // pass 1 of the IFFT is warp-local
+  auto st2 = [&](int k1p, int c, double2 v) { Ut[(unsigned)(k1p * R) * ub + c] = v; };
+  const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, k1, 0};
+  hyb_tile_fft_from<C, +1, TrB, 0x2u, 1, 4>(sm, st2, twC, pt);  // pass 1 warp-local, pass 2 column-fast
+}
+
 // XOUT: the tile also stores x (coalesced rows), so the last pass of the
 // C-point FFT keeps the column-fast mapping and is followed by a CTA barrier.
 template <int R, int C, bool XOUT>
@@ -772,6 +929,11 @@ template __global__ void kbm_band_h<NFFT45_EXP_RC>(const double2*, double2*, int
                                               const double*, const double2*, double2*);
 template __global__ void kbm_mid_h<NFFT45_EXP_RC>(const double2*, double2*, int64_t, const double2*, const double2*, const double2*,
                                              int, const double2*, int, const double2*);
+template __global__ void kbm_band_hf<NFFT45_EXP_RC>(const double2*, double2*, int64_t, const double2*, const double2*, const double2*,
+                                               const double2*, int, const double2*, int, const double*, const double*,
+                                               const double*, const double2*, double2*);
+template __global__ void kbm_mid_hf<NFFT45_EXP_RC>(const double2*, double2*, int64_t, const double2*, const double2*, const double2*,
+                                              int, const double2*, int, const double2*);
 template __global__ void kbm_pad_h<NFFT45_EXP_RC, false>(const double2*, double2*, int64_t, const double2*, const double2*,
                                                     const double2*, const double2*, int, const double2*, int,
                                                     const double*, const double*, const double*, const double2*, double2*);
@@ -834,6 +996,7 @@ struct ChainBM {
   bool sw = false;           // grid order: signal groups fastest (blockIdx.x) instead of tile index
   int pf = 0;                // L2 prefetch distance in launch slots (0: off)
   bool hyb = false;          // hybrid two-FFT kernels (warp-local middle passes), when bm_hyb<R, C>()
+  bool fuse = true;          // register handoff between the two transforms of band / mid (NFFT45_FUSE=0: off)
   // grid of (tiles x groups*mult); with sw the signal groups run fastest
   dim3 gdim(int tiles, int mult = 1) const {
     return sw ? dim3(groups * mult, (unsigned)tiles) : dim3((unsigned)tiles, groups * mult);
@@ -877,6 +1040,8 @@ struct ChainBM {
   int band_h(const double2* T_, double2* U, const ChainPlanView& pv, const double2* sub, double2* rsave) {
     if constexpr (bm_hyb<R, C>()) {
       auto bm_band = kbm_band_h<R, C>;
+      if constexpr (bm_band_fused<R, C>())
+        if (fuse) bm_band = kbm_band_hf<R, C>;  // band handoff in registers
       const size_t smem = sizeof(double2) * 2 * C * kSig + 2 * sizeof(double) * C + (sub ? sizeof(double2) * C * kSig : 0);
       NFFT_CHECK(bm_attr(bm_band, smem));
       constexpr int T = fast_threads<2 * C, kSig>();
@@ -897,6 +1062,8 @@ struct ChainBM {
   int mid_h(const double2* U, double2* Z, const ChainPlanView& pv) {
     if constexpr (bm_hyb<R, C>()) {
       auto bm_mid = kbm_mid_h<R, C>;
+      if constexpr (bm_mid_fused<R, C>())
+        if (fuse) bm_mid = kbm_mid_hf<R, C>;  // IFFT -> ks -> FFT handoff in registers
       constexpr size_t smem = sizeof(double2) * R * kSig + sizeof(double2) * R;
       NFFT_CHECK(bm_attr(bm_mid, smem));
       constexpr int T = fast_threads<R, kSig>();
@@ -1085,6 +1252,8 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
     // passes); NFFT45_HYB=0 restores the all-column-fast kernels for A/B runs
     static const bool hyb_on = !(getenv("NFFT45_HYB") && atoi(getenv("NFFT45_HYB")) == 0);
     ch.hyb = hyb_on && bm_hyb<R, C>() && !ch.small_tiles;
+    static const bool fuse_on = !(getenv("NFFT45_FUSE") && atoi(getenv("NFFT45_FUSE")) == 0);
+    ch.fuse = fuse_on;
   }
   int status = NFFT45_OK;
   {

@@ -407,7 +407,7 @@ __host__ __device__ constexpr bool hyb_ok() {
 // SRC_SMEM: the first pass's `ld` reads this tile's shared memory (in-place
 // hazard); DST_SMEM: the last pass's `st` writes shared memory.
 template <int N, int S, int P, int Ns, class Tr, unsigned WLMASK, bool SRC_SMEM, bool DST_SMEM, int P0, class Ld,
-          class St, class PT, class Hk>
+          class St, class PT, class Hk, int PEND = Tr::np>
 __device__ __forceinline__ void hyb_passes(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
                                            const PT& pt, const Hk& hook) {
   constexpr int C = 8;
@@ -470,8 +470,22 @@ __device__ __forceinline__ void hyb_passes(double2* sm, const Ld& ld, const St& 
     if constexpr (WL && WLN) __syncwarp();
     else __syncthreads();
     if constexpr (FIRST && Hk::kActive) hook.after();
-    hyb_passes<N, S, P + 1, Ns * R, Tr, WLMASK, SRC_SMEM, DST_SMEM, P0>(sm, ld, st, tw, pt, NoHook());
+    // PEND < np: the caller runs the remaining passes itself (fused handoff
+    // to the next transform in registers); the boundary sync above is done
+    if constexpr (P + 1 < PEND)
+      hyb_passes<N, S, P + 1, Ns * R, Tr, WLMASK, SRC_SMEM, DST_SMEM, P0, Ld, St, PT, NoHook, PEND>(sm, ld, st, tw, pt,
+                                                                                                  NoHook());
   }
+}
+
+// passes 0 .. PEND-1 of a tile FFT (all of them write shared memory); ends
+// with the sync that pass PEND's mapping (WLMASK bit PEND) needs
+template <int N, int S, class Tr, unsigned WLMASK, int PEND, class Ld, class Hk = NoHook>
+__device__ __forceinline__ void hyb_tile_fft_head(double2* sm, const Ld& ld, const double2* __restrict__ tw,
+                                                  const Hk& hook = Hk()) {
+  auto no_st = [](int, int, double2) {};
+  hyb_passes<N, S, 0, 1, Tr, WLMASK, false, true, 0, Ld, decltype(no_st), NoPostTw, Hk, PEND>(sm, ld, no_st, tw,
+                                                                                              NoPostTw(), hook);
 }
 
 // whole tile FFT, first pass through `ld`

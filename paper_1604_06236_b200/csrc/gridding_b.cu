@@ -10,8 +10,10 @@
 // results are bitwise reproducible and independent of the batch split.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "ops.cuh"
+#include "tma.cuh"
 
 namespace nfft45 {
 
@@ -748,12 +750,14 @@ template <bool OUT_BM, int SUBM, int SIG>  // SUBM: 0 none, 1 batch-minor, 2 sig
 __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 ? 4 : 5)) k_gather_p(
     const double* __restrict__ ts, const int* __restrict__ perm, int64_t Q, int64_t n, double alpha, GaussTab G,
     const double2* __restrict__ H, int64_t H_ld, int64_t batch, NodeFactor nf, const double2* __restrict__ sub,
-    int64_t sub_ld, int mode, double2* __restrict__ out, int64_t out_ld, int ngroups, int* __restrict__ overflow, int sw) {
+    int64_t sub_ld, int mode, double2* __restrict__ out, int64_t out_ld, int ngroups, int* __restrict__ overflow, int sw,
+    const __grid_constant__ CUtensorMap tmH, int tma) {
   pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int HALVES = 32 / SIG, NPL = kNPW / HALVES;
   static_assert(kGatherNodes == 32, "one node per lane in the signal-major staging");
-  extern __shared__ __align__(16) unsigned char smraw[];
-  double2* Y = reinterpret_cast<double2*>(smraw);                     // [kGPSpan][SIG]
+  extern __shared__ __align__(128) unsigned char smraw_gp[];  // own symbol: 128-byte aligned for the TMA box
+  __shared__ __align__(8) uint64_t s_bar;  // TMA completion (transaction count) of the staged cell tile
+  double2* Y = reinterpret_cast<double2*>(smraw_gp);                     // [kGPSpan][SIG]
   double* WT = reinterpret_cast<double*>(Y + kGPSpan * SIG);           // [warps][kWTSpan][8]
   double2* Sb = reinterpret_cast<double2*>(WT + kGatherWarps * kWTSpan * kNPW);  // [nodes][SIG] (SUBM == 2)
   double2* O = Sb + (SUBM == 2 ? kGatherNodes * SIG : 0);              // [nodes][SIG] (!OUT_BM)
@@ -763,6 +767,10 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
   __shared__ int s_pq[kGatherNodes];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    mbar_fence_init();
+  }
   // sw: slices (signal-group walkers) fastest in the grid, node blocks second
   const unsigned bx = sw ? blockIdx.y : blockIdx.x, by = sw ? blockIdx.x : blockIdx.y;
   const unsigned gy = sw ? gridDim.x : gridDim.y;
@@ -805,14 +813,30 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
   // signal-major operands: this thread's node (lane) and first signal (warp)
   const int64_t my_off = (int64_t)warp * Q + (lane < nq ? s_pq[lane] : 0);
   const double2* sb_src = sub + my_off;
+  // Cell tile of a signal group: ONE bulk tensor copy (TMA, SASS UTMALDG)
+  // issued by thread 0 when the block's cell span does not wrap around the
+  // period -- the copy bypasses the LSU data pipe, which bounds this kernel
+  // (an LDGSTS costs twice the pipe cycles of an LDS of the same bytes); rows
+  // past the block's span and signals past the padded batch arrive as zeros /
+  // unused rows.  Blocks that wrap keep the per-thread cp.async copies.
+  const bool tma_blk = tma && cs >= 0 && ce < ni;
+  constexpr unsigned kBoxBytes = (unsigned)(kGPSpan * SIG * sizeof(double2));
   auto stage = [&](int64_t g) {
     const int64_t b0 = g * SIG;
-    const bool ok = b0 + sl < batch;
-    const double2* col = H + b0 + (ok ? sl : 0);
-    for (int c = warp * HALVES + hf; c < len; c += kGatherWarps * HALVES) {
-      int cell = cs + c;
-      cell = cell < 0 ? cell + ni : (cell >= ni ? cell - ni : cell);
-      cp_async16(&Y[c * SIG + sl], col + (int64_t)cell * H_ld, ok);
+    if (tma_blk) {
+      if (tid == 0) {
+        fence_proxy_async();  // the previous group's generic reads of Y precede the async refill
+        mbar_expect_tx(&s_bar, kBoxBytes);
+        tma_load_2d(Y, &tmH, (int)(2 * b0), cs, &s_bar);
+      }
+    } else {
+      const bool ok = b0 + sl < batch;
+      const double2* col = H + b0 + (ok ? sl : 0);
+      for (int c = warp * HALVES + hf; c < len; c += kGatherWarps * HALVES) {
+        int cell = cs + c;
+        cell = cell < 0 ? cell + ni : (cell >= ni ? cell - ni : cell);
+        cp_async16(&Y[c * SIG + sl], col + (int64_t)cell * H_ld, ok);
+      }
     }
     if (SUBM == 2 && mode != 0) {  // node = lane, signals warp + 4k: one base pointer, stride 4Q
 #pragma unroll
@@ -829,9 +853,14 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
   const double2* __restrict__ yw = Y + (w_lo - cs) * SIG + sl;
   const double2* __restrict__ wr0 = reinterpret_cast<const double2*>(wt) + hf * (NPL / 2);
   const int e0 = warp * kNPW + hf * NPL;  // node of acc[0]
+  unsigned phase = 0;
   for (; g < ngroups; g += gy) {
     const int64_t b0 = g * SIG;
     cp_async_wait_group<0>();
+    if (tma_blk) {
+      mbar_wait(&s_bar, phase);
+      phase ^= 1u;
+    }
     __syncthreads();
     double2 acc[NPL];
 #pragma unroll
@@ -965,12 +994,18 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
                 (subm == 2 ? (size_t)kGatherNodes * SIG * 16 : 0) + (out_ld ? 0 : (size_t)kGatherNodes * SIG * 16);
   const dim3 grid = sw ? dim3((unsigned)slices, (unsigned)nblk) : dim3((unsigned)nblk, (unsigned)slices);
   GaussTab G = gauss_tab(win);
+  // TMA-staged cell tiles (NFFT45_GATHER_TMA=0: per-thread cp.async copies, for A/B runs)
+  static const int use_tma = !(getenv("NFFT45_GATHER_TMA") && atoi(getenv("NFFT45_GATHER_TMA")) == 0);
+  CUtensorMap tmH;
+  memset(&tmH, 0, sizeof(tmH));
+  int tma = use_tma && (reinterpret_cast<uintptr_t>(H) % 16 == 0) && n >= kGPSpan;
+  if (tma) NFFT_CHECK(tma_map_rows(&tmH, H, n, H_ld, kGPSpan, SIG));
 #define NFFT_GP_LAUNCH(OBM, SM_, S_)                                                                           \
   {                                                                                                          \
     auto gather_p = k_gather_p<OBM, SM_, S_>;                                                                \
     NFFT_CUDA(cudaFuncSetAttribute(gather_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
     LAUNCH_PDL(gather_p, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, H_ld, batch, f,  \
-           sub, sub_ld, mode, out, out_ld, ngroups, overflow, sw);                                           \
+           sub, sub_ld, mode, out, out_ld, ngroups, overflow, sw, tmH, tma);                                 \
   }
 #define NFFT_GP_SUB(OBM, S_) \
   if (subm == 0) NFFT_GP_LAUNCH(OBM, 0, S_) else if (subm == 1) NFFT_GP_LAUNCH(OBM, 1, S_) else NFFT_GP_LAUNCH(OBM, 2, S_)
