@@ -557,6 +557,211 @@ __global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_thre
   hyb_tile_fft_from<C, +1, TrB, 0x2u, 1, 4>(sm, st2, twC, pt);  // pass 1 warp-local, pass 2 column-fast
 }
 
+// kbm_pad_h (no x output) with the zero-padding handoff done by ONE warp
+// shuffle exchange: after the last (radix-8) pass of the row FFT_P (C = 256)
+// lane j of the signal's warp holds S[k2 = j + 32 r]; butterfly j' = 2a + b of
+// the first computed pass (radix 16, Ns = 2) of the zero-padded IFFT_2P needs
+// V[s] = S[a + 16 s], s < 16 -- the values of lanes a (even s) and a + 16
+// (odd s) -- as inputs q -> V[(q + 8) & 15] (times (-1)^b for q >= 8: the
+// radix-2 first pass over the zero half is a copy, see kbm_pad).  Lanes a and
+// a + 16 swap their eight values (__shfl_xor 16) and run butterflies b = 0 and
+// b = 1: the padded tile is never written and re-read (8 instead of 12
+// half-tile shared-memory transfers per tile).  Same arithmetic per element.
+template <int R, int C>
+__host__ __device__ constexpr bool bm_pad_fused() {
+  return bm_hyb<R, C>() && C == 256;  // FFT_256 = 4 x 8 x 8, IFFT_512 = (2) x 16 x 16
+}
+
+__device__ __forceinline__ double2 shfl_xor16(double2 v) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, 16), __shfl_xor_sync(0xffffffffu, v.y, 16));
+}
+
+struct PadHfArgs {
+  double2* Y;
+  int64_t Bp;
+  const double2 *twR, *twC, *loN, *hiN;
+  int sN;
+  const double2* twQ;
+  int Q;
+  const double* cd;
+  int ntiles, groups;
+};
+
+// one tile (row r, signals b0 ..) of the fused pad; `ld1` reads the tile's Z
+// rows (global memory, or a TMA-staged dense copy), `sy` is the CTA or one
+// tile group of a persistent CTA
+template <int R, int C, class Ld, class Hk, class Sy>
+__device__ __forceinline__ void pad_hf_tile(const PadHfArgs& a, double2* sm, double* s_t0, const Ld& ld1,
+                                            const Hk& hook, int r, int64_t b0, const Sy& sy) {
+  constexpr int NC = 2 * C;
+  using TrA = HalfTr<C>;
+  using TrB = FastTraits<NC>;
+  static_assert(NC == 512 && TrA::np == 3 && TrA::radix(2) == 8 && TrB::np == 3 && TrB::radix(0) == 2,
+                "fused pad handoff: 256 / 512");
+  const unsigned ub = (unsigned)a.Bp;
+  double2* __restrict__ Yt = a.Y + (int64_t)r * a.Bp + b0;
+  hyb_tile_fft_head<C, -1, TrA, 0x6u, 2>(sm, ld1, a.twR, hook, sy);  // passes 0 (global / staged), 1 (+ warp sync)
+  {
+    const int tid = sy.tid();
+    const int c = tid >> 5, j = tid & 31;  // warp = signal
+    const int hj = (c ^ hsw8(j)) & 7;
+    double2 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) v[q] = sm[((j + q * 32) << 3) + (hj ^ hsw8(q * 32))];
+    __syncwarp();
+    {  // FFT_256 pass 2 (radix 8): Ns = 32 (k = j), twiddle step 1
+      double2 w[8];
+      twiddles_pw<8, C>(a.twR, j, w);
+#pragma unroll
+      for (int q = 1; q < 8; q++) v[q] = cmul(v[q], w[q]);
+    }
+    bfly_fast<8, -1>(v);  // v[q] = S[k2 = j + 32 q]
+#pragma unroll
+    for (int q = 0; q < 8; q++) v[q] = rsc(v[q], s_t0[j + 32 * q]);
+    // V[s] = S[a + 16 s]: even s from lane a, odd s from lane a + 16
+    const int la = j & 15, b = j >> 4;
+    double2 in[16];
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const double2 o = shfl_xor16(v[q]);
+      const double2 ev = b ? o : v[q];  // V[2 q]
+      const double2 od = b ? v[q] : o;  // V[2 q + 1]
+      // input q' of the butterfly = V[(q' + 8) & 15], negated for q' >= 8 when b = 1
+      const int qe = (2 * q + 8) & 15, qo = (2 * q + 1 + 8) & 15;
+      in[qe] = (qe >= 8 && b) ? make_double2(-ev.x, -ev.y) : ev;
+      in[qo] = (qo >= 8 && b) ? make_double2(-od.x, -od.y) : od;
+    }
+    {  // IFFT_512 pass 1 (radix 16): Ns = 2 (k = b), twiddle step 16
+      double2 w[16];
+      twiddles_pw<16, NC>(a.twC, b * 16, w);
+#pragma unroll
+      for (int q = 1; q < 16; q++) in[q] = cmulc(in[q], w[q]);
+    }
+    bfly_fast<16, +1>(in);
+    const int d = 32 * la + b;  // (j' - k) * 16 + k with j' = 2 a + b
+    const int hd = (c ^ hsw8(d)) & 7;
+#pragma unroll
+    for (int q = 0; q < 16; q++) sm[((d + 2 * q) << 3) + (hd ^ hsw8(2 * q))] = in[q];
+  }
+  sy.sync();  // the last pass is column-fast
+  auto st2 = [&](int k, int c, double2 v) { Yt[(unsigned)(k * R) * ub + c] = v; };
+  const FourStepTw<+1> pt{a.loN, a.hiN, a.sN, a.twQ, a.Q, r, 0};
+  hyb_tile_fft_from<NC, +1, TrB, 0x0u, 2, 32>(sm, st2, a.twC, pt, sy);
+}
+
+template <int R, int C>
+__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_pad_hf(
+    const double2* __restrict__ Z, const __grid_constant__ PadHfArgs a) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
+  constexpr int NC = 2 * C;
+  extern __shared__ double2 sm[];
+  double* s_t0 = reinterpret_cast<double*>(sm + NC * kSig);
+  const int r = blockIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * kSig;
+  const unsigned ub = (unsigned)a.Bp;
+  const double2* __restrict__ Zt = Z + (int64_t)r * C * a.Bp + b0;
+  for (int k2 = threadIdx.x; k2 < C; k2 += blockDim.x) cpa8(&s_t0[k2], &a.cd[(int64_t)r + (int64_t)R * k2]);
+  cpa_commit();
+  auto ld1 = [&](int i, int c) -> double2 { return Zt[(unsigned)i * ub + c]; };
+  pad_hf_tile<R, C>(a, sm, s_t0, ld1, CpAsyncWaitHook(), r, b0, CtaSync());
+}
+
+// Persistent form of kbm_pad_hf: ONE CTA per SM made of two tile groups of
+// 256 threads (named barriers), each with its own work tile, table slot, TMA
+// staging buffer and mbarrier.  A group's next Z tile is requested (one bulk
+// tensor copy, SASS UTMALDG) right after its first pass has consumed the
+// staged one, so the tile's DRAM latency hides under the current tile's
+// remaining passes and no registers idle behind a load.  The tile body is a
+// real call: inlined into the loop, ptxas keeps ~30 more registers live across
+// the barriers and spills > 1 KB per thread.
+// First-pass hook of the persistent kernels: wait for this thread's cp.async
+// table copies before the group barrier; after it (every thread of the group
+// has pulled the staged tile into registers) thread 0 refills the staging
+// buffer with the group's next tile of ROWS rows.
+template <int ROWS>
+struct TmaRefill {
+  static constexpr bool kActive = true;
+  static constexpr bool kOpaque = false;
+  const CUtensorMap* map;
+  double2* dst;
+  uint64_t* bar;
+  int tn, ntiles, groups;
+  int tid;
+  __device__ __forceinline__ void operator()() const { asm volatile("cp.async.wait_all;\n" ::); }
+  __device__ __forceinline__ void after() const {
+    if (tid == 0 && tn < ntiles) {
+      fence_proxy_async();  // the group's generic reads of the buffer precede the async refill
+      mbar_expect_tx(bar, (unsigned)(ROWS * kSig * sizeof(double2)));
+      tma_load_2d(dst, map, 2 * kSig * (tn % groups), ROWS * (tn / groups), bar);
+    }
+  }
+};
+
+template <int R, int C>
+struct PadHpLayout {
+  static constexpr size_t kWork = sizeof(double2) * 2 * C * kSig + sizeof(double) * C;  // tile + cd slot
+  static constexpr size_t kStage = sizeof(double2) * C * kSig;                          // dense TMA box
+  static constexpr size_t kGroup = (kWork + kStage + 127) / 128 * 128;
+  static constexpr size_t kBytes = 2 * kGroup + 16;
+};
+
+template <int R, int C>
+__device__ __noinline__ bool pad_hp_body(const CUtensorMap* tmZ, const PadHfArgs* ap, unsigned char* smraw, int it) {
+  constexpr int T = fast_threads<2 * C, kSig>();
+  using L = PadHpLayout<R, C>;
+  const PadHfArgs& a = *ap;
+  const int g = threadIdx.x / T;
+  const GroupSync<T> sy{g, (int)threadIdx.x - g * T};
+  const int stride = 2 * gridDim.x;
+  const int t = 2 * blockIdx.x + g + it * stride;
+  if (t >= a.ntiles) return false;
+  double2* inb = reinterpret_cast<double2*>(smraw + g * L::kGroup);  // [C][8] dense (TMA box), 128-byte aligned
+  double2* sm = reinterpret_cast<double2*>(smraw + g * L::kGroup + L::kStage);
+  double* s_t0 = reinterpret_cast<double*>(sm + 2 * C * kSig);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * L::kGroup) + g;
+  const int r = t / a.groups;
+  const int64_t b0 = (int64_t)(t % a.groups) * kSig;
+  sy.sync();  // the group's previous tile is done with `sm` and the table slot
+  for (int k2 = sy.t; k2 < C; k2 += T) cpa8(&s_t0[k2], &a.cd[(int64_t)r + (int64_t)R * k2]);
+  cpa_commit();
+  mbar_wait(bar, it & 1);
+  const TmaRefill<C> hook{tmZ, inb, bar, t + stride, a.ntiles, a.groups, sy.t};
+  auto ld1 = [&](int i, int c) -> double2 { return inb[i * kSig + c]; };
+  pad_hf_tile<R, C>(a, sm, s_t0, ld1, hook, r, b0, sy);
+  return true;
+}
+
+template <int R, int C>
+__global__ void __launch_bounds__(2 * fast_threads<2 * C, kSig>(), 1) kbm_pad_hp(
+    const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ PadHfArgs a) {
+  constexpr int T = fast_threads<2 * C, kSig>();
+  using L = PadHpLayout<R, C>;
+  extern __shared__ __align__(128) unsigned char smraw_hp[];
+  {
+    const int g = threadIdx.x / T;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw_hp + 2 * L::kGroup) + g;
+    if ((int)threadIdx.x - g * T == 0) {
+      if (g == 0) tma_prefetch_desc(&tmZ);
+      mbar_init(bar, 1);
+      mbar_fence_init();
+    }
+  }
+  __syncthreads();
+  pdl_enter();  // programmatic dependent launch: Z is the producer's output
+  {
+    const int g = threadIdx.x / T;
+    const int t = 2 * blockIdx.x + g;
+    if ((int)threadIdx.x - g * T == 0 && t < a.ntiles) {
+      uint64_t* bar = reinterpret_cast<uint64_t*>(smraw_hp + 2 * L::kGroup) + g;
+      mbar_expect_tx(bar, (unsigned)L::kStage);
+      tma_load_2d(smraw_hp + g * L::kGroup, &tmZ, 2 * kSig * (t % a.groups), C * (t / a.groups), bar);
+    }
+  }
+#pragma unroll 1
+  for (int it = 0; pad_hp_body<R, C>(&tmZ, &a, smraw_hp, it); it++) {
+  }
+}
+
 // XOUT: the tile also stores x (coalesced rows), so the last pass of the
 // C-point FFT keeps the column-fast mapping and is followed by a CTA barrier.
 template <int R, int C, bool XOUT>
@@ -934,6 +1139,8 @@ template __global__ void kbm_band_hf<NFFT45_EXP_RC>(const double2*, double2*, in
                                                const double*, const double2*, double2*);
 template __global__ void kbm_mid_hf<NFFT45_EXP_RC>(const double2*, double2*, int64_t, const double2*, const double2*, const double2*,
                                               int, const double2*, int, const double2*);
+template __global__ void kbm_pad_hf<NFFT45_EXP_RC>(const double2*, const __grid_constant__ PadHfArgs);
+template __global__ void kbm_pad_hp<NFFT45_EXP_RC>(const __grid_constant__ CUtensorMap, const __grid_constant__ PadHfArgs);
 template __global__ void kbm_pad_h<NFFT45_EXP_RC, false>(const double2*, double2*, int64_t, const double2*, const double2*,
                                                     const double2*, const double2*, int, const double2*, int,
                                                     const double*, const double*, const double*, const double2*, double2*);
@@ -1158,6 +1365,37 @@ struct ChainBM {
   }
   template <bool XOUT>
   int pad_h(const double2* Z, double2* Y, const ChainPlanView& pv, const double2* xsub, double2* xout) {
+    if constexpr (bm_pad_fused<R, C>() && !XOUT) {
+      if (fuse) {  // zero-padding handoff by warp shuffle
+        constexpr int T = fast_threads<2 * C, kSig>();
+        const int64_t Q = n / last_stride<2 * C>();
+        const double2* twQ = nullptr;
+        NFFT_CHECK(qtab(Q, &twQ));
+        const int ntiles = (int)(R * groups);
+        const PadHfArgs args{Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q, pv.cd, ntiles, (int)groups};
+        static const bool persist = getenv("NFFT45_PAD_PERSIST") != nullptr;
+        if (persist) {  // one CTA per SM, two tile groups, TMA-prefetched tiles
+          auto bm_pad = kbm_pad_hp<R, C>;
+          constexpr size_t smem = PadHpLayout<R, C>::kBytes;
+          NFFT_CHECK(bm_attr(bm_pad, smem));
+          CUtensorMap tm;
+          NFFT_CHECK(tma_map_rows(&tm, Z, P, Bp, C, kSig));
+          static const int sms = [] {
+            int dev = 0, v = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+            return v;
+          }();
+          LAUNCH_PDL(bm_pad, std::min(sms, (ntiles + 1) / 2), 2 * T, smem, st, tm, args);
+          return NFFT45_OK;
+        }
+        auto bm_pad = kbm_pad_hf<R, C>;
+        const size_t smem = sizeof(double2) * 2 * C * kSig + 2 * sizeof(double) * C;
+        NFFT_CHECK(bm_attr(bm_pad, smem));
+        LAUNCH_PDL(bm_pad, dim3(groups, (unsigned)R), T, smem, st, Z, args);
+        return NFFT45_OK;
+      }
+    }
     if constexpr (bm_hyb<R, C>()) {
       auto bm_pad = kbm_pad_h<R, C, XOUT>;
       const size_t smem =

@@ -407,9 +407,9 @@ __host__ __device__ constexpr bool hyb_ok() {
 // SRC_SMEM: the first pass's `ld` reads this tile's shared memory (in-place
 // hazard); DST_SMEM: the last pass's `st` writes shared memory.
 template <int N, int S, int P, int Ns, class Tr, unsigned WLMASK, bool SRC_SMEM, bool DST_SMEM, int P0, class Ld,
-          class St, class PT, class Hk, int PEND = Tr::np>
+          class St, class PT, class Hk, int PEND = Tr::np, class Sy = CtaSync>
 __device__ __forceinline__ void hyb_passes(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
-                                           const PT& pt, const Hk& hook) {
+                                           const PT& pt, const Hk& hook, const Sy& sy = Sy()) {
   constexpr int C = 8;
   constexpr int E = Tr::E;
   constexpr int R = Tr::radix(P);
@@ -421,7 +421,7 @@ __device__ __forceinline__ void hyb_passes(double2* sm, const Ld& ld, const St& 
   constexpr bool LAST = (P == Tr::np - 1);
   constexpr bool WL = (WLMASK >> P) & 1u;
   constexpr bool LD_FN = FIRST && P0 == 0;  // the very first pass reads through `ld`
-  const int tid = threadIdx.x;
+  const int tid = sy.tid();
   double2 v[MB][R];
 #pragma unroll
   for (int u = 0; u < MB; u++) {
@@ -437,7 +437,7 @@ __device__ __forceinline__ void hyb_passes(double2* sm, const Ld& ld, const St& 
   // in place: every read of the pass precedes every write of its sync domain
   if constexpr ((!LD_FN || SRC_SMEM) && (!LAST || DST_SMEM)) {
     if constexpr (WL) __syncwarp();
-    else __syncthreads();
+    else sy.sync();
   }
 #pragma unroll
   for (int u = 0; u < MB; u++) {
@@ -468,24 +468,25 @@ __device__ __forceinline__ void hyb_passes(double2* sm, const Ld& ld, const St& 
     constexpr bool WLN = (WLMASK >> (P + 1)) & 1u;
     if constexpr (FIRST && Hk::kActive) hook();
     if constexpr (WL && WLN) __syncwarp();
-    else __syncthreads();
+    else sy.sync();
     if constexpr (FIRST && Hk::kActive) hook.after();
     // PEND < np: the caller runs the remaining passes itself (fused handoff
     // to the next transform in registers); the boundary sync above is done
     if constexpr (P + 1 < PEND)
-      hyb_passes<N, S, P + 1, Ns * R, Tr, WLMASK, SRC_SMEM, DST_SMEM, P0, Ld, St, PT, NoHook, PEND>(sm, ld, st, tw, pt,
-                                                                                                  NoHook());
+      hyb_passes<N, S, P + 1, Ns * R, Tr, WLMASK, SRC_SMEM, DST_SMEM, P0, Ld, St, PT, NoHook, PEND, Sy>(
+          sm, ld, st, tw, pt, NoHook(), sy);
   }
 }
 
 // passes 0 .. PEND-1 of a tile FFT (all of them write shared memory); ends
 // with the sync that pass PEND's mapping (WLMASK bit PEND) needs
-template <int N, int S, class Tr, unsigned WLMASK, int PEND, class Ld, class Hk = NoHook>
+template <int N, int S, class Tr, unsigned WLMASK, int PEND, bool SRC_SMEM = false, class Ld, class Hk = NoHook,
+          class Sy = CtaSync>
 __device__ __forceinline__ void hyb_tile_fft_head(double2* sm, const Ld& ld, const double2* __restrict__ tw,
-                                                  const Hk& hook = Hk()) {
+                                                  const Hk& hook = Hk(), const Sy& sy = Sy()) {
   auto no_st = [](int, int, double2) {};
-  hyb_passes<N, S, 0, 1, Tr, WLMASK, false, true, 0, Ld, decltype(no_st), NoPostTw, Hk, PEND>(sm, ld, no_st, tw,
-                                                                                              NoPostTw(), hook);
+  hyb_passes<N, S, 0, 1, Tr, WLMASK, SRC_SMEM, true, 0, Ld, decltype(no_st), NoPostTw, Hk, PEND, Sy>(
+      sm, ld, no_st, tw, NoPostTw(), hook, sy);
 }
 
 // whole tile FFT, first pass through `ld`
@@ -497,11 +498,12 @@ __device__ __forceinline__ void hyb_tile_fft(double2* sm, const Ld& ld, const St
 }
 // passes P0.. of a tile FFT whose earlier passes were produced directly in
 // shared memory (swizzled Stockham layout after pass P0 - 1, Ns = NS0)
-template <int N, int S, class Tr, unsigned WLMASK, int P0, int NS0, class St, class PT = NoPostTw>
+template <int N, int S, class Tr, unsigned WLMASK, int P0, int NS0, class St, class PT = NoPostTw, class Sy = CtaSync>
 __device__ __forceinline__ void hyb_tile_fft_from(double2* sm, const St& st, const double2* __restrict__ tw,
-                                                  const PT& pt = PT()) {
+                                                  const PT& pt = PT(), const Sy& sy = Sy()) {
   auto no_ld = [](int, int) -> double2 { return make_double2(0.0, 0.0); };
-  hyb_passes<N, S, P0, NS0, Tr, WLMASK, true, false, P0>(sm, no_ld, st, tw, pt, NoHook());
+  hyb_passes<N, S, P0, NS0, Tr, WLMASK, true, false, P0, decltype(no_ld), St, PT, NoHook, Tr::np, Sy>(
+      sm, no_ld, st, tw, pt, NoHook(), sy);
 }
 // warp-local mask: every pass but the first (when it reads global memory)
 // and the last (when it writes global memory)

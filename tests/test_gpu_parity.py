@@ -574,8 +574,9 @@ def test_kernel_variants_bitwise(tmp_path):
     in the same order: programmatic dependent launch off (NFFT45_NO_PDL),
     warp-tiled single-signal spreading forced on / off (NFFT45_SPREAD_WARP),
     256-cell spreading tiles (NFFT45_STILE) and 256-node interpolation CTAs
-    (NFFT45_GNODES) and the TMA-staged pad kernel instead of the LDG-staged
-    one (NFFT45_TMA) must all give bitwise the outputs of the
+    (NFFT45_GNODES), the TMA-staged pad kernel instead of the LDG-staged
+    one (NFFT45_TMA), and the round-2 switches (hybrid / fused chain kernels,
+    TMA gather tiles, persistent pad) must all give bitwise the outputs of the
     default build, for single signals on both sides of the warp-tile
     threshold, a 4-signal batch, batch-minor chains and a non-chain size."""
     import os
@@ -584,7 +585,11 @@ def test_kernel_variants_bitwise(tmp_path):
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     variants = ({}, {"NFFT45_NO_PDL": "1"}, {"NFFT45_SPREAD_WARP": "1"}, {"NFFT45_SPREAD_WARP": "0"},
-                {"NFFT45_STILE": "256", "NFFT45_GNODES": "256"}, {"NFFT45_TMA": "1"})
+                {"NFFT45_STILE": "256", "NFFT45_GNODES": "256"}, {"NFFT45_TMA": "1"},
+                # round 2: all-column-fast two-FFT kernels instead of the hybrid (warp-local) ones, hybrid
+                # without the register / shuffle handoffs, cp.async instead of TMA cell tiles in the
+                # persistent gather, the persistent TMA-prefetching pad
+                {"NFFT45_HYB": "0"}, {"NFFT45_FUSE": "0"}, {"NFFT45_GATHER_TMA": "0"}, {"NFFT45_PAD_PERSIST": "1"})
     outs = []
     for i, extra in enumerate(variants):
         f = tmp_path / f"v{i}.npz"
