@@ -334,13 +334,13 @@ __global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_thre
   double2* s_sb = reinterpret_cast<double2*>(s_t1 + C);
   const int k1 = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * SG;
-  for (int m1 = threadIdx.x; m1 < C; m1 += blockDim.x) {
-    const int64_t p = (int64_t)k1 + (int64_t)R * m1;
+  for (int i = threadIdx.x; i < C / 2; i += blockDim.x) {  // tile-major tables: contiguous slices
+    const int64_t o = (int64_t)k1 * C + 2 * i;
     if (sub) {
-      cpa8(&s_t0[m1], &deconv[p]);
-      cpa8(&s_t1[m1], &decay[p]);
+      cpa16(&s_t0[2 * i], &deconv[o]);
+      cpa16(&s_t1[2 * i], &decay[o]);
     } else {
-      cpa8(&s_t0[m1], &dd[p]);
+      cpa16(&s_t0[2 * i], &dd[o]);
     }
   }
   if (sub)  // subtrahend tile, swizzled like the data tile (it is read by warp-local lanes)
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<
   double2* s_ks = sm + R * kSig;
   const int r = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * kSig;
-  for (int k2 = threadIdx.x; k2 < R; k2 += blockDim.x) cpa16(&s_ks[k2], &ks[(int64_t)r + (int64_t)C * k2]);
+  for (int k2 = threadIdx.x; k2 < R; k2 += blockDim.x) cpa16(&s_ks[k2], &ks[(int64_t)r * R + k2]);  // tile-major ks
   cpa_commit();
   const unsigned ub = (unsigned)Bp;  // 32-bit in-tile offsets (see kbm_col)
   const double2* __restrict__ Ut = U + (int64_t)r * R * Bp + b0;
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<
   double2* s_ks = sm + R * kSig;
   const int r = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * kSig;
-  for (int k2 = threadIdx.x; k2 < R; k2 += blockDim.x) cpa16(&s_ks[k2], &ks[(int64_t)r + (int64_t)C * k2]);
+  for (int k2 = threadIdx.x; k2 < R; k2 += blockDim.x) cpa16(&s_ks[k2], &ks[(int64_t)r * R + k2]);  // tile-major ks
   cpa_commit();
   const unsigned ub = (unsigned)Bp;  // 32-bit in-tile offsets (see kbm_col)
   const double2* __restrict__ Ut = U + (int64_t)r * R * Bp + b0;
@@ -488,13 +488,13 @@ __global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_thre
   double2* s_sb = reinterpret_cast<double2*>(s_t1 + C);
   const int k1 = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * SG;
-  for (int m1 = threadIdx.x; m1 < C; m1 += blockDim.x) {
-    const int64_t p = (int64_t)k1 + (int64_t)R * m1;
+  for (int i = threadIdx.x; i < C / 2; i += blockDim.x) {  // tile-major tables: contiguous slices
+    const int64_t o = (int64_t)k1 * C + 2 * i;
     if (sub) {
-      cpa8(&s_t0[m1], &deconv[p]);
-      cpa8(&s_t1[m1], &decay[p]);
+      cpa16(&s_t0[2 * i], &deconv[o]);
+      cpa16(&s_t1[2 * i], &decay[o]);
     } else {
-      cpa8(&s_t0[m1], &dd[p]);
+      cpa16(&s_t0[2 * i], &dd[o]);
     }
   }
   if (sub)  // subtrahend tile, swizzled like the data tile (it is read by warp-local lanes)
@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_thre
   const int64_t b0 = (int64_t)blockIdx.x * kSig;
   const unsigned ub = (unsigned)a.Bp;
   const double2* __restrict__ Zt = Z + (int64_t)r * C * a.Bp + b0;
-  for (int k2 = threadIdx.x; k2 < C; k2 += blockDim.x) cpa8(&s_t0[k2], &a.cd[(int64_t)r + (int64_t)R * k2]);
+  for (int i = threadIdx.x; i < C / 2; i += blockDim.x) cpa16(&s_t0[2 * i], &a.cd[(int64_t)r * C + 2 * i]);  // tile-major
   cpa_commit();
   auto ld1 = [&](int i, int c) -> double2 { return Zt[(unsigned)i * ub + c]; };
   pad_hf_tile<R, C>(a, sm, s_t0, ld1, CpAsyncWaitHook(), r, b0, CtaSync());
@@ -722,7 +722,7 @@ __device__ __noinline__ bool pad_hp_body(const CUtensorMap* tmZ, const PadHfArgs
   const int r = t / a.groups;
   const int64_t b0 = (int64_t)(t % a.groups) * kSig;
   sy.sync();  // the group's previous tile is done with `sm` and the table slot
-  for (int k2 = sy.t; k2 < C; k2 += T) cpa8(&s_t0[k2], &a.cd[(int64_t)r + (int64_t)R * k2]);
+  for (int i = sy.t; i < C / 2; i += T) cpa16(&s_t0[2 * i], &a.cd[(int64_t)r * C + 2 * i]);  // tile-major
   cpa_commit();
   mbar_wait(bar, it & 1);
   const TmaRefill<C> hook{tmZ, inb, bar, t + stride, a.ntiles, a.groups, sy.t};
@@ -787,13 +787,13 @@ __global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_thre
   double2* __restrict__ Yt = Y + (int64_t)r * Bp + b0;
   double2* __restrict__ Xt = XOUT ? xout + (int64_t)r * Bp + b0 : nullptr;
   const double2* __restrict__ XSt = (XOUT && xsub) ? xsub + (int64_t)r * Bp + b0 : nullptr;
-  for (int k2 = threadIdx.x; k2 < C; k2 += blockDim.x) {
-    const int64_t p = (int64_t)r + (int64_t)R * k2;
+  for (int i = threadIdx.x; i < C / 2; i += blockDim.x) {  // tile-major tables: contiguous slices
+    const int64_t o = (int64_t)r * C + 2 * i;
     if (XOUT) {
-      cpa8(&s_t0[k2], &coef[p]);
-      cpa8(&s_t1[k2], &deconv[p]);
+      cpa16(&s_t0[2 * i], &coef[o]);
+      cpa16(&s_t1[2 * i], &deconv[o]);
     } else {
-      cpa8(&s_t0[k2], &cd[p]);
+      cpa16(&s_t0[2 * i], &cd[o]);
     }
   }
   if (XOUT && xsub)
@@ -1256,7 +1256,7 @@ struct ChainBM {
       const double2* twQ = nullptr;
       NFFT_CHECK(qtab(Q, &twQ));
       LAUNCH_PDL(bm_band, dim3(groups, (unsigned)R), T, smem, st, T_, U, Bp, t.tw2C, t.twC, t.tP->lo, t.tP->hi, t.tP->s,
-                 twQ, (int)Q, pv.deconv, pv.decay, pv.dd, sub, rsave);
+                 twQ, (int)Q, pv.tdeconv, pv.tdecay, pv.tdd, sub, rsave);
     }
     return NFFT45_OK;
   }
@@ -1278,7 +1278,7 @@ struct ChainBM {
       const double2* twQ = nullptr;
       NFFT_CHECK(qtab(Q, &twQ));
       LAUNCH_PDL(bm_mid, dim3(groups, (unsigned)C), T, smem, st, U, Z, Bp, t.twR, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q,
-                 pv.ks);
+                 pv.tks);
     }
     return NFFT45_OK;
   }
@@ -1372,7 +1372,7 @@ struct ChainBM {
         const double2* twQ = nullptr;
         NFFT_CHECK(qtab(Q, &twQ));
         const int ntiles = (int)(R * groups);
-        const PadHfArgs args{Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q, pv.cd, ntiles, (int)groups};
+        const PadHfArgs args{Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q, pv.tcd, ntiles, (int)groups};
         static const bool persist = getenv("NFFT45_PAD_PERSIST") != nullptr;
         if (persist) {  // one CTA per SM, two tile groups, TMA-prefetched tiles
           auto bm_pad = kbm_pad_hp<R, C>;
@@ -1406,7 +1406,7 @@ struct ChainBM {
       const double2* twQ = nullptr;
       NFFT_CHECK(qtab(Q, &twQ));
       LAUNCH_PDL(bm_pad, dim3(groups, (unsigned)R), T, smem, st, Z, Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s,
-                 twQ, (int)Q, pv.coef, pv.deconv, pv.cd, xsub, xout);
+                 twQ, (int)Q, pv.tcoef, pv.tdeconv, pv.tcd, xsub, xout);
     }
     return NFFT45_OK;
   }
@@ -1489,7 +1489,7 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
     // hybrid two-FFT kernels (2 CTA barriers per tile, warp-local middle
     // passes); NFFT45_HYB=0 restores the all-column-fast kernels for A/B runs
     static const bool hyb_on = !(getenv("NFFT45_HYB") && atoi(getenv("NFFT45_HYB")) == 0);
-    ch.hyb = hyb_on && bm_hyb<R, C>() && !ch.small_tiles;
+    ch.hyb = hyb_on && bm_hyb<R, C>() && !ch.small_tiles && pv.tdd != nullptr;  // needs the tile-major tables
     static const bool fuse_on = !(getenv("NFFT45_FUSE") && atoi(getenv("NFFT45_FUSE")) == 0);
     ch.fuse = fuse_on;
   }
@@ -1576,6 +1576,25 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
   status = run();
   cudaFreeAsync(base, st);
   return status;
+}
+
+bool chain_bm_hybrid_factors(int64_t P, int* R, int* C) {
+  auto set = [&](int r, int c) {
+    *R = r;
+    *C = c;
+    return true;
+  };
+  switch (P) {  // the sizes whose ChainBM<R, C> satisfies bm_hyb (chain_run_bm's table)
+    case 1024: return bm_hyb<32, 32>() && set(32, 32);
+    case 2048: return bm_hyb<64, 32>() && set(64, 32);
+    case 4096: return bm_hyb<64, 64>() && set(64, 64);
+    case 8192: return bm_hyb<128, 64>() && set(128, 64);
+    case 16384: return bm_hyb<128, 128>() && set(128, 128);
+    case 32768: return bm_hyb<256, 128>() && set(256, 128);
+    case 65536: return bm_hyb<256, 256>() && set(256, 256);
+    case 131072: return bm_hyb<512, 256>() && set(512, 256);
+  }
+  return false;
 }
 
 bool chain_bm_supported(int64_t P) {

@@ -742,6 +742,7 @@ int gather_fallback(const GridDev& g, int64_t n, const Window& win, const double
 // staging buffer (strongly clustered grids) return early and are handled by
 // k_gather_b (host passes `fallback` so those blocks are recomputed there).
 constexpr int kGPSpan = 112;
+constexpr int kGPSpanS = 96;  // short TMA box (rows)
 
 // SIG signals per group (16 or 32).  With SIG = 16 the two half-warps take
 // 4 nodes each of the warp's 8 (same cells, broadcast reads), which halves
@@ -751,7 +752,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
     const double* __restrict__ ts, const int* __restrict__ perm, int64_t Q, int64_t n, double alpha, GaussTab G,
     const double2* __restrict__ H, int64_t H_ld, int64_t batch, NodeFactor nf, const double2* __restrict__ sub,
     int64_t sub_ld, int mode, double2* __restrict__ out, int64_t out_ld, int ngroups, int* __restrict__ overflow, int sw,
-    const __grid_constant__ CUtensorMap tmH, int tma) {
+    const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmHs, int tma) {
   pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int HALVES = 32 / SIG, NPL = kNPW / HALVES;
   static_assert(kGatherNodes == 32, "one node per lane in the signal-major staging");
@@ -820,14 +821,16 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
   // past the block's span and signals past the padded batch arrive as zeros /
   // unused rows.  Blocks that wrap keep the per-thread cp.async copies.
   const bool tma_blk = tma && cs >= 0 && ce < ni;
-  constexpr unsigned kBoxBytes = (unsigned)(kGPSpan * SIG * sizeof(double2));
+  // two boxes: kGPSpanS rows cover the span of most blocks (29 + 31 node gaps), kGPSpan rows the rest
+  const bool box_s = len <= kGPSpanS;
+  const unsigned kBoxBytes = (unsigned)((box_s ? kGPSpanS : kGPSpan) * SIG * sizeof(double2));
   auto stage = [&](int64_t g) {
     const int64_t b0 = g * SIG;
     if (tma_blk) {
       if (tid == 0) {
         fence_proxy_async();  // the previous group's generic reads of Y precede the async refill
         mbar_expect_tx(&s_bar, kBoxBytes);
-        tma_load_2d(Y, &tmH, (int)(2 * b0), cs, &s_bar);
+        tma_load_2d(Y, box_s ? &tmHs : &tmH, (int)(2 * b0), cs, &s_bar);
       }
     } else {
       const bool ok = b0 + sl < batch;
@@ -999,13 +1002,16 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
   CUtensorMap tmH;
   memset(&tmH, 0, sizeof(tmH));
   int tma = use_tma && (reinterpret_cast<uintptr_t>(H) % 16 == 0) && n >= kGPSpan;
+  CUtensorMap tmHs;
+  memset(&tmHs, 0, sizeof(tmHs));
   if (tma) NFFT_CHECK(tma_map_rows(&tmH, H, n, H_ld, kGPSpan, SIG));
+  if (tma) NFFT_CHECK(tma_map_rows(&tmHs, H, n, H_ld, kGPSpanS, SIG));
 #define NFFT_GP_LAUNCH(OBM, SM_, S_)                                                                           \
   {                                                                                                          \
     auto gather_p = k_gather_p<OBM, SM_, S_>;                                                                \
     NFFT_CUDA(cudaFuncSetAttribute(gather_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
     LAUNCH_PDL(gather_p, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, H_ld, batch, f,  \
-           sub, sub_ld, mode, out, out_ld, ngroups, overflow, sw, tmH, tma);                                 \
+           sub, sub_ld, mode, out, out_ld, ngroups, overflow, sw, tmH, tmHs, tma);                           \
   }
 #define NFFT_GP_SUB(OBM, S_) \
   if (subm == 0) NFFT_GP_LAUNCH(OBM, 0, S_) else if (subm == 1) NFFT_GP_LAUNCH(OBM, 1, S_) else NFFT_GP_LAUNCH(OBM, 2, S_)

@@ -155,6 +155,9 @@ struct nfft45_plan {
   double* rtab;      // real copies: decay, coef_scale, deconvolution (length P each)
   double *rdecay, *rcoef, *rdeconv;
   double *rdd, *rcd;  // deconv*decay, coef*deconv
+  // tile-major copies for the batch-minor hybrid chain kernels (null when P has none)
+  double *tdd = nullptr, *tcd = nullptr, *tdeconv = nullptr, *tdecay = nullptr, *tcoef = nullptr;
+  double2* tks = nullptr;
 };
 
 // ------------------------------------------------------------- kernels
@@ -258,6 +261,31 @@ __global__ void k_plan_tables(const double* __restrict__ t, const double* __rest
   double2 ct = cis_turns(tq >= 0.5 ? tq - 1.0 : tq);
   double2 w = cdiv(h, cmul(dL[q], ct));
   nw[q] = w;
+}
+
+// tile-major copies of the per-index solve tables for the P = R x C layout
+// p = k + R m (chain_bm.cu): a chain tile then stages its slice as one
+// contiguous run (the stride-R gather cost 16x the shared-memory wavefronts)
+__global__ void k_tile_major_tables(int64_t P, int R, int C, const double* __restrict__ rdd,
+                                    const double* __restrict__ rcd, const double* __restrict__ rdeconv,
+                                    const double* __restrict__ rdecay, const double* __restrict__ rcoef,
+                                    const double2* __restrict__ ks, double* __restrict__ tdd, double* __restrict__ tcd,
+                                    double* __restrict__ tdeconv, double* __restrict__ tdecay,
+                                    double* __restrict__ tcoef, double2* __restrict__ tks) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  {
+    const int64_t k = i / C, m = i % C, p = k + (int64_t)R * m;
+    tdd[i] = rdd[p];
+    tcd[i] = rcd[p];
+    tdeconv[i] = rdeconv[p];
+    tdecay[i] = rdecay[p];
+    tcoef[i] = rcoef[p];
+  }
+  {
+    const int64_t r = i / R, k = i % R;
+    tks[i] = ks[r + (int64_t)C * k];
+  }
 }
 
 // real solve tables for the fused chains
@@ -417,6 +445,12 @@ static ChainPlanView chain_view(const nfft45_plan* p) {
   v.deconv = p->rdeconv;
   v.dd = p->rdd;
   v.cd = p->rcd;
+  v.tdd = p->tdd;
+  v.tcd = p->tcd;
+  v.tdeconv = p->tdeconv;
+  v.tdecay = p->tdecay;
+  v.tcoef = p->tcoef;
+  v.tks = p->tks;
   return v;
 }
 
@@ -1027,12 +1061,23 @@ int nfft45_plan_create_terms(const nfft45_grid* g, double a, int64_t R, int m, v
   // a rebuilt plan reuses pooled memory instead of a fresh cudaMalloc (1-20 ms
   // for the 184 MB of tables at P = 2^20); the build ends with a stream
   // synchronize (check_guards), after which every stream may use the tables
-  cudaError_t e = cudaMallocAsync(&p->tables, sizeof(double2) * 9 * P + sizeof(double) * 5 * P, s);
+  int hR = 0, hC = 0;
+  const bool tile_major = m == kFastM && chain_bm_hybrid_factors(P, &hR, &hC);
+  cudaError_t e = cudaMallocAsync(&p->tables, sizeof(double2) * (9 + (tile_major ? 1 : 0)) * P +
+                                                  sizeof(double) * (5 + (tile_major ? 5 : 0)) * P, s);
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "cudaMalloc(plan)");
   }
-  p->rtab = reinterpret_cast<double*>(p->tables + 9 * P);
+  p->rtab = reinterpret_cast<double*>(p->tables + (9 + (tile_major ? 1 : 0)) * P);
+  if (tile_major) {
+    p->tks = p->tables + 9 * P;
+    p->tdd = p->rtab + 5 * P;
+    p->tcd = p->rtab + 6 * P;
+    p->tdeconv = p->rtab + 7 * P;
+    p->tdecay = p->rtab + 8 * P;
+    p->tcoef = p->rtab + 9 * P;
+  }
   p->rdecay = p->rtab;
   p->rcoef = p->rtab + P;
   p->rdeconv = p->rtab + 2 * P;
@@ -1067,6 +1112,12 @@ int nfft45_plan_create_terms(const nfft45_grid* g, double a, int64_t R, int m, v
       k_real_tables<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(p->decay, p->coef, P, Window::make(m).b, p->rdecay,
                                                               p->rcoef, p->rdeconv, p->rdd, p->rcd);
       g_launches++;
+      if (tile_major) {
+        k_tile_major_tables<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(P, hR, hC, p->rdd, p->rcd, p->rdeconv, p->rdecay,
+                                                                      p->rcoef, p->ks, p->tdd, p->tcd, p->tdeconv,
+                                                                      p->tdecay, p->tcoef, p->tks);
+        g_launches++;
+      }
       cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) status = cuda_fail(le, "plan tables");
     }

@@ -69,7 +69,15 @@ struct ChainPlanView {
   const double2 *ks, *c5, *c4;         // complex tables (c5/c4 in ascending-node order)
   const double *decay, *coef, *deconv;  // real tables of length P
   const double *dd, *cd;                // deconv*decay, coef*deconv
+  // tile-major copies for the batch-minor hybrid kernels (nullptr when P has no
+  // hybrid chain): T[k * C + m] = table[k + R m] (P = R x C layout p = k + R m),
+  // so a tile's slice is one contiguous run instead of a stride-R gather;
+  // tks[r * R + k] = ks[r + C k]
+  const double *tdd = nullptr, *tcd = nullptr, *tdeconv = nullptr, *tdecay = nullptr, *tcoef = nullptr;
+  const double2* tks = nullptr;
 };
+// (R, C) of the batch-minor hybrid chain for P (false: none)
+bool chain_bm_hybrid_factors(int64_t P, int* R, int* C);
 bool chain_supported(int64_t P, int m);
 // P the batch-minor chains handle (P = R*C with R = C or R = 2C, powers of two).
 bool chain_bm_supported(int64_t P);

@@ -55,6 +55,7 @@ def full(path):
             "dram_pct": g("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
             "fp64_pct": g("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
             "l1_pct": g("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+            "lsu_pct": g("l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed"),
             "issue_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "warps_active_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
             "regs": g("launch__registers_per_thread"),
@@ -95,14 +96,16 @@ def main(lpath, fpath, tag, steps, config="c4"):
     tscale = {"msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "us": 1e-3, "ns": 1e-6}.get(tunit, 1.0)
     with open(os.path.join(REPO, "profiles", f"{tag}_{config}_kernels.md"), "w") as f:
         f.write(f"# {tag}: ncu --set full captures ({config}, one bench step)\n\n")
-        f.write("Shared-memory busy = LSU shared wavefronts / (SMs x active cycles); L2->SM GB = "
+        f.write("LSU pipe % = `l1tex__data_pipe_lsu_wavefronts` (shared + global + local wavefronts of the one L1 data "
+                "pipe, % of its peak: the resource that bounds the two-FFT chain kernels and the gridding kernels); "
+                "Shared-memory busy = LSU shared wavefronts / (SMs x active cycles); L2->SM GB = "
                 "`l1tex__m_xbar2l1tex_read_bytes.sum` (bytes the SMs read from L2; writes go through to L2 as "
                 "well), its rate over the kernel time, `lts__throughput` % of peak (the busiest L2 sub-unit) and "
                 "the L2 read-sector hit rate; stalls = top three `smsp__average_warps_issue_stalled_*` per issued "
                 "instruction.\n\n")
         f.write("| kernel | grid | ms | DRAM read GB | DRAM write GB | DRAM % peak | L2->SM GB | L2->SM GB/s | L2 % peak | L2 read hit % "
-                "| fp64 pipe % | L1 % | SMEM busy % | bank conflicts % | issue % | warps active % | regs | top stalls |\n")
-        f.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
+                "| fp64 pipe % | L1 % | LSU pipe % | SMEM busy % | bank conflicts % | issue % | warps active % | regs | top stalls |\n")
+        f.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
         for r in res:
             rb, wb = (r["dram_bytes_read"] or 0) * ur, (r["dram_bytes_write"] or 0) * uw
             traffic[r["kernel"]].append(rb + wb)
@@ -114,7 +117,7 @@ def main(lpath, fpath, tag, steps, config="c4"):
             l2 = (f"{lb / 1e9:.3f} | {lb / (ms / 1e3) / 1e9:.0f} | {r['l2_pct'] or 0:.1f} | {r['l2_hit'] or 0:.1f}"
                   if r["l2_bytes"] is not None else "— | — | — | —")
             f.write(f"| `{r['kernel']}` | {r['grid']} | {ms:.3f} | {rb / 1e9:.3f} | {wb / 1e9:.3f} | "
-                    f"{r['dram_pct']:.1f} | {l2} | {r['fp64_pct']:.1f} | {r['l1_pct']:.1f} | {smem:.1f} | {conf:.1f} | "
+                    f"{r['dram_pct']:.1f} | {l2} | {r['fp64_pct']:.1f} | {r['l1_pct']:.1f} | {r['lsu_pct'] or 0:.1f} | {smem:.1f} | {conf:.1f} | "
                     f"{r['issue_pct']:.1f} | {r['warps_active_pct']:.1f} | {r['regs']:.0f} | {st} |\n")
     short = {}
     for k, v in traffic.items():
@@ -122,7 +125,13 @@ def main(lpath, fpath, tag, steps, config="c4"):
                "k_spread_p": "spread_p", "k_gather_b": "gather_b", "k_gather_p": "gather_p", "kbm_colin": "bm_colin",
                "kbm_rowout": "bm_rowout", "kc_col": "chain_col", "kc_band": "chain_band", "kc_mid": "chain_mid",
                "kc_pad": "chain_pad", "kc_row": "chain_row", "k_spread_s": "spread_s1",
-               "k_gather_s": "gather_s1"}.get(k.split("<")[0], k.split("<")[0])
+               "k_gather_s": "gather_s1"}
+        base = k.split("<")[0]
+        for suf in ("_hf", "_hp", "_h"):  # hybrid / fused / persistent variants report under the stage's name
+            if base.startswith("kbm_") and base.endswith(suf):
+                base = base[: -len(suf)]
+                break
+        key = key.get(base, base)
         short[key] = sum(v) / len(v)
     json.dump(short, open(os.path.join(REPO, "profiles", f"traffic_{config}.json"), "w"), indent=1)
     print(json.dumps(short, indent=1))
