@@ -32,6 +32,15 @@ constexpr int kGatherSpan = 112; // cells staged per chunk
 constexpr int kWTSpan = 64;      // per-warp weight-table cells per chunk
 
 __device__ __forceinline__ int swz(int sig, int row) { return sig ^ (row & 7); }
+// Slot of (row e, signal sig) in a [rows][SIG] tile staged from a SIGNAL-MAJOR
+// array by cp.async with lanes = consecutive rows of one signal: 8 consecutive
+// rows of a signal share one 128-byte line (an LDGSTS writes shared memory
+// sector by sector as the data returns, so lanes that scatter over 512-byte
+// rows cost 6-7x the wavefronts -- ncu: 38 % of the first spreading launch);
+// the XOR keeps the reads (lanes = consecutive signals, 128 bytes apart)
+// on 8 distinct bank groups.
+template <int SIG>
+__device__ __forceinline__ int swz_nb(int sig, int e) { return (((e >> 3) * SIG + sig) << 3) + ((e & 7) ^ (sig & 7)); }
 
 // 16-byte global -> shared async copy (LDGSTS); `valid == false` zero-fills.
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool valid) {
@@ -252,7 +261,7 @@ __global__ void __launch_bounds__(256, 2) k_spread_b(const double* __restrict__ 
 // per group (weights recomputed), same arithmetic order.
 constexpr int kPipeCap = 64;
 
-template <int SPL>
+template <int SPL, bool NB>  // NB: signal-major amplitudes, node-blocked staging layout (swz_nb)
 __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double* __restrict__ ts, const int* __restrict__ perm,
                                                     int64_t Q, int64_t n, double alpha, GaussTab G,
                                                     const double2* __restrict__ amp, int64_t batch, NodeFactor nf,
@@ -336,7 +345,7 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
         const int64_t b = b0 + sig;
         const bool ok = b < batch;
         const double2* row = amp + (ok ? b : 0) * Q;
-        for (int e = lane; e < cnt; e += 32) cp_async16(&A[e * SIG + swz(sig, e)], row + Pi[e], ok);
+        for (int e = lane; e < cnt; e += 32) cp_async16(&A[swz_nb<SIG>(sig, e)], row + Pi[e], ok);
       }
     } else {
       for (int e = warp; e < cnt; e += kSpreadWarps) {
@@ -392,8 +401,8 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
       double2 x0[SPL], x1[SPL];
 #pragma unroll
       for (int s2 = 0; s2 < SPL; s2++) {
-        x0[s2] = A[n0.x * SIG + (sw[s2] ^ (n0.x & 7))];
-        x1[s2] = A[n1.x * SIG + (sw[s2] ^ (n1.x & 7))];
+        x0[s2] = A[NB ? swz_nb<SIG>(sw[s2], n0.x) : n0.x * SIG + (sw[s2] ^ (n0.x & 7))];
+        x1[s2] = A[NB ? swz_nb<SIG>(sw[s2], n1.x) : n1.x * SIG + (sw[s2] ^ (n1.x & 7))];
       }
       const double c0[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
       const double c1[8] = {b01.x, b01.y, b23.x, b23.y, b45.x, b45.y, b67.x, b67.y};
@@ -415,7 +424,7 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
       const double c0[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
 #pragma unroll
       for (int s2 = 0; s2 < SPL; s2++) {
-        const double2 y0 = cmul(A[n0.x * SIG + (sw[s2] ^ (n0.x & 7))], f0);
+        const double2 y0 = cmul(A[NB ? swz_nb<SIG>(sw[s2], n0.x) : n0.x * SIG + (sw[s2] ^ (n0.x & 7))], f0);
 #pragma unroll
         for (int c = 0; c < kCPW; c++) caxpy(acc[c][s2], c0[c], y0);
       }
@@ -496,7 +505,7 @@ int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const doubl
   const int sw = env_sl > 0;
   if (env_sl > 0) slices = (int)std::min<int64_t>(ngroups, env_sl);
   size_t smem = (size_t)2 * kPipeCap * SIG * 16 + (size_t)kPipeCap * kWRow * 8 + kPipeCap * 16 + kPipeCap * 16;
-  auto spread_p = k_spread_p<1>;
+  auto spread_p = amp_ld == 0 ? k_spread_p<1, true> : k_spread_p<1, false>;
   NFFT_CUDA(cudaFuncSetAttribute(spread_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const dim3 grid = sw ? dim3((unsigned)slices, (unsigned)ntiles) : dim3((unsigned)ntiles, (unsigned)slices);
   LAUNCH_PDL(spread_p, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), amp, batch, f, H, ranges,
@@ -846,7 +855,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
       for (int k = 0; k < SIG / kGatherWarps; k++) {
         const int sig = warp + kGatherWarps * k;
         const bool okb = b0 + sig < batch && lane < nq;
-        cp_async16(&Sb[lane * SIG + swz(sig, lane)], sb_src + (okb ? (b0 + kGatherWarps * k) * Q : 0), okb);
+        cp_async16(&Sb[swz_nb<SIG>(sig, lane)], sb_src + (okb ? (b0 + kGatherWarps * k) * Q : 0), okb);
       }
     }
     cp_async_commit();
@@ -894,7 +903,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
 #pragma unroll
       for (int i = 0; i < NPL; i++) {
         const int e = e0 + i;
-        sb_in[i] = e < nq ? Sb[e * SIG + swz(sl, e)] : make_double2(0.0, 0.0);
+        sb_in[i] = e < nq ? Sb[swz_nb<SIG>(sl, e)] : make_double2(0.0, 0.0);
       }
     }
     __syncthreads();  // Y (and Sb) consumed: prefetch the next group during the epilogue
