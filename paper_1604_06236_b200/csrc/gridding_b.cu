@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
         for (int s2 = 0; s2 < SPL; s2++) {
           const int sig = lane + 32 * s2;
           const bool ok = b0 + sig < batch;
-          cp_async16(&A[e * SIG + swz(sig, e)], row + (ok ? sig : 0), ok);
+          cp_async16(&A[e * SIG + sig], row + (ok ? sig : 0), ok);  // lanes = signals: plain rows (no swizzle needed)
         }
       }
     }
@@ -401,8 +401,8 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
       double2 x0[SPL], x1[SPL];
 #pragma unroll
       for (int s2 = 0; s2 < SPL; s2++) {
-        x0[s2] = A[NB ? swz_nb<SIG>(sw[s2], n0.x) : n0.x * SIG + (sw[s2] ^ (n0.x & 7))];
-        x1[s2] = A[NB ? swz_nb<SIG>(sw[s2], n1.x) : n1.x * SIG + (sw[s2] ^ (n1.x & 7))];
+        x0[s2] = A[NB ? swz_nb<SIG>(sw[s2], n0.x) : n0.x * SIG + sw[s2]];
+        x1[s2] = A[NB ? swz_nb<SIG>(sw[s2], n1.x) : n1.x * SIG + sw[s2]];
       }
       const double c0[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
       const double c1[8] = {b01.x, b01.y, b23.x, b23.y, b45.x, b45.y, b67.x, b67.y};
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
       const double c0[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
 #pragma unroll
       for (int s2 = 0; s2 < SPL; s2++) {
-        const double2 y0 = cmul(A[NB ? swz_nb<SIG>(sw[s2], n0.x) : n0.x * SIG + (sw[s2] ^ (n0.x & 7))], f0);
+        const double2 y0 = cmul(A[NB ? swz_nb<SIG>(sw[s2], n0.x) : n0.x * SIG + sw[s2]], f0);
 #pragma unroll
         for (int c = 0; c < kCPW; c++) caxpy(acc[c][s2], c0[c], y0);
       }
