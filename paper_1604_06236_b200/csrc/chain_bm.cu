@@ -980,79 +980,6 @@ __global__ void __launch_bounds__(fast_threads<2 * C, SG>(), bm_minb(fast_thread
   }
 }
 
-template <int R, int C, int SG>
-__device__ __noinline__ bool pad_p_body(const CUtensorMap* tmZ, const PadTileArgs* ap, unsigned char* smraw, int it) {
-  constexpr int NC = 2 * C;
-  constexpr int T = fast_threads<NC, SG>();
-  constexpr unsigned kTileBytes = (unsigned)(C * SG * sizeof(double2));
-  constexpr size_t kWork = (fast_smem<NC, SG>() + 2 * sizeof(double) * C + 127) / 128 * 128;
-  constexpr size_t kGroup = kWork + kTileBytes;
-  const PadTileArgs& a = *ap;
-  const int tx = threadIdx.x;
-  const int g = tx / T;
-  const GroupSync<T> sy{g, tx - g * T};
-  const int stride = 2 * gridDim.x;
-  const int t = 2 * blockIdx.x + g + it * stride;
-  if (t >= a.ntiles) return false;
-  double2* sm = reinterpret_cast<double2*>(smraw + g * kGroup);
-  double2* inb = reinterpret_cast<double2*>(smraw + g * kGroup + kWork);  // [C][SG] dense (TMA box)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * kGroup) + g;
-  mbar_wait(bar, it & 1);
-  pad_tile<R, C, SG, false>(a, tmZ, sm, inb, bar, t, t + stride, sy);
-  return true;
-}
-
-// Persistent, software-pipelined pad: ONE CTA per SM made of two independent
-// tile groups of T threads.  Each group owns a work buffer, its table slots,
-// a TMA staging buffer and an mbarrier, and walks the tiles
-// t = 2 blockIdx.x + group, + 2 gridDim.x, ... : right after the first pass
-// has pulled the staged tile into registers (its barrier), the group's thread
-// 0 refills the staging buffer with the group's NEXT tile, so that tile's
-// DRAM latency runs under the remaining five passes of the current one, and
-// the other group's arithmetic fills this group's barrier waits.  Registers
-// hold only tiles being computed (the one-shot kernels keep 2 x 32K registers
-// idle while their tiles are in flight).  Arithmetic and store order are those
-// of kbm_pad: bitwise identical results.
-template <int R, int C, int SG>
-__global__ void __launch_bounds__(2 * fast_threads<2 * C, SG>(), 1) kbm_pad_p(
-    const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ PadTileArgs a) {
-  constexpr int NC = 2 * C;
-  constexpr int T = fast_threads<NC, SG>();
-  constexpr unsigned kTileBytes = (unsigned)(C * SG * sizeof(double2));
-  constexpr size_t kWork = (fast_smem<NC, SG>() + 2 * sizeof(double) * C + 127) / 128 * 128;
-  constexpr size_t kGroup = kWork + kTileBytes;
-  extern __shared__ __align__(128) unsigned char smraw_p[];
-  {
-    const int g = threadIdx.x / T;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw_p + 2 * kGroup) + g;
-    if ((int)threadIdx.x - g * T == 0) {
-      if (g == 0) tma_prefetch_desc(&tmZ);
-      mbar_init(bar, 1);
-      mbar_fence_init();
-    }
-  }
-  __syncthreads();
-  pdl_enter();  // programmatic dependent launch: Z is the producer's output
-  {
-    const int g = threadIdx.x / T;
-    const int t = 2 * blockIdx.x + g;
-    if ((int)threadIdx.x - g * T == 0 && t < a.ntiles) {
-      uint64_t* bar = reinterpret_cast<uint64_t*>(smraw_p + 2 * kGroup) + g;
-      mbar_expect_tx(bar, kTileBytes);
-      tma_load_2d(smraw_p + g * kGroup + kWork, &tmZ, 2 * SG * (t % a.groups), C * (t / a.groups), bar);
-    }
-  }
-  // loop state: the iteration count only; everything else is re-derived from
-  // (laundered) special registers inside the body so that nothing thread- or
-  // tile-dependent stays live across the tile's barriers
-  // the tile body is a real call (see pad_p_body): inlined into this loop,
-  // ptxas keeps ~30 more registers live across the tile's barriers and spills
-  // 1.3 KB per thread; as a function with one integer argument it spills 80 B
-#pragma unroll 1
-  for (int it = 0; pad_p_body<R, C, SG>(&tmZ, &a, smraw_p, it); it++) {
-  }
-}
-
 // row pass: row r = blockIdx.x (length L), output index r + R1 k.
 template <int L, int S>
 __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<L, kSig>())) kbm_row(const double2* __restrict__ in,
@@ -1338,31 +1265,6 @@ struct ChainBM {
     LAUNCH_PDL(bm_pad, grid, T, smem, st, tm, args);
     return NFFT45_OK;
   }
-  // Persistent two-group pad (kbm_pad_p): one CTA per SM, TMA-prefetched tiles.
-  int pad_persist(const double2* Z, double2* Y, const ChainPlanView& pv, double2* xout) {
-    auto bm_pad = kbm_pad_p<R, C, kSig>;
-    constexpr size_t kWork = (fast_smem<2 * C, kSig>() + 2 * sizeof(double) * C + 127) / 128 * 128;
-    constexpr size_t smem = 2 * (kWork + sizeof(double2) * C * kSig) + 16;
-    NFFT_CHECK(bm_attr(bm_pad, smem));
-    constexpr int T = 2 * fast_threads<2 * C, kSig>();
-    const int64_t Q = n / last_stride<2 * C>();
-    const double2* twQ = nullptr;
-    NFFT_CHECK(qtab(Q, &twQ));
-    CUtensorMap tm;
-    NFFT_CHECK(tma_map_rows(&tm, Z, P, Bp, C, kSig));
-    const int ntiles = (int)(R * groups);
-    static const int sms = [] {
-      int dev = 0, v = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-      return v;
-    }();
-    const int grid = std::min(sms, (ntiles + 1) / 2);
-    const PadTileArgs args{Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q,
-                           pv.coef, pv.deconv, pv.cd, xout, ntiles, (int)groups};
-    LAUNCH_PDL(bm_pad, grid, T, smem, st, tm, args);
-    return NFFT45_OK;
-  }
   template <bool XOUT>
   int pad_h(const double2* Z, double2* Y, const ChainPlanView& pv, const double2* xsub, double2* xout) {
     if constexpr (bm_pad_fused<R, C>() && !XOUT) {
@@ -1412,11 +1314,8 @@ struct ChainBM {
   }
   int pad(const double2* Z, double2* Y, const ChainPlanView& pv, const double2* xsub, double2* xout) {
     static const bool tma = getenv("NFFT45_TMA") != nullptr;
-    if (hyb && !small_tiles && !tma && !getenv("NFFT45_PADP"))
+    if (hyb && !small_tiles && !tma)
       return xout ? pad_h<true>(Z, Y, pv, xsub, xout) : pad_h<false>(Z, Y, pv, xsub, xout);
-    static const bool padp = getenv("NFFT45_PADP") != nullptr;
-    if constexpr (C <= 256 && SG == kSig)
-      if (padp && !small_tiles && !(xout && xsub)) return pad_persist(Z, Y, pv, xout);
     if constexpr (C <= 256 && SG == kSig)
       if (tma && !small_tiles && !(xout && xsub)) return pad_tma(Z, Y, pv, xout);
     if (small_tiles || SG < kSig) return pad_g<kSig / 2>(Z, Y, pv, xsub, xout);  // always for C = 1024

@@ -1,5 +1,5 @@
 # A/B of env-switch variants on the C4 bench (kernel table from the profiled pass).
-# VARIANTS="NFFT45_PADP=1 NFFT45_TMA=1" scripts/env_ab.sh   ("-" = default build)
+# VARIANTS="NFFT45_HYB=0 NFFT45_FUSE=0" scripts/env_ab.sh   ("-" = default build)
 cd $GRAFT_REPO_ROOT
 for i in 1 2; do
 for V in - ${VARIANTS}; do

@@ -1,5 +1,5 @@
 """Bitwise check of an env-switch kernel variant against the default build on batch-minor
-chain shapes: python scripts/variant_check.py NFFT45_PADP=1 [more VAR=VAL ...]"""
+chain shapes: python scripts/variant_check.py NFFT45_HYB=0 [more VAR=VAL ...]"""
 import os
 import subprocess
 import sys

@@ -557,7 +557,8 @@ sys.path.insert(0, sys.argv[2])
 import paper_1604_06236_b200 as nf
 out = {}
 for P, B, J in [(1000, 1, 0.3), (4096, 1, 0.45), (4096, 4, 0.3), (1 << 16, 1, 0.3), (1 << 18, 1, 0.4),
-                (4096, 32, 0.3), (1 << 16, 16, 0.3), (1 << 15, 24, 0.3), (12288, 16, 0.3)]:
+                (4096, 32, 0.3), (1 << 16, 16, 0.3), (1 << 15, 24, 0.3), (12288, 16, 0.3),
+                (2048, 16, 0.3), (1 << 14, 24, 0.45), (1 << 17, 17, 0.3)]:
     rng = np.random.default_rng(P + B)
     t = np.mod((np.arange(P) + rng.uniform(-J, J, P)) / P, 1.0)
     plan = nf.build_plan(nf.validate_grid(t), nf.MethodParams.from_mu(1e-15, P, 2))
