@@ -87,7 +87,7 @@ template <int L, int S>
 __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<L, kSig>())) kbm_col(
     const double2* __restrict__ in, double2* __restrict__ out, int L2, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ lo, const double2* __restrict__ hi, int sh, const double2* __restrict__ twQ, int Q,
-    const double* __restrict__ pre, int sw, int pf) {
+    const double* __restrict__ pre, int sw, int pf, int perm) {
   pdl_enter();  // programmatic dependent launch: wait for the producer grid
   extern __shared__ double2 sm[];
   const int n2 = sw ? blockIdx.y : blockIdx.x;
@@ -101,10 +101,15 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<
   // tile base pointers + 32-bit in-tile offsets (n * Bp < 2^31, guarded on the
   // host): the per-element address math stays out of 64-bit registers
   const unsigned ub = (unsigned)Bp;
-  const double2* __restrict__ it = in + (int64_t)n2 * Bp + b0;
+  // perm: the producer (spreading) stored cell i L2 + n2 at row n2 L + i, so this column is one
+  // contiguous range of L rows (DRAM reads like the row pass's instead of L scattered 128-byte runs)
+  // (perm = block size cblk of the producer's row permutation, 0: natural order)
+  const double2* __restrict__ it =
+      in + (perm ? (int64_t)(n2 / perm) * L * perm + n2 % perm : (int64_t)n2) * Bp + b0;
   double2* __restrict__ ot = out + (int64_t)n2 * Bp + b0;
+  const int istep = perm ? perm : L2;
   auto ld = [&](int i, int c) -> double2 {
-    double2 v = it[(unsigned)(i * L2) * ub + c];
+    double2 v = it[(unsigned)(i * istep) * ub + c];
     if (pre) v = rsc(v, __ldg(&pre[(int64_t)i * L2 + n2]));
     return v;
   };
@@ -1145,7 +1150,7 @@ struct ChainBM {
   }
 
   // FFT_2P column pass: R-point columns over the 2C columns of H
-  int col(const double2* in, double2* out) {
+  int col(const double2* in, double2* out, int perm = 0) {
     auto bm_col = kbm_col<R, -1>;
     constexpr size_t smem = fast_smem<R, kSig>();
     NFFT_CHECK(bm_attr(bm_col, smem));
@@ -1154,7 +1159,7 @@ struct ChainBM {
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
     LAUNCH_PDL(bm_col, gdim(2 * C), T, smem, st, in, out, 2 * C, Bp, t.twR, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q,
-           nullptr, (int)sw, pf);
+           nullptr, (int)sw, pf, perm);
     return NFFT45_OK;
   }
 
@@ -1421,14 +1426,29 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
   double2* Z = U + Bp * P;
   double2* X = Z + Bp * P;
   double2* Rs = X + Bp * P;
+  // Spreading stores cell j of the fine grid at row (j % 2C) R + j / 2C, so the column pass of
+  // FFT_2P reads each column as one contiguous range (it wrote and read 128-byte runs 2C rows apart
+  // before: 78 % of the copy rate against the row pass's 98 %) and runs H -> Y instead of in place.
+  // NFFT45_COL_PERM=0 restores the natural order (A/B switch).
+  static const bool perm_on = !(getenv("NFFT45_COL_PERM") && atoi(getenv("NFFT45_COL_PERM")) == 0);
+  // block size of the permutation (NFFT45_COL_BLK, a divisor of 2C)
+  static const int cblk_env = getenv("NFFT45_COL_BLK") ? atoi(getenv("NFFT45_COL_BLK")) : 1;
+  const int cblk = (cblk_env >= 1 && (2 * C) % cblk_env == 0) ? cblk_env : 1;
+  const bool perm = perm_on && spread_layout_pipelined(n, kFastM, Bp);
   auto run = [&]() -> int {
     if (kind == 5) {
       NodeFactor fc5{pv.c5, 0.0, 0};
       // r (or s) -> spread -> colFFT_2P -> band -> mid -> Z
       auto front = [&](const double2* src, bool src_bm) -> int {
-        NFFT_CHECK(spread_layout(g, n, win, src, batch, src_bm ? Bp : 0, fc5, H, Bp, st));
-        NFFT_CHECK(ch.col(H, H));
-        NFFT_CHECK(ch.band(H, U, pv, nullptr));
+        if (perm) {  // grid rows permuted by the spreading kernel: contiguous columns, column pass H -> Y
+          NFFT_CHECK(spread_layout(g, n, win, src, batch, src_bm ? Bp : 0, fc5, H, Bp, st, 2 * C, cblk));
+          NFFT_CHECK(ch.col(H, Y, cblk));
+          NFFT_CHECK(ch.band(Y, U, pv, nullptr));
+        } else {
+          NFFT_CHECK(spread_layout(g, n, win, src, batch, src_bm ? Bp : 0, fc5, H, Bp, st));
+          NFFT_CHECK(ch.col(H, H));
+          NFFT_CHECK(ch.band(H, U, pv, nullptr));
+        }
         NFFT_CHECK(ch.mid(U, Z, pv));
         return NFFT45_OK;
       };
@@ -1461,12 +1481,20 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
       for (int pass = 0; pass < passes; pass++) {
         const bool last = pass == passes - 1;
         NodeFactor ph{nullptr, (double)(P / 2), -1};
-        NFFT_CHECK(spread_layout(g, n, win, X, batch, Bp, ph, H, Bp, st));
-        NFFT_CHECK(ch.col(H, H));
-        // passes >= 2: the band epilogue also stores r itself into Y (free until
-        // the pad below), whose norms feed the NonConvergence check (inverse.py:154-159)
-        NFFT_CHECK(ch.band(H, U, pv, AT, norms ? Y : nullptr));
-        if (norms) NFFT_CHECK(norms_bm(Y, P, batch, Bp, norms + (int64_t)pass * batch, st));
+        // passes >= 2: the band epilogue also stores r itself into the free grid buffer (Y, or H
+        // when the column pass ran H -> Y), whose norms feed the NonConvergence check
+        // (inverse.py:154-159)
+        double2* rbuf = perm ? H : Y;
+        if (perm) {
+          NFFT_CHECK(spread_layout(g, n, win, X, batch, Bp, ph, H, Bp, st, 2 * C, cblk));
+          NFFT_CHECK(ch.col(H, Y, cblk));
+          NFFT_CHECK(ch.band(Y, U, pv, AT, norms ? rbuf : nullptr));
+        } else {
+          NFFT_CHECK(spread_layout(g, n, win, X, batch, Bp, ph, H, Bp, st));
+          NFFT_CHECK(ch.col(H, H));
+          NFFT_CHECK(ch.band(H, U, pv, AT, norms ? rbuf : nullptr));
+        }
+        if (norms) NFFT_CHECK(norms_bm(rbuf, P, batch, Bp, norms + (int64_t)pass * batch, st));
         NFFT_CHECK(back(last ? out : X, last ? 0 : Bp, X, Bp));
       }
     }

@@ -410,11 +410,19 @@ int gather(const GridDev& g, int64_t n, const Window& win, const double2* H, int
   return gather_mode(g, n, win, H, batch, f, sub, sub ? 1 : 0, out, st);
 }
 
-int spread_layout(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch, int64_t amp_ld,
-                  NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st) {
+bool spread_layout_pipelined(int64_t n, int m, int64_t H_ld) {
   static const bool no_pipe = getenv("NFFT45_NO_PIPE") != nullptr;  // A/B switch
-  if (!no_pipe && win.m == kFastM && n >= 128 && H_ld && amp)
-    return spread_pipelined(g, n, win, amp, batch, amp_ld, f, H, H_ld, st);
+  return !no_pipe && m == kFastM && n >= 128 && H_ld != 0;
+}
+
+int spread_layout(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch, int64_t amp_ld,
+                  NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st, int64_t cols, int cblk) {
+  if (spread_layout_pipelined(n, win.m, H_ld) && amp)
+    return spread_pipelined(g, n, win, amp, batch, amp_ld, f, H, H_ld, st, cols, cblk);
+  if (cols) {
+    set_error(NFFT45_ERR_INVALID_ARGUMENT, "permuted grid rows need the pipelined spreading kernel");
+    return NFFT45_ERR_INVALID_ARGUMENT;
+  }
   if (win.m == kFastM && n >= 128 && (amp_ld || H_ld || batch >= 32))
     return spread_batched(g, n, win, amp, batch, f, H, st, batch >= 64 ? 2 : 1, amp_ld, H_ld);
   if (amp_ld || H_ld) {

@@ -266,7 +266,8 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
                                                     int64_t Q, int64_t n, double alpha, GaussTab G,
                                                     const double2* __restrict__ amp, int64_t batch, NodeFactor nf,
                                                     double2* __restrict__ H, const int2* __restrict__ ranges, int NS,
-                                                    int64_t amp_ld, int64_t H_ld, int ngroups, int sw) {
+                                                    int64_t amp_ld, int64_t H_ld, int ngroups, int sw, int cols,
+                                                    int cblk) {
   pdl_enter();  // programmatic dependent launch: wait for the producer grid
   constexpr int SIG = 32 * SPL;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -430,15 +431,29 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
       }
     }
   };
+  // cols > 0: cell j = i cols + n2 goes to row (n2 / cblk) (L cblk) + i cblk + n2 % cblk, L = n / cols:
+  // the columns of the four-step layout in blocks of cblk (cblk = cols: natural order, cblk = 1:
+  // every column one contiguous range of L rows)
+  const int rows_per_col = cols > 0 ? (int)(n / cols) : 0;
+  // rows of this warp's 8 cells, once per CTA (the divisions by the run-time `cols`, `cblk` cost
+  // more than a signal group's FMAs when they sit in the store loop)
+  int rowc[kCPW];
+#pragma unroll
+  for (int c = 0; c < kCPW; c++) {
+    const int j = jw + c;
+    const int n2 = cols > 0 ? j % cols : 0;
+    rowc[c] = cols > 0 ? (n2 / cblk) * rows_per_col * cblk + (j / cols) * cblk + n2 % cblk : j;
+  }
   auto store = [&](int64_t g, double2 (&acc)[kCPW][SPL]) {
     const int ncell_w = (int)min((int64_t)kCPW, n - jw);
 #pragma unroll
-    for (int c = 0; c < kCPW; c++)
+    for (int c = 0; c < kCPW; c++) {
 #pragma unroll
       for (int s2 = 0; s2 < SPL; s2++) {
         const int64_t b = g * SIG + lane + 32 * s2;
-        if (c < ncell_w && b < H_ld) H[(int64_t)(jw + c) * H_ld + b] = acc[c][s2];
+        if (c < ncell_w && b < H_ld) H[(int64_t)rowc[c] * H_ld + b] = acc[c][s2];
       }
+    }
   };
 
   if (pipelined) {
@@ -490,7 +505,7 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
 }
 
 int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch,
-                     int64_t amp_ld, NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st) {
+                     int64_t amp_ld, NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st, int64_t cols, int cblk) {
   const int64_t ntiles = ceil_div(n, kSpreadTile);
   const int NS = tile_images(n, win.m, kSpreadTile);
   if (NS > 8) return NFFT45_ERR_INVALID_ARGUMENT;
@@ -509,7 +524,7 @@ int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const doubl
   NFFT_CUDA(cudaFuncSetAttribute(spread_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const dim3 grid = sw ? dim3((unsigned)slices, (unsigned)ntiles) : dim3((unsigned)ntiles, (unsigned)slices);
   LAUNCH_PDL(spread_p, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), amp, batch, f, H, ranges,
-         NS, amp_ld, H_ld, ngroups, sw);
+         NS, amp_ld, H_ld, ngroups, sw, (int)cols, cblk);
   if (own) NFFT_CUDA(cudaFreeAsync(own, st));
   return NFFT45_OK;
 }

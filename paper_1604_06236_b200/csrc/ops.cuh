@@ -126,11 +126,19 @@ int gather_batched(const GridDev& g, int64_t n, const Window& win, const double2
 int gather_persistent(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t H_ld, int64_t batch,
                       NodeFactor f, const double2* sub, int64_t sub_ld, int mode, double2* out, int64_t out_ld,
                       cudaStream_t st);
+// cols > 0: cell j = i cols + n2 of the batch-minor grid is stored at row
+// (n2 / cblk) (L cblk) + i cblk + n2 % cblk (L = n / cols): the columns of the n = L x cols four-step
+// layout, in blocks of cblk, become contiguous row ranges, so the column pass of FFT_2P reads L-row
+// ranges with stride cblk instead of 128-byte runs `cols` rows apart (a cell is a whole row of
+// signals either way: the permutation costs the spreading kernel no coalescing)
 int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch,
-                     int64_t amp_ld, NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st);
+                     int64_t amp_ld, NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st, int64_t cols = 0,
+                     int cblk = 1);
+// true when spread_layout writes through the pipelined kernel (the one that honours `cols`)
+bool spread_layout_pipelined(int64_t n, int m, int64_t H_ld);
 // Layout-aware wrappers for the batch-minor chains (ld == 0: signal-major).
 int spread_layout(const GridDev& g, int64_t n, const Window& win, const double2* amp, int64_t batch, int64_t amp_ld,
-                  NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st);
+                  NodeFactor f, double2* H, int64_t H_ld, cudaStream_t st, int64_t cols = 0, int cblk = 1);
 int gather_layout(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t H_ld, int64_t batch,
                   NodeFactor f, const double2* sub, int64_t sub_ld, int mode, double2* out, int64_t out_ld,
                   cudaStream_t st);

@@ -590,7 +590,10 @@ def test_kernel_variants_bitwise(tmp_path):
                 # round 2: all-column-fast two-FFT kernels instead of the hybrid (warp-local) ones, hybrid
                 # without the register / shuffle handoffs, cp.async instead of TMA cell tiles in the
                 # persistent gather, the persistent TMA-prefetching pad
-                {"NFFT45_HYB": "0"}, {"NFFT45_FUSE": "0"}, {"NFFT45_GATHER_TMA": "0"}, {"NFFT45_PAD_PERSIST": "1"})
+                {"NFFT45_HYB": "0"}, {"NFFT45_FUSE": "0"}, {"NFFT45_GATHER_TMA": "0"}, {"NFFT45_PAD_PERSIST": "1"},
+                # natural-order fine grid (column pass in place) instead of the row-permuted one, and a
+                # blocked permutation
+                {"NFFT45_COL_PERM": "0"}, {"NFFT45_COL_BLK": "8"})
     outs = []
     for i, extra in enumerate(variants):
         f = tmp_path / f"v{i}.npz"
