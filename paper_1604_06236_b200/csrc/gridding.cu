@@ -116,25 +116,6 @@ struct RangeCache {
   std::vector<Flags> gf;  // persistent-gather overflow flags per fine-grid size
 };
 
-int gather_flags_cache(const GridDev& g, int64_t n, cudaStream_t st) {
-  if (!g.rc) return NFFT45_OK;
-  {
-    std::lock_guard<std::mutex> lk(g.rc->mu);
-    for (const auto& e : g.rc->gf)
-      if (e.n == n) return NFFT45_OK;
-  }
-  const int64_t nblk = gather_blocks(g.Q);
-  int* d = nullptr;
-  NFFT_CUDA(cudaMalloc(&d, sizeof(int) * (nblk + 1)));
-  NFFT_CHECK(gather_flags_compute(g, n, d, d + nblk, st));
-  int any = 0;
-  NFFT_CUDA(cudaMemcpyAsync(&any, d + nblk, sizeof(int), cudaMemcpyDeviceToHost, st));
-  NFFT_CUDA(cudaStreamSynchronize(st));
-  std::lock_guard<std::mutex> lk(g.rc->mu);
-  g.rc->gf.push_back({n, d, any != 0});
-  return NFFT45_OK;
-}
-
 bool gather_flags_lookup(const GridDev& g, int64_t n, int** flags, bool* any) {
   if (!g.rc) return false;
   std::lock_guard<std::mutex> lk(g.rc->mu);
@@ -166,29 +147,121 @@ int tile_ranges(const GridDev& g, int64_t n, int m, int TC, int NS, cudaStream_t
   return NFFT45_OK;
 }
 
-int tile_ranges_cache(const GridDev& g, int64_t n, int m, int TC, cudaStream_t st) {
+// Node-set caches a plan needs for its fine grid of n cells (per-tile node ranges for the
+// spreading tile sizes in TCs, overflow flags of the persistent gather), in two phases so the
+// plan build pays ONE stream synchronize: begin() allocates from the stream-ordered pool and
+// launches everything on `st` (all tile sizes in one launch); end(), called after the caller
+// has synchronized `st`, publishes the tables in the node set's cache (commit) or releases
+// them.  Entries only become visible to other threads once their kernels have completed.
+struct GridCachePending {
+  std::vector<RangeCache::Entry> ranges;
+  RangeCache::Flags flags{0, nullptr, false};
+  int any = 0;
+};
+
+struct TileRangeJobs {
+  struct J {
+    int TC, NS;
+    int64_t ntiles, first;  // first: index of the job's first (tile, image) pair in the launch
+    int2* out;
+  } j[3];
+  int count;
+};
+
+__global__ void k_tile_ranges_multi(const double* __restrict__ ts, int64_t Q, int64_t n, int m,
+                                    const __grid_constant__ TileRangeJobs jobs) {
+  const int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int k = 0;
+  while (k + 1 < jobs.count && e0 >= jobs.j[k + 1].first) k++;
+  const int64_t e = e0 - jobs.j[k].first;
+  const int TC = jobs.j[k].TC, NS = jobs.j[k].NS;
+  if (e >= jobs.j[k].ntiles * NS) return;
+  const int64_t tile = e / NS;
+  const int si = (int)(e % NS);
+  const int64_t j0 = tile * TC, j1 = min(j0 + TC, n);
+  const int64_t s_lo = floordiv(-m - (j1 - 1) + n - 1, n);
+  const int64_t s_hi = floordiv(n + m - j0, n);
+  const int64_t s = s_lo + si;
+  int2 r = make_int2(0, 0);
+  if (s <= s_hi) {
+    r.x = (int)first_ge(ts, Q, (double)n, j0 + s * n - m);
+    r.y = (int)first_ge(ts, Q, (double)n, j1 - 1 + s * n + m + 1);
+  }
+  jobs.j[k].out[e] = r;
+}
+
+int grid_caches_begin(const GridDev& g, int64_t n, int m, const int* TCs, int nTC, cudaStream_t st,
+                      GridCachePending** out) {
+  *out = nullptr;
   if (!g.rc) return NFFT45_OK;
-  const int NS = tile_images(n, m, TC);
-  if (NS > 8) return NFFT45_OK;
+  GridCachePending* pd = new GridCachePending();
+  *out = pd;
+  TileRangeJobs jobs{};
+  int64_t total = 0;
   {
     std::lock_guard<std::mutex> lk(g.rc->mu);
-    for (const auto& e : g.rc->v)
-      if (e.n == n && e.m == m && e.TC == TC && e.NS == NS) return NFFT45_OK;
+    for (int i = 0; i < nTC && jobs.count < 3; i++) {
+      const int TC = TCs[i], NS = tile_images(n, m, TC);
+      if (NS > 8) continue;
+      bool have = false;
+      for (const auto& e : g.rc->v) have = have || (e.n == n && e.m == m && e.TC == TC && e.NS == NS);
+      for (int k = 0; k < jobs.count; k++) have = have || jobs.j[k].TC == TC;
+      if (have) continue;
+      const int64_t ntiles = ceil_div(n, TC);
+      jobs.j[jobs.count++] = {TC, NS, ntiles, total, nullptr};
+      total += ceil_div(ntiles * NS, 128) * 128;  // jobs start on CTA boundaries
+    }
+    for (const auto& e : g.rc->gf)
+      if (e.n == n) pd->flags.n = -1;  // already cached
   }
-  const int64_t ntiles = ceil_div(n, TC);
-  int2* r = nullptr;
-  NFFT_CUDA(cudaMalloc(&r, sizeof(int2) * ntiles * NS));
-  LAUNCH(k_tile_ranges, (unsigned)ceil_div(ntiles * NS, 128), 128, 0, st, g.ts, g.Q, n, m, TC, ntiles, NS, r);
-  NFFT_CUDA(cudaStreamSynchronize(st));
-  std::lock_guard<std::mutex> lk(g.rc->mu);
-  g.rc->v.push_back({n, m, TC, NS, r});
+  for (int k = 0; k < jobs.count; k++) {
+    int2* r = nullptr;
+    NFFT_CUDA(cudaMallocAsync(&r, sizeof(int2) * jobs.j[k].ntiles * jobs.j[k].NS, st));
+    jobs.j[k].out = r;
+    pd->ranges.push_back({n, m, jobs.j[k].TC, jobs.j[k].NS, r});
+  }
+  if (jobs.count > 0) LAUNCH(k_tile_ranges_multi, (unsigned)(total / 128), 128, 0, st, g.ts, g.Q, n, m, jobs);
+  if (pd->flags.n == 0) {
+    const int64_t nblk = gather_blocks(g.Q);
+    int* d = nullptr;
+    NFFT_CUDA(cudaMallocAsync(&d, sizeof(int) * (nblk + 1), st));
+    pd->flags = {n, d, false};
+    NFFT_CHECK(gather_flags_compute(g, n, d, d + nblk, st));
+    NFFT_CUDA(cudaMemcpyAsync(&pd->any, d + nblk, sizeof(int), cudaMemcpyDeviceToHost, st));
+  }
   return NFFT45_OK;
+}
+
+void grid_caches_end(const GridDev& g, GridCachePending* pd, bool commit, cudaStream_t st) {
+  if (!pd) return;
+  if (commit && g.rc) {
+    std::lock_guard<std::mutex> lk(g.rc->mu);
+    for (auto& e : pd->ranges) {
+      bool dup = false;  // another thread published the same table meanwhile
+      for (const auto& x : g.rc->v) dup = dup || (x.n == e.n && x.m == e.m && x.TC == e.TC && x.NS == e.NS);
+      if (dup) cudaFreeAsync(e.d, st);
+      else g.rc->v.push_back(e);
+    }
+    if (pd->flags.d) {
+      bool dup = false;
+      for (const auto& x : g.rc->gf) dup = dup || x.n == pd->flags.n;
+      if (dup) cudaFreeAsync(pd->flags.d, st);
+      else g.rc->gf.push_back({pd->flags.n, pd->flags.d, pd->any != 0});
+    }
+  } else {
+    for (auto& e : pd->ranges) cudaFreeAsync(e.d, st);
+    if (pd->flags.d) cudaFreeAsync(pd->flags.d, st);
+  }
+  delete pd;
 }
 
 RangeCache* range_cache_new() { return new RangeCache(); }
 
 void tile_ranges_free(GridDev& g) {
   if (!g.rc) return;
+  // the tables come from the stream-ordered pool (cudaFree does not wait for pool memory):
+  // solves that read them may still be running on any stream
+  if (!g.rc->v.empty() || !g.rc->gf.empty()) cudaDeviceSynchronize();
   for (auto& e : g.rc->v) cudaFree(e.d);
   for (auto& e : g.rc->gf) cudaFree(e.d);
   delete g.rc;

@@ -313,12 +313,21 @@ __global__ void k_fused_factors(const double* __restrict__ ts, const int* __rest
   c4[i] = cmul(w, cis_turns(x));
 }
 
+// max (or min) of the per-CTA partials: one CTA of 256 threads (max / min are exact and
+// order-independent, so the tree gives the value of the serial loop it replaces, which took
+// 40 us for 1024 partials: dependent L2 loads from one thread)
 __global__ void k_max_reduce(const double* in, int n, double* out, int is_min) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double r = is_min ? INFINITY : 0.0;
-    for (int i = 0; i < n; i++) r = is_min ? fmin(r, in[i]) : fmax(r, in[i]);
-    *out = r;
+  __shared__ double red[256];
+  double r = is_min ? INFINITY : 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) r = is_min ? fmin(r, in[i]) : fmax(r, in[i]);
+  red[threadIdx.x] = r;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w)
+      red[threadIdx.x] = is_min ? fmin(red[threadIdx.x], red[threadIdx.x + w]) : fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
   }
+  if (threadIdx.x == 0) *out = red[0];
 }
 
 }  // namespace nfft45
@@ -388,7 +397,7 @@ static int ks_core(const GridDev& g, const double2* v, double2* ks, double* d_ma
   Scratch part(st);
   NFFT_CHECK(part.alloc(sizeof(double) * blocks));
   LAUNCH(k_kernel_samples, blocks, 256, 0, st, v, ks, P, const_turns(g), part.d());
-  LAUNCH(k_max_reduce, 1, 32, 0, st, part.d(), blocks, d_maxre, 0);
+  LAUNCH(k_max_reduce, 1, 256, 0, st, part.d(), blocks, d_maxre, 0);
   return NFFT45_OK;
 }
 
@@ -407,7 +416,7 @@ static int deriv_core(const GridDev& g, const double2* L, int m, double2* dL, do
   int blocks = (int)std::min<int64_t>(ceil_div(P, 256), 1024);
   NFFT_CHECK(part.alloc(sizeof(double) * blocks));
   LAUNCH(k_min_abs, blocks, 256, 0, st, dL, P, part.d());
-  LAUNCH(k_max_reduce, 1, 32, 0, st, part.d(), blocks, d_minabs, 1);
+  LAUNCH(k_max_reduce, 1, 256, 0, st, part.d(), blocks, d_minabs, 1);
   return NFFT45_OK;
 }
 
@@ -1010,7 +1019,7 @@ int nfft45_min_abs(const double* x, int64_t n, double* out, void* st) {
   NFFT_CHECK(part.alloc(sizeof(double) * blocks));
   NFFT_CHECK(res.alloc(sizeof(double)));
   LAUNCH(k_min_abs, blocks, 256, 0, s, C2(x), n, part.d());
-  LAUNCH(k_max_reduce, 1, 32, 0, s, part.d(), blocks, res.d(), 1);
+  LAUNCH(k_max_reduce, 1, 256, 0, s, part.d(), blocks, res.d(), 1);
   NFFT_CUDA(cudaMemcpyAsync(out, res.d(), sizeof(double), cudaMemcpyDeviceToHost, s));
   NFFT_CUDA(cudaStreamSynchronize(s));
   return NFFT45_OK;
@@ -1121,18 +1130,22 @@ int nfft45_plan_create_terms(const nfft45_grid* g, double a, int64_t R, int m, v
       cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) status = cuda_fail(le, "plan tables");
     }
+    // node-set caches of the solve grid n = 2P (per-tile node ranges of the spreading kernels,
+    // overflow flags of the persistent gather): launched behind the tables so the build pays
+    // one stream synchronize (check_guards), published after it
+    GridCachePending* pend = nullptr;
+    if (!status && m == kFastM) {
+      int tcs[3] = {64, getenv("NFFT45_STILE") ? atoi(getenv("NFFT45_STILE")) : 128, 32};  // 32: warp tiles
+      status = grid_caches_begin(g->d, 2 * P, m, tcs, 2 * P <= (int64_t(1) << 17) ? 3 : 2, s, &pend);
+    }
     if (!status) status = check_guards(guard.d(), 1, 1, s);
+    else cudaStreamSynchronize(s);
+    grid_caches_end(g->d, pend, status == NFFT45_OK, s);
   }
   const auto T2 = now();
-  if (!status && m == kFastM) {  // per-tile node ranges of the solve grid n = 2P (spread kernels)
-    status = tile_ranges_cache(g->d, 2 * P, m, 64, s);
-    if (!status) status = tile_ranges_cache(g->d, 2 * P, m, getenv("NFFT45_STILE") ? atoi(getenv("NFFT45_STILE")) : 128, s);
-    if (!status && 2 * P <= (int64_t(1) << 17)) status = tile_ranges_cache(g->d, 2 * P, m, 32, s);  // warp tiles
-    if (!status) status = gather_flags_cache(g->d, 2 * P, s);
-  }
   if (timing)
-    fprintf(stderr, "plan P=%lld: alloc %.3f ms, tables+guards %.3f ms, caches %.3f ms\n", (long long)P, ms(T0, T1),
-            ms(T1, T2), ms(T2, now()));
+    fprintf(stderr, "plan P=%lld: alloc %.3f ms, tables + caches + guards %.3f ms\n", (long long)P, ms(T0, T1),
+            ms(T1, T2));
   if (status) {
     cudaStreamSynchronize(s);
     cudaFreeAsync(p->tables, s);

@@ -21,15 +21,19 @@ struct GridDev {
 // of n cells: the cached device table when the node set holds one for
 // (n, m, TC), else computed on `st` into `*own` (caller frees it, stream-ordered).
 int tile_ranges(const GridDev& g, int64_t n, int m, int TC, int NS, cudaStream_t st, const int2** out, int2** own);
-// Compute and cache the table for (n, m, TC) (synchronous; outside stream capture).
-int tile_ranges_cache(const GridDev& g, int64_t n, int m, int TC, cudaStream_t st);
+// Node-set caches of a plan's fine grid (tile ranges for the tile sizes TCs, persistent-gather
+// overflow flags): begin() launches on `st` without synchronizing, end() publishes (commit) or
+// releases them after the caller has synchronized `st` (gridding.cu; outside stream capture).
+struct GridCachePending;
+int grid_caches_begin(const GridDev& g, int64_t n, int m, const int* TCs, int nTC, cudaStream_t st,
+                      GridCachePending** out);
+void grid_caches_end(const GridDev& g, GridCachePending* pd, bool commit, cudaStream_t st);
 void tile_ranges_free(GridDev& g);
 RangeCache* range_cache_new();
 // Per-node-block overflow flags of the persistent gather for a fine grid of n
 // cells (gridding_b.cu): cached per node set at plan creation.
 int gather_flags_compute(const GridDev& g, int64_t n, int* flags, int* any, cudaStream_t st);
 int64_t gather_blocks(int64_t Q);
-int gather_flags_cache(const GridDev& g, int64_t n, cudaStream_t st);
 bool gather_flags_lookup(const GridDev& g, int64_t n, int** flags, bool* any);
 inline int tile_images(int64_t n, int m, int TC) { return (int)((2 * m + TC - 1) / n + 3); }
 
