@@ -413,6 +413,30 @@ def test_concurrent_solves_share_one_plan():
         assert np.array_equal(a, b)
 
 
+def test_concurrent_plan_builds_share_one_node_set():
+    """Plans built at the same time on one node-set handle (each build launches the node
+    set's caches and publishes them after its own stream synchronize; the losers of the race
+    drop their copies) give bitwise the tables and solves of a serial build."""
+    rng = np.random.default_rng(151)
+    P = 4096
+    t = np.arange(P) / P + rng.uniform(0, 0.6 / P, P)
+    prm = std_params(P)
+    ref_plan = nf.build_plan(nf.validate_grid(t), prm)
+    x = randc(P, rng)
+    want5, want4 = nf.refine_type5(ref_plan, x, passes=1), nf.refine_type4(ref_plan, x, passes=1)
+    g = nf.validate_grid(t)  # fresh handle: no cached tile ranges / gather flags yet
+    g.device_handle(0)
+    with ThreadPoolExecutor(max_workers=4) as pool:
+        plans = list(pool.map(lambda _: nf.build_plan(g, prm), range(8)))
+    for p in plans:
+        assert np.array_equal(p.kernel_data.kernel_samples, ref_plan.kernel_data.kernel_samples)
+        assert np.array_equal(nf.refine_type5(p, x, passes=1), want5)
+        assert np.array_equal(nf.refine_type4(p, x, passes=1), want4)
+    batch = np.stack([x, 2 * x, x[::-1]] * 6)  # 18 rows: the batch-minor chains and the persistent gather
+    got = nf.refine_type5(plans[-1], batch, passes=1)
+    assert np.array_equal(got, nf.refine_type5(ref_plan, batch, passes=1))
+
+
 def test_flop_reports_match_reference(golden):
     def rep(fc):
         r = fc.report()
