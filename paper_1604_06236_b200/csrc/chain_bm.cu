@@ -1057,6 +1057,93 @@ __global__ void __launch_bounds__(fast_threads<C, 4 * RW>(), bm_minb(fast_thread
   fast_tile_fft<C, 4 * RW, -1, true>(sm, ld, st, tw);
 }
 
+// ------------------------------------------------------------------------
+// Batched FORWARD transforms (nfft_type1 / nfft_type2 with R = P = Q, forward.py:26-102) on
+// the batch-minor passes: the user's signal-major operand meets the batch-minor grid in ONE
+// boundary kernel per direction, on 2-D tiles of KK adjacent indices x 8 / KK signals of length
+// 2C (KK = 2: 32-byte runs on the signal-major side, 64-byte runs on the batch-minor side).
+//
+// deconvolution weights of the band p < P of the n = 2P grid (gridding.py:90), once per call
+__global__ void k_fwd_deconv(double* __restrict__ d, int64_t P, double wb) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < P) d[p] = deconv_weight(p, P / 2, 2 * P, wb);
+}
+
+// Launch order (1-D grid): W index blocks x all G signal groups, then the next W index blocks.
+// The ~150 resident CTAs then cover W x 64 bytes of every signal-major row AND ~150 / W x 64
+// bytes of every batch-minor row (index blocks fastest alone leaves the batch-minor side with
+// isolated 64-byte runs, signal groups fastest alone the signal-major side).
+__device__ __forceinline__ void fwd_block(int W, int G, int& kb, int& sg) {
+  const unsigned L = blockIdx.x;
+  const unsigned per = (unsigned)W * (unsigned)G;
+  kb = (int)((L / per) * W + L % W);
+  sg = (int)((L % per) / W);
+}
+
+// type-2 front: S[b][p] (signal-major) * deconv(p) -> zero-padded column IFFT_2P (columns
+// k = KK kb + c % KK of the n = R x 2C layout: input position (m1 - C/2) mod 2C holds
+// p = k + R m1, m1 < C) -> W_n^{+k n2} -> Y[(n2 R + k)][b]; kbm_row + the gather finish it.
+// 8-column tiles (KK indices x 8 / KK signals, 256 threads for 2C = 512, two CTAs per SM) on
+// the hybrid schedule: the passes between the global-memory ones are warp-local (hyb_passes),
+// 2 CTA barriers per tile (a 16-column, 512-thread tile with a barrier per pass measured
+// 1.43 ms for this kernel at C4 size against 1.00 ms, 1.04 against 0.80 ms for kbm_fwd_out_h).
+template <int R, int C, int KK>
+__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_fwd_in_h(
+    const double2* __restrict__ S, int64_t batch, double2* __restrict__ Y, int64_t Bp, const double2* __restrict__ tw,
+    const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN, const double2* __restrict__ twQ, int Q,
+    const double* __restrict__ deconv, int W, int G) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
+  constexpr int64_t P = (int64_t)R * C;
+  constexpr int NC = 2 * C;
+  constexpr int BB = 8 / KK;
+  using Tr = FastTraits<NC>;
+  extern __shared__ double2 sm[];
+  int kb, sg;
+  fwd_block(W, G, kb, sg);
+  const int k0 = kb * KK;
+  const int64_t bb = (int64_t)sg * BB;
+  auto ld = [&](int i, int c) -> double2 {
+    const int m1 = (i + C / 2) & (NC - 1);
+    const int64_t b = bb + c / KK;
+    if (m1 >= C || b >= batch) return make_double2(0.0, 0.0);
+    const int64_t p = (int64_t)(k0 + (c % KK)) + (int64_t)R * m1;
+    return rsc(S[b * P + p], __ldg(&deconv[p]));
+  };
+  auto st = [&](int n2, int c, double2 v) { Y[((int64_t)n2 * R + k0 + (c % KK)) * Bp + bb + c / KK] = v; };
+  const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, k0, KK - 1};
+  hyb_tile_fft<NC, +1, Tr, hyb_mask<Tr>(true, true), false, false>(sm, ld, st, tw, pt);
+}
+
+// type-1 back: rows k1 = KK kb + c % KK of the column pass's output T[(k1 2C + n2)][b]
+// -> row FFT_2P -> band m1 = (k2 + C/2) mod 2C < C -> * deconv(p), p = k1 + R m1 [- sub]
+// -> out[b][p] (signal-major).
+template <int R, int C, int KK>
+__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_fwd_out_h(
+    const double2* __restrict__ T, double2* __restrict__ out, int64_t batch, int64_t Bp, const double2* __restrict__ tw,
+    const double2* __restrict__ sub, const double* __restrict__ deconv, int W, int G) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
+  constexpr int64_t P = (int64_t)R * C;
+  constexpr int NC = 2 * C;
+  constexpr int BB = 8 / KK;
+  using Tr = FastTraits<NC>;
+  extern __shared__ double2 sm[];
+  int kb, sg;
+  fwd_block(W, G, kb, sg);
+  const int k0 = kb * KK;
+  const int64_t bb = (int64_t)sg * BB;
+  auto ld = [&](int i, int c) -> double2 { return T[((int64_t)(k0 + (c % KK)) * NC + i) * Bp + bb + c / KK]; };
+  auto st = [&](int k2, int c, double2 v) {
+    const int m1 = (k2 + C / 2) & (NC - 1);
+    const int64_t b = bb + c / KK;
+    if (m1 >= C || b >= batch) return;
+    const int64_t p = (int64_t)(k0 + (c % KK)) + (int64_t)R * m1;
+    v = rsc(v, __ldg(&deconv[p]));
+    if (sub) v = csub(v, sub[b * P + p]);
+    out[b * P + p] = v;
+  };
+  hyb_tile_fft<NC, -1, Tr, hyb_mask<Tr>(true, true), false, false>(sm, ld, st, tw);
+}
+
 // Kernel-only build for register / SASS experiments:
 //   nvcc ... -DNFFT45_EXP_ONLY -Xptxas -v -c csrc/chain_bm.cu
 #ifdef NFFT45_EXP_ONLY
@@ -1337,6 +1424,53 @@ struct ChainBM {
     return NFFT45_OK;
   }
 
+  // forward type-2 front / type-1 back boundary kernels (KK indices x 8 / KK signals, length 2C)
+  static int fwd_w(int nkb) {  // index blocks per launch-order group (a divisor of nkb; NFFT45_FWD_W for A/B runs)
+    static const int env = getenv("NFFT45_FWD_W") ? atoi(getenv("NFFT45_FWD_W")) : 8;
+    int w = env < 1 ? 1 : env;
+    while (nkb % w) w--;
+    return w;
+  }
+  template <int KK>
+  int fwd_in_h(const double2* S, double2* Y, const double* deconv) {
+    if constexpr (hyb_ok<2 * C>()) {
+      auto bm_fwd_in = kbm_fwd_in_h<R, C, KK>;
+      constexpr size_t smem = sizeof(double2) * 2 * C * kSig;
+      NFFT_CHECK(bm_attr(bm_fwd_in, smem));
+      constexpr int T = fast_threads<2 * C, kSig>();
+      const int64_t Q = n / last_stride<2 * C>();
+      const double2* twQ = nullptr;
+      NFFT_CHECK(qtab(Q, &twQ));
+      const int G = (int)ceil_div(Bp, 8 / KK);
+      LAUNCH_PDL(bm_fwd_in, dim3((unsigned)((R / KK) * G)), T, smem, st, S, batch, Y, Bp, t.tw2C, t.tN->lo, t.tN->hi,
+                 t.tN->s, twQ, (int)Q, deconv, fwd_w(R / KK), G);
+    }
+    return NFFT45_OK;
+  }
+  template <int KK>
+  int fwd_out_h(const double2* T_, double2* out, const double2* sub, const double* deconv) {
+    if constexpr (hyb_ok<2 * C>()) {
+      auto bm_fwd_out = kbm_fwd_out_h<R, C, KK>;
+      constexpr size_t smem = sizeof(double2) * 2 * C * kSig;
+      NFFT_CHECK(bm_attr(bm_fwd_out, smem));
+      constexpr int T = fast_threads<2 * C, kSig>();
+      const int G = (int)ceil_div(Bp, 8 / KK);
+      LAUNCH_PDL(bm_fwd_out, dim3((unsigned)((R / KK) * G)), T, smem, st, T_, out, batch, Bp, t.tw2C, sub, deconv,
+                 fwd_w(R / KK), G);
+    }
+    return NFFT45_OK;
+  }
+  static int fwd_kk() {  // tile shape (NFFT45_FWD_KK = 2 | 4 for A/B runs)
+    static const int kk = getenv("NFFT45_FWD_KK") ? atoi(getenv("NFFT45_FWD_KK")) : 2;
+    return kk == 4 ? 4 : 2;
+  }
+  int fwd_in(const double2* S, double2* Y, const double* deconv) {
+    return fwd_kk() == 2 ? fwd_in_h<2>(S, Y, deconv) : fwd_in_h<4>(S, Y, deconv);
+  }
+  int fwd_out(const double2* T_, double2* out, const double2* sub, const double* deconv) {
+    return fwd_kk() == 2 ? fwd_out_h<2>(T_, out, sub, deconv) : fwd_out_h<4>(T_, out, sub, deconv);
+  }
+
   int colin(const double2* A, double2* U, const ChainPlanView& pv, double2* AT) {
     constexpr int RW = bm_rw<C>();
     auto bm_colin = kbm_colin<R, C, RW>;
@@ -1503,6 +1637,87 @@ static int chain_solve_bm(const ChainPlanView& pv, int kind, const double2* data
   status = run();
   cudaFreeAsync(base, st);
   return status;
+}
+
+// Batched forward transform on the batch-minor passes (kind 1: out[b][p] = sum_q a[b][q]
+// e^{-2 pi i p t_q} [- sub]; kind 2: out[b][q] = sum_p S[b][p] e^{+2 pi i p t_q} [- sub]), R = P = Q.
+template <int R, int C>
+static int forward_solve_bm(const GridDev& g, int kind, const double2* in, int64_t batch, const double2* sub,
+                            double2* out, cudaStream_t st) {
+  using Ch = ChainBM<R, C>;
+  constexpr int64_t P = Ch::P, n = Ch::n;
+  Ch ch;
+  ch.st = st;
+  ch.batch = batch;
+  ch.Bp = ceil_div(batch, kSig) * kSig;
+  ch.groups = (unsigned)(ch.Bp / kSig);
+  ch.sw = true;
+  int status = NFFT45_OK;
+  {
+    const FftTables* a = fft_tables(R, st, &status);
+    if (!a) return status;
+    const FftTables* c = fft_tables(2 * C, st, &status);
+    if (!c) return status;
+    ch.t.twR = a->tw;
+    ch.t.twC = nullptr;
+    ch.t.tw2C = c->tw;
+    ch.t.tP = nullptr;
+    ch.t.tN = fft_tables(n, st, &status);
+    if (!ch.t.tN) return status;
+  }
+  const int64_t Bp = ch.Bp;
+  const Window win = Window::make(kFastM);
+  double2* base = nullptr;
+  NFFT_CUDA(cudaMallocAsync(&base, sizeof(double2) * Bp * 2 * n + sizeof(double) * P, st));
+  double2* H = base;
+  double2* Y = H + Bp * n;
+  double* dtab = reinterpret_cast<double*>(Y + Bp * n);
+  auto run = [&]() -> int {
+    LAUNCH(k_fwd_deconv, (unsigned)ceil_div(P, 256), 256, 0, st, dtab, P, win.b);
+    if (kind == 1) {
+      const NodeFactor f{nullptr, (double)(P / 2), -1};
+      if (spread_layout_pipelined(n, kFastM, Bp)) {  // row-permuted grid: contiguous columns
+        NFFT_CHECK(spread_layout(g, n, win, in, batch, 0, f, H, Bp, st, 2 * C, 1));
+        NFFT_CHECK(ch.col(H, Y, 1));
+        NFFT_CHECK(ch.fwd_out(Y, out, sub, dtab));
+      } else {
+        NFFT_CHECK(spread_layout(g, n, win, in, batch, 0, f, H, Bp, st));
+        NFFT_CHECK(ch.col(H, H));
+        NFFT_CHECK(ch.fwd_out(H, out, sub, dtab));
+      }
+    } else {
+      NFFT_CHECK(ch.fwd_in(in, Y, dtab));
+      NFFT_CHECK(ch.row_grid(Y, H));
+      const NodeFactor f{nullptr, (double)(P / 2), +1};
+      NFFT_CHECK(gather_layout(g, n, win, H, Bp, batch, f, sub, 0, sub ? 1 : 0, out, 0, st));
+    }
+    return NFFT45_OK;
+  };
+  status = run();
+  cudaFreeAsync(base, st);
+  return status;
+}
+
+bool forward_bm_usable(int64_t Q, int64_t P, int m, int64_t batch) {
+  static const bool off = getenv("NFFT45_NO_FORWARD_BM") != nullptr;  // A/B switch: generic batched forward path
+  int r = 0, c = 0;
+  return !off && m == kFastM && Q == P && batch >= 16 && chain_bm_hybrid_factors(P, &r, &c) &&
+         2 * P * ((batch + kSig - 1) / kSig * kSig) < (int64_t(1) << 31);  // 32-bit in-tile offsets of kbm_col
+}
+
+int forward_run_bm(const GridDev& g, int kind, const double2* in, int64_t batch, const double2* sub, double2* out,
+                   cudaStream_t st) {
+  switch (g.Q) {
+    case 1024: return forward_solve_bm<32, 32>(g, kind, in, batch, sub, out, st);
+    case 2048: return forward_solve_bm<64, 32>(g, kind, in, batch, sub, out, st);
+    case 4096: return forward_solve_bm<64, 64>(g, kind, in, batch, sub, out, st);
+    case 8192: return forward_solve_bm<128, 64>(g, kind, in, batch, sub, out, st);
+    case 16384: return forward_solve_bm<128, 128>(g, kind, in, batch, sub, out, st);
+    case 32768: return forward_solve_bm<256, 128>(g, kind, in, batch, sub, out, st);
+    case 65536: return forward_solve_bm<256, 256>(g, kind, in, batch, sub, out, st);
+    case 131072: return forward_solve_bm<512, 256>(g, kind, in, batch, sub, out, st);
+  }
+  return NFFT45_ERR_INVALID_ARGUMENT;
 }
 
 bool chain_bm_hybrid_factors(int64_t P, int* R, int* C) {

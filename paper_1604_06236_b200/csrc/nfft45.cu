@@ -343,6 +343,8 @@ static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 // nfft_type1, nonuniform_conv, compute_v_samples and the type-4 refinement.
 static int type1_core(const GridDev& g, const double2* a, int64_t batch, int64_t R, int m, int64_t P,
                       const double2* tab, const double2* sub, double2* out, cudaStream_t st) {
+  if (a && !tab && R == P && forward_bm_usable(g.Q, R, m, batch))  // batched: batch-minor passes
+    return forward_run_bm(g, 1, a, batch, sub, out, st);
   const int64_t n = 2 * R;
   const int64_t K = R / 2;
   Window win = Window::make(m);
@@ -358,6 +360,7 @@ static int type1_core(const GridDev& g, const double2* a, int64_t batch, int64_t
 // s = type2(S, grid) (forward.py:67-102), optional subtraction.
 static int type2_core(const GridDev& g, const double2* Sc, int64_t batch, int64_t P, int m, const double2* sub,
                       double2* out, cudaStream_t st) {
+  if (forward_bm_usable(g.Q, P, m, batch)) return forward_run_bm(g, 2, Sc, batch, sub, out, st);  // batched
   const int64_t n = 2 * P;
   const int64_t K = P / 2;
   Window win = Window::make(m);

@@ -152,6 +152,11 @@ int spread_small(const GridDev& g, int64_t n, const Window& win, const double2* 
 int gather_small(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t batch, NodeFactor f,
                  const double2* sub, int mode, double2* out, cudaStream_t st);
 int norms_bm(const double2* r, int64_t len, int64_t batch, int64_t ld, double* norms, cudaStream_t st);
+// Batched forward NFFTs (R = P = Q a hybrid chain size, m = 14, batch >= 16) on the batch-minor
+// passes (chain_bm.cu): kind 1 = nfft_type1, kind 2 = nfft_type2, optional signal-major subtrahend.
+bool forward_bm_usable(int64_t Q, int64_t P, int m, int64_t batch);
+int forward_run_bm(const GridDev& g, int kind, const double2* in, int64_t batch, const double2* sub, double2* out,
+                   cudaStream_t st);
 int chain_run_bm(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes, double2* out,
                  double* norms, cudaStream_t st);
 

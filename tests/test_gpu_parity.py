@@ -605,6 +605,72 @@ def test_kernel_variants_bitwise(tmp_path):
             assert np.array_equal(outs[0][k], o[k]), (extra, k)
 
 
+# ------------------------------------- batched forward transforms on the batch-minor passes
+
+@pytest.mark.parametrize("P,B,J", [(1024, 16, 0.3), (2048, 19, 0.45), (4096, 64, 0.3), (1 << 15, 18, 0.3),
+                                   (1 << 16, 17, 0.3), (1 << 17, 16, 0.4)])
+def test_batched_forward_fast_path(P, B, J):
+    """nfft_type1 / nfft_type2 on batches of 16 or more signals (R = P = Q a power of two in
+    2^10 ... 2^17) run on the batch-minor FFT passes with one 2-D boundary kernel per direction
+    (chain_bm.cu: kbm_fwd_in / kbm_fwd_out).  Every row must match the oracle's fast transform
+    (forward.py:26-102 restated) to 1e-13 and the per-signal path of the library (single signals
+    take the signal-major kernels: a different FFT schedule, so roundoff-level differences) to
+    1e-13; ragged batches exercise the padded signal groups."""
+    t, data = O.make_inputs(P, J, B, 16050 + B)
+    g = nf.validate_grid(t)
+    got1 = nf.nfft_type1(g, data, P)
+    got2 = nf.nfft_type2(data, g)
+    assert got1.shape == (B, P) and got2.shape == (B, P)
+    for r in sorted({0, 7, B - 2, B - 1}):
+        assert rel(O.type1(t, data[r], P), got1[r]) <= 1e-13
+        assert rel(O.type2(data[r], t), got2[r]) <= 1e-13
+        assert rel(nf.nfft_type1(g, data[r], P), got1[r]) <= 1e-13
+        assert rel(nf.nfft_type2(data[r], g), got2[r]) <= 1e-13
+    if P <= 2048:  # exact direct sums (forward.py:105-130)
+        assert rel(O.type1_exact(t, data[B - 1], P), got1[B - 1]) <= 1e-12
+        assert rel(O.type2_exact(data[B - 1], t), got2[B - 1]) <= 1e-12
+
+
+_FWD_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[2])
+import paper_1604_06236_b200 as nf
+rng = np.random.default_rng(5)
+P, B = 4096, 24
+t = np.mod((np.arange(P) + rng.uniform(-0.3, 0.3, P)) / P, 1.0)
+g = nf.validate_grid(t)
+x = (rng.standard_normal((B, P)) + 1j * rng.standard_normal((B, P))) / np.sqrt(2)
+plan = nf.build_plan(g, nf.MethodParams.from_mu(1e-15, P, 2))
+np.savez(sys.argv[1], t1=nf.nfft_type1(g, x, P), t2=nf.nfft_type2(x, g),
+         r5=nf.refine_type5(plan, x, passes=2), r4=nf.refine_type4(plan, x, passes=2))
+"""
+
+
+def test_batched_forward_fast_path_vs_generic(tmp_path):
+    """The batch-minor forward path against the generic batched path (NFFT45_NO_FORWARD_BM=1:
+    signal-major spread / four-step FFT / band kernels), and inside the UNFUSED refinement
+    (NFFT45_NO_CHAIN=1: solve, forward transform with the subtrahend fused, solve), whose forward
+    transforms take the fast path with a subtrahend: roundoff-level agreement."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for i, extra in enumerate(({}, {"NFFT45_NO_FORWARD_BM": "1"}, {"NFFT45_NO_CHAIN": "1"},
+                               {"NFFT45_NO_CHAIN": "1", "NFFT45_NO_FORWARD_BM": "1"})):
+        f = tmp_path / f"f{i}.npz"
+        subprocess.run([sys.executable, "-c", _FWD_SCRIPT, str(f), root], check=True, env=dict(os.environ, **extra),
+                       timeout=300)
+        outs.append(np.load(f))
+    for k in ("t1", "t2"):
+        assert rel(outs[1][k], outs[0][k]) <= 1e-13
+        assert not np.array_equal(outs[1][k], outs[0][k])  # the switch really selects another path
+    for k in ("r5", "r4"):
+        assert rel(outs[0][k], outs[2][k]) <= 1e-11 and rel(outs[3][k], outs[2][k]) <= 1e-11
+
+
 # ------------------------------------- fused multi-pass type-4 refinement
 
 @pytest.mark.parametrize("B", [1, 20])
