@@ -1701,12 +1701,21 @@ static int forward_solve_bm(const GridDev& g, int kind, const double2* in, int64
 bool forward_bm_usable(int64_t Q, int64_t P, int m, int64_t batch) {
   static const bool off = getenv("NFFT45_NO_FORWARD_BM") != nullptr;  // A/B switch: generic batched forward path
   int r = 0, c = 0;
-  return !off && m == kFastM && Q == P && batch >= 16 && chain_bm_hybrid_factors(P, &r, &c) &&
-         2 * P * ((batch + kSig - 1) / kSig * kSig) < (int64_t(1) << 31);  // 32-bit in-tile offsets of kbm_col
+  return !off && m == kFastM && Q == P && batch >= 16 && chain_bm_hybrid_factors(P, &r, &c);
 }
 
 int forward_run_bm(const GridDev& g, int kind, const double2* in, int64_t batch, const double2* sub, double2* out,
                    cudaStream_t st) {
+  // kbm_col addresses a tile's rows with 32-bit offsets (n * Bp < 2^31): large batches run in
+  // independent slices of rows, like chain_run_bm
+  const int64_t max_rows = ((int64_t(1) << 31) / (2 * g.Q)) / kSig * kSig;
+  if (batch > max_rows && max_rows >= 16) {
+    for (int64_t b0 = 0; b0 < batch; b0 += max_rows) {
+      const int64_t nb = std::min(max_rows, batch - b0);
+      NFFT_CHECK(forward_run_bm(g, kind, in + b0 * g.Q, nb, sub ? sub + b0 * g.Q : nullptr, out + b0 * g.Q, st));
+    }
+    return NFFT45_OK;
+  }
   switch (g.Q) {
     case 1024: return forward_solve_bm<32, 32>(g, kind, in, batch, sub, out, st);
     case 2048: return forward_solve_bm<64, 32>(g, kind, in, batch, sub, out, st);

@@ -1138,7 +1138,7 @@ int nfft45_plan_create_terms(const nfft45_grid* g, double a, int64_t R, int m, v
     // one stream synchronize (check_guards), published after it
     GridCachePending* pend = nullptr;
     if (!status && m == kFastM) {
-      int tcs[3] = {64, getenv("NFFT45_STILE") ? atoi(getenv("NFFT45_STILE")) : 128, 32};  // 32: warp tiles
+      int tcs[3] = {64, getenv("NFFT45_STILE") && atoi(getenv("NFFT45_STILE")) == 256 ? 256 : 128, 32};  // 32: warp tiles
       status = grid_caches_begin(g->d, 2 * P, m, tcs, 2 * P <= (int64_t(1) << 17) ? 3 : 2, s, &pend);
     }
     if (!status) status = check_guards(guard.d(), 1, 1, s);
