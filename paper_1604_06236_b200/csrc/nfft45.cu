@@ -974,6 +974,12 @@ int nfft45_type2_direct(const nfft45_grid* g, const double* Sc, int64_t batch, i
 
 int nfft45_dft(const double* in, double* out, int64_t batch, int64_t N, int sign, void* st) {
   if (N < 1) return fail(NFFT45_ERR_INVALID_ARGUMENT, "DFT length must be >= 1");
+  // current device: the guard's first use keeps freed scratch in the stream-ordered pool (a process
+  // that only calls the DFT entry points would otherwise re-map its scratch on every call)
+  int dev = 0;
+  NFFT_CUDA(cudaGetDevice(&dev));
+  DeviceGuard dg(dev);
+  if (dg.status) return dg.status;
   return by_rows(batch, [&](int64_t b0, int64_t nb) {
     return fft_run(C2(in) + b0 * N, D2(out) + b0 * N, nb, N, sign, nullptr, nullptr, S(st));
   });

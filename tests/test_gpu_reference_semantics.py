@@ -437,6 +437,23 @@ def test_concurrent_plan_builds_share_one_node_set():
     assert np.array_equal(got, nf.refine_type5(ref_plan, batch, passes=1))
 
 
+@pytest.mark.parametrize("lgN,B", [(11, 16), (12, 19), (13, 16), (14, 17), (15, 16), (16, 24), (17, 16), (18, 17)])
+def test_batched_dft(lgN, B):
+    """dft / idft of batches of rows of length 2^11 ... 2^18 (the four-step Stockham passes of
+    fft.cu, forward.py:21-23): numpy's FFT to roundoff, every row equal to the single-row call,
+    ragged batches."""
+    rng = np.random.default_rng(lgN)
+    N = 1 << lgN
+    x = rng.standard_normal((B, N)) + 1j * rng.standard_normal((B, N))
+    X = nf.dft(x)
+    assert X.shape == (B, N)
+    assert rel(np.fft.fft(x, axis=-1), X) < 1e-14
+    assert rel(np.fft.ifft(x, axis=-1), nf.idft(x)) < 1e-14
+    for r in (0, B - 1):
+        assert rel(nf.dft(x[r]), X[r]) < 1e-14
+    assert rel(x, nf.idft(X)) < 1e-14
+
+
 def test_flop_reports_match_reference(golden):
     def rep(fc):
         r = fc.report()
