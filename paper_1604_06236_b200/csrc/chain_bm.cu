@@ -416,8 +416,10 @@ __host__ __device__ constexpr bool bm_mid_fused() {
   return bm_hyb<R, C>() && FastTraits<R>::rem == 0 && FastTraits<R>::np == 2;
 }
 
-template <int R, int C>
-__global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<R, kSig>())) kbm_mid_hf(
+// TST: the last pass leaves dense rows [k][8] in the tile's shared memory and
+// one thread stores them with the TMA unit (see kbm_pad_hs)
+template <int R, int C, bool TST>
+__device__ __forceinline__ void mid_hf_body(double2* sm, const CUtensorMap* tmZ,
     const double2* __restrict__ U, double2* __restrict__ Z, int64_t Bp, const double2* __restrict__ tw,
     const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
     const double2* __restrict__ ks) {
@@ -425,7 +427,6 @@ __global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<
   using Tr = FastTraits<R>;
   static_assert(Tr::np == 2 && Tr::rem == 0, "fused handoff: schedule 16 x 16");
   constexpr int LPS = R / 16;  // lanes per signal = stride of the radix-16 passes
-  extern __shared__ double2 sm[];
   double2* s_ks = sm + R * kSig;
   const int r = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * kSig;
@@ -461,9 +462,39 @@ __global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<
     for (int q = 0; q < 16; q++) sm[((d + q) << 3) + (hd ^ hsw8(q))] = v[q];
   }
   __syncthreads();  // the last pass is column-fast
-  auto st2 = [&](int k, int c, double2 v) { Zt[(unsigned)(k * C) * ub + c] = v; };
   const FourStepTw<-1> pt{loP, hiP, sP, twQ, Q, r, 0};
-  hyb_tile_fft_from<R, -1, Tr, 0x0u, 1, 16>(sm, st2, tw, pt);
+  if constexpr (TST) {
+    static_assert(R <= 256, "one TMA box");
+    auto st2 = [&](int k, int c, double2 v) { sm[(k << 3) + c] = v; };
+    hyb_tile_fft_from<R, -1, Tr, 0x0u, 1, 16, decltype(st2), FourStepTw<-1>, CtaSync, true>(sm, st2, tw, pt);
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tma_store_3d(tmZ, (int)(2 * b0), r, 0, sm);
+      tma_store_commit();
+      tma_store_wait_read();
+    }
+  } else {
+    auto st2 = [&](int k, int c, double2 v) { Zt[(unsigned)(k * C) * ub + c] = v; };
+    hyb_tile_fft_from<R, -1, Tr, 0x0u, 1, 16>(sm, st2, tw, pt);
+  }
+}
+
+template <int R, int C>
+__global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<R, kSig>())) kbm_mid_hf(
+    const double2* __restrict__ U, double2* __restrict__ Z, int64_t Bp, const double2* __restrict__ tw,
+    const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
+    const double2* __restrict__ ks) {
+  extern __shared__ double2 sm[];
+  mid_hf_body<R, C, false>(sm, nullptr, U, Z, Bp, tw, loP, hiP, sP, twQ, Q, ks);
+}
+template <int R, int C>
+__global__ void __launch_bounds__(fast_threads<R, kSig>(), bm_minb(fast_threads<R, kSig>())) kbm_mid_hs(
+    const __grid_constant__ CUtensorMap tmZ, const double2* __restrict__ U, double2* __restrict__ Z, int64_t Bp,
+    const double2* __restrict__ tw, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
+    const double2* __restrict__ twQ, int Q, const double2* __restrict__ ks) {
+  extern __shared__ __align__(128) double2 sm_hs[];
+  mid_hf_body<R, C, true>(sm_hs, &tmZ, U, Z, Bp, tw, loP, hiP, sP, twQ, Q, ks);
 }
 
 // kbm_band_h with the band handoff in registers: after the last (radix-16)
@@ -475,8 +506,8 @@ __host__ __device__ constexpr bool bm_band_fused() {
   return bm_hyb<R, C>() && C == 256;  // FFT_512 = 2 x 16 x 16, IFFT_256 = 4 x 8 x 8
 }
 
-template <int R, int C>
-__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_band_hf(
+template <int R, int C, bool TST>
+__device__ __forceinline__ void band_hf_body(double2* sm, const CUtensorMap* tmU,
     const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
@@ -487,7 +518,6 @@ __global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_thre
   using TrA = FastTraits<NR>;
   using TrB = HalfTr<C>;
   static_assert(NR == 512 && TrA::np == 3 && TrB::np == 3 && TrB::radix(0) == 4, "fused band handoff: 512 / 256");
-  extern __shared__ double2 sm[];
   double* s_t0 = reinterpret_cast<double*>(sm + NR * SG);
   double* s_t1 = s_t0 + C;
   double2* s_sb = reinterpret_cast<double2*>(s_t1 + C);
@@ -557,9 +587,41 @@ __global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_thre
     }
   }
   __syncwarp();  // pass 1 of the IFFT is warp-local
-  auto st2 = [&](int k1p, int c, double2 v) { Ut[(unsigned)(k1p * R) * ub + c] = v; };
   const FourStepTw<+1> pt{loP, hiP, sP, twQ, Q, k1, 0};
-  hyb_tile_fft_from<C, +1, TrB, 0x2u, 1, 4>(sm, st2, twC, pt);  // pass 1 warp-local, pass 2 column-fast
+  if constexpr (TST) {  // dense rows [k1'][8] in the first half of the tile buffer, stored by the TMA unit
+    auto st2 = [&](int k1p, int c, double2 v) { sm[(k1p << 3) + c] = v; };
+    hyb_tile_fft_from<C, +1, TrB, 0x2u, 1, 4, decltype(st2), FourStepTw<+1>, CtaSync, true>(sm, st2, twC, pt);
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tma_store_3d(tmU, (int)(2 * b0), k1, 0, sm);
+      tma_store_commit();
+      tma_store_wait_read();
+    }
+  } else {
+    auto st2 = [&](int k1p, int c, double2 v) { Ut[(unsigned)(k1p * R) * ub + c] = v; };
+    hyb_tile_fft_from<C, +1, TrB, 0x2u, 1, 4>(sm, st2, twC, pt);  // pass 1 warp-local, pass 2 column-fast
+  }
+}
+
+template <int R, int C>
+__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_band_hf(
+    const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp, const double2* __restrict__ twR,
+    const double2* __restrict__ twC, const double2* __restrict__ loP, const double2* __restrict__ hiP, int sP,
+    const double2* __restrict__ twQ, int Q, const double* __restrict__ deconv, const double* __restrict__ decay,
+    const double* __restrict__ dd, const double2* __restrict__ sub, double2* __restrict__ rsave) {
+  extern __shared__ double2 sm[];
+  band_hf_body<R, C, false>(sm, nullptr, T, U, Bp, twR, twC, loP, hiP, sP, twQ, Q, deconv, decay, dd, sub, rsave);
+}
+template <int R, int C>
+__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_band_hs(
+    const __grid_constant__ CUtensorMap tmU, const double2* __restrict__ T, double2* __restrict__ U, int64_t Bp,
+    const double2* __restrict__ twR, const double2* __restrict__ twC, const double2* __restrict__ loP,
+    const double2* __restrict__ hiP, int sP, const double2* __restrict__ twQ, int Q,
+    const double* __restrict__ deconv, const double* __restrict__ decay, const double* __restrict__ dd,
+    const double2* __restrict__ sub, double2* __restrict__ rsave) {
+  extern __shared__ __align__(128) double2 sm_hs[];
+  band_hf_body<R, C, true>(sm_hs, &tmU, T, U, Bp, twR, twC, loP, hiP, sP, twQ, Q, deconv, decay, dd, sub, rsave);
 }
 
 // kbm_pad_h (no x output) with the zero-padding handoff done by ONE warp
@@ -595,7 +657,7 @@ struct PadHfArgs {
 // one tile (row r, signals b0 ..) of the fused pad; `ld1` reads the tile's Z
 // rows (global memory, or a TMA-staged dense copy), `sy` is the CTA or one
 // tile group of a persistent CTA
-template <int R, int C, class Ld, class Hk, class Sy>
+template <int R, int C, bool TST = false, class Ld, class Hk, class Sy>
 __device__ __forceinline__ void pad_hf_tile(const PadHfArgs& a, double2* sm, double* s_t0, const Ld& ld1,
                                             const Hk& hook, int r, int64_t b0, const Sy& sy) {
   constexpr int NC = 2 * C;
@@ -649,9 +711,14 @@ __device__ __forceinline__ void pad_hf_tile(const PadHfArgs& a, double2* sm, dou
     for (int q = 0; q < 16; q++) sm[((d + 2 * q) << 3) + (hd ^ hsw8(2 * q))] = in[q];
   }
   sy.sync();  // the last pass is column-fast
-  auto st2 = [&](int k, int c, double2 v) { Yt[(unsigned)(k * R) * ub + c] = v; };
   const FourStepTw<+1> pt{a.loN, a.hiN, a.sN, a.twQ, a.Q, r, 0};
-  hyb_tile_fft_from<NC, +1, TrB, 0x0u, 2, 32>(sm, st2, a.twC, pt, sy);
+  if constexpr (TST) {  // dense rows [k][8] in place; the caller stores them with the TMA unit
+    auto st2 = [&](int k, int c, double2 v) { sm[(k << 3) + c] = v; };
+    hyb_tile_fft_from<NC, +1, TrB, 0x0u, 2, 32, decltype(st2), FourStepTw<+1>, Sy, true>(sm, st2, a.twC, pt, sy);
+  } else {
+    auto st2 = [&](int k, int c, double2 v) { Yt[(unsigned)(k * R) * ub + c] = v; };
+    hyb_tile_fft_from<NC, +1, TrB, 0x0u, 2, 32>(sm, st2, a.twC, pt, sy);
+  }
 }
 
 template <int R, int C>
@@ -669,6 +736,38 @@ __global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_thre
   cpa_commit();
   auto ld1 = [&](int i, int c) -> double2 { return Zt[(unsigned)i * ub + c]; };
   pad_hf_tile<R, C>(a, sm, s_t0, ld1, CpAsyncWaitHook(), r, b0, CtaSync());
+}
+
+// kbm_pad_hf whose output leaves through the TMA unit: the last pass writes
+// its rows back into the tile's shared memory (dense [k][8], in place — see
+// ROWST in fft_fast.cuh), then one thread issues two bulk tensor stores (SASS
+// UTMASTG) of 256 rows each to rows k R + r of Y.  The 2 units of output of
+// the zero-padded first IFFT_2P pass cost STS wavefronts instead of STG ones
+// (about half the L1 data-pipe cycles per byte).
+template <int R, int C>
+__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_pad_hs(
+    const double2* __restrict__ Z, const __grid_constant__ CUtensorMap tmY, const __grid_constant__ PadHfArgs a) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
+  constexpr int NC = 2 * C;
+  extern __shared__ __align__(128) double2 sm_hs[];
+  double2* sm = sm_hs;
+  double* s_t0 = reinterpret_cast<double*>(sm + NC * kSig);
+  const int r = blockIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * kSig;
+  const unsigned ub = (unsigned)a.Bp;
+  const double2* __restrict__ Zt = Z + (int64_t)r * C * a.Bp + b0;
+  for (int i = threadIdx.x; i < C / 2; i += blockDim.x) cpa16(&s_t0[2 * i], &a.cd[(int64_t)r * C + 2 * i]);  // tile-major
+  cpa_commit();
+  auto ld1 = [&](int i, int c) -> double2 { return Zt[(unsigned)i * ub + c]; };
+  pad_hf_tile<R, C, true>(a, sm, s_t0, ld1, CpAsyncWaitHook(), r, b0, CtaSync());
+  fence_proxy_async();  // this thread's rows become visible to the async proxy
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k0 = 0; k0 < NC; k0 += 256) tma_store_3d(&tmY, (int)(2 * b0), r, k0, sm + k0 * kSig);
+    tma_store_commit();
+    tma_store_wait_read();
+  }
 }
 
 // Persistent form of kbm_pad_hf: ONE CTA per SM made of two tile groups of
@@ -1159,6 +1258,8 @@ template __global__ void kbm_band_hf<NFFT45_EXP_RC>(const double2*, double2*, in
 template __global__ void kbm_mid_hf<NFFT45_EXP_RC>(const double2*, double2*, int64_t, const double2*, const double2*, const double2*,
                                               int, const double2*, int, const double2*);
 template __global__ void kbm_pad_hf<NFFT45_EXP_RC>(const double2*, const __grid_constant__ PadHfArgs);
+template __global__ void kbm_pad_hs<NFFT45_EXP_RC>(const double2*, const __grid_constant__ CUtensorMap,
+                                              const __grid_constant__ PadHfArgs);
 template __global__ void kbm_pad_hp<NFFT45_EXP_RC>(const __grid_constant__ CUtensorMap, const __grid_constant__ PadHfArgs);
 template __global__ void kbm_pad_h<NFFT45_EXP_RC, false>(const double2*, double2*, int64_t, const double2*, const double2*,
                                                     const double2*, const double2*, int, const double2*, int,
@@ -1169,22 +1270,43 @@ template __global__ void kbm_pad_h<NFFT45_EXP_RC, true>(const double2*, double2*
 #else
 // ------------------------------------------------------------ host side
 
-int tma_map_rows(CUtensorMap* map, const void* base, int64_t rows, int64_t Bp, int box_rows, int box_sig) {
-  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static Encode encode = [] {
+using TmaEncode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TmaEncode tma_encoder() {
+  static TmaEncode encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
         q != cudaDriverEntryPointSuccess)
       fn = nullptr;
-    return reinterpret_cast<Encode>(fn);
+    return reinterpret_cast<TmaEncode>(fn);
   }();
-  if (!encode) {
-    set_error(NFFT45_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (!encode) set_error(NFFT45_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return encode;
+}
+
+int tma_map_strided(CUtensorMap* map, const void* base, int64_t outer_n, int64_t inner_n, int64_t Bp, int box_outer,
+                    int box_sig) {
+  TmaEncode encode = tma_encoder();
+  if (!encode) return NFFT45_ERR_CUDA;
+  const cuuint64_t gdim[3] = {(cuuint64_t)(2 * Bp), (cuuint64_t)inner_n, (cuuint64_t)outer_n};
+  const cuuint64_t gstride[2] = {(cuuint64_t)(Bp * sizeof(double2)), (cuuint64_t)(inner_n * Bp * sizeof(double2))};
+  const cuuint32_t box[3] = {(cuuint32_t)(2 * box_sig), 1u, (cuuint32_t)box_outer};
+  const cuuint32_t estride[3] = {1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), gdim, gstride, box, estride,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error(NFFT45_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed (" + std::to_string((int)r) + ")");
     return NFFT45_ERR_CUDA;
   }
+  return NFFT45_OK;
+}
+
+int tma_map_rows(CUtensorMap* map, const void* base, int64_t rows, int64_t Bp, int box_rows, int box_sig) {
+  TmaEncode encode = tma_encoder();
+  if (!encode) return NFFT45_ERR_CUDA;
   const cuuint64_t gdim[2] = {(cuuint64_t)(2 * Bp), (cuuint64_t)rows};
   const cuuint64_t gstride[1] = {(cuuint64_t)(Bp * sizeof(double2))};
   const cuuint32_t box[2] = {(cuuint32_t)(2 * box_sig), (cuuint32_t)box_rows};
@@ -1223,6 +1345,12 @@ struct ChainBM {
   int pf = 0;                // L2 prefetch distance in launch slots (0: off)
   bool hyb = false;          // hybrid two-FFT kernels (warp-local middle passes), when bm_hyb<R, C>()
   bool fuse = true;          // register handoff between the two transforms of band / mid (NFFT45_FUSE=0: off)
+  // outputs of the fused hybrid kernels through bulk tensor stores: 1 (default) pad and mid, 2 also
+  // band, 0 off (NFFT45_TMAST; A/B and the variant test)
+  static int tma_st() {
+    static const int on = getenv("NFFT45_TMAST") ? atoi(getenv("NFFT45_TMAST")) : 1;
+    return on;
+  }
   // grid of (tiles x groups*mult); with sw the signal groups run fastest
   dim3 gdim(int tiles, int mult = 1) const {
     return sw ? dim3(groups * mult, (unsigned)tiles) : dim3((unsigned)tiles, groups * mult);
@@ -1274,6 +1402,17 @@ struct ChainBM {
       const int64_t Q = P / last_stride<C, HalfTr<C>>();
       const double2* twQ = nullptr;
       NFFT_CHECK(qtab(Q, &twQ));
+      if constexpr (bm_band_fused<R, C>()) {
+        if (fuse && tma_st() >= 2) {  // output through a bulk tensor store (measured neutral: opt-in)
+          auto bm_band = kbm_band_hs<R, C>;
+          NFFT_CHECK(bm_attr(bm_band, smem));
+          CUtensorMap tm;
+          NFFT_CHECK(tma_map_strided(&tm, U, C, R, Bp, C, kSig));
+          LAUNCH_PDL(bm_band, dim3(groups, (unsigned)R), T, smem, st, tm, T_, U, Bp, t.tw2C, t.twC, t.tP->lo, t.tP->hi,
+                     t.tP->s, twQ, (int)Q, pv.tdeconv, pv.tdecay, pv.tdd, sub, rsave);
+          return NFFT45_OK;
+        }
+      }
       LAUNCH_PDL(bm_band, dim3(groups, (unsigned)R), T, smem, st, T_, U, Bp, t.tw2C, t.twC, t.tP->lo, t.tP->hi, t.tP->s,
                  twQ, (int)Q, pv.tdeconv, pv.tdecay, pv.tdd, sub, rsave);
     }
@@ -1296,6 +1435,17 @@ struct ChainBM {
       const int64_t Q = P / last_stride<R>();
       const double2* twQ = nullptr;
       NFFT_CHECK(qtab(Q, &twQ));
+      if constexpr (bm_mid_fused<R, C>() && R <= 256) {
+        if (fuse && tma_st()) {
+          auto bm_mid = kbm_mid_hs<R, C>;
+          NFFT_CHECK(bm_attr(bm_mid, smem));
+          CUtensorMap tm;
+          NFFT_CHECK(tma_map_strided(&tm, Z, R, C, Bp, R, kSig));
+          LAUNCH_PDL(bm_mid, dim3(groups, (unsigned)C), T, smem, st, tm, U, Z, Bp, t.twR, t.tP->lo, t.tP->hi, t.tP->s,
+                     twQ, (int)Q, pv.tks);
+          return NFFT45_OK;
+        }
+      }
       LAUNCH_PDL(bm_mid, dim3(groups, (unsigned)C), T, smem, st, U, Z, Bp, t.twR, t.tP->lo, t.tP->hi, t.tP->s, twQ, (int)Q,
                  pv.tks);
     }
@@ -1383,8 +1533,16 @@ struct ChainBM {
           LAUNCH_PDL(bm_pad, std::min(sms, (ntiles + 1) / 2), 2 * T, smem, st, tm, args);
           return NFFT45_OK;
         }
-        auto bm_pad = kbm_pad_hf<R, C>;
         const size_t smem = sizeof(double2) * 2 * C * kSig + 2 * sizeof(double) * C;
+        if (tma_st()) {  // output through bulk tensor stores
+          auto bm_pad = kbm_pad_hs<R, C>;
+          NFFT_CHECK(bm_attr(bm_pad, smem));
+          CUtensorMap tm;
+          NFFT_CHECK(tma_map_strided(&tm, Y, 2 * C, R, Bp, 256, kSig));
+          LAUNCH_PDL(bm_pad, dim3(groups, (unsigned)R), T, smem, st, Z, tm, args);
+          return NFFT45_OK;
+        }
+        auto bm_pad = kbm_pad_hf<R, C>;
         NFFT_CHECK(bm_attr(bm_pad, smem));
         LAUNCH_PDL(bm_pad, dim3(groups, (unsigned)R), T, smem, st, Z, args);
         return NFFT45_OK;

@@ -406,8 +406,14 @@ __host__ __device__ constexpr bool hyb_ok() {
 // Passes P.. of the hybrid schedule.  WLMASK bit p: pass p is warp-local.
 // SRC_SMEM: the first pass's `ld` reads this tile's shared memory (in-place
 // hazard); DST_SMEM: the last pass's `st` writes shared memory.
+//
+// ROWST: the last pass's `st` writes row d (all 8 signals) of THIS tile's
+// shared memory in some other slot order (the dense rows a TMA store reads).
+// The last pass of a Stockham schedule writes exactly the indices it read
+// (Ns = stride: d + r Ns = j + r stride), and the 8 threads of a row are
+// adjacent lanes of one warp, so the in-place hazard needs only __syncwarp.
 template <int N, int S, int P, int Ns, class Tr, unsigned WLMASK, bool SRC_SMEM, bool DST_SMEM, int P0, class Ld,
-          class St, class PT, class Hk, int PEND = Tr::np, class Sy = CtaSync>
+          class St, class PT, class Hk, int PEND = Tr::np, class Sy = CtaSync, bool ROWST = false>
 __device__ __forceinline__ void hyb_passes(double2* sm, const Ld& ld, const St& st, const double2* __restrict__ tw,
                                            const PT& pt, const Hk& hook, const Sy& sy = Sy()) {
   constexpr int C = 8;
@@ -438,6 +444,9 @@ __device__ __forceinline__ void hyb_passes(double2* sm, const Ld& ld, const St& 
   if constexpr ((!LD_FN || SRC_SMEM) && (!LAST || DST_SMEM)) {
     if constexpr (WL) __syncwarp();
     else sy.sync();
+  } else if constexpr (LAST && ROWST) {
+    static_assert(!WL && Ns * R == N, "row-local in-place store: column-fast last pass");
+    __syncwarp();
   }
 #pragma unroll
   for (int u = 0; u < MB; u++) {
@@ -473,7 +482,7 @@ __device__ __forceinline__ void hyb_passes(double2* sm, const Ld& ld, const St& 
     // PEND < np: the caller runs the remaining passes itself (fused handoff
     // to the next transform in registers); the boundary sync above is done
     if constexpr (P + 1 < PEND)
-      hyb_passes<N, S, P + 1, Ns * R, Tr, WLMASK, SRC_SMEM, DST_SMEM, P0, Ld, St, PT, NoHook, PEND, Sy>(
+      hyb_passes<N, S, P + 1, Ns * R, Tr, WLMASK, SRC_SMEM, DST_SMEM, P0, Ld, St, PT, NoHook, PEND, Sy, ROWST>(
           sm, ld, st, tw, pt, NoHook(), sy);
   }
 }
@@ -498,11 +507,12 @@ __device__ __forceinline__ void hyb_tile_fft(double2* sm, const Ld& ld, const St
 }
 // passes P0.. of a tile FFT whose earlier passes were produced directly in
 // shared memory (swizzled Stockham layout after pass P0 - 1, Ns = NS0)
-template <int N, int S, class Tr, unsigned WLMASK, int P0, int NS0, class St, class PT = NoPostTw, class Sy = CtaSync>
+template <int N, int S, class Tr, unsigned WLMASK, int P0, int NS0, class St, class PT = NoPostTw, class Sy = CtaSync,
+          bool ROWST = false>
 __device__ __forceinline__ void hyb_tile_fft_from(double2* sm, const St& st, const double2* __restrict__ tw,
                                                   const PT& pt = PT(), const Sy& sy = Sy()) {
   auto no_ld = [](int, int) -> double2 { return make_double2(0.0, 0.0); };
-  hyb_passes<N, S, P0, NS0, Tr, WLMASK, true, false, P0, decltype(no_ld), St, PT, NoHook, Tr::np, Sy>(
+  hyb_passes<N, S, P0, NS0, Tr, WLMASK, true, false, P0, decltype(no_ld), St, PT, NoHook, Tr::np, Sy, ROWST>(
       sm, no_ld, st, tw, pt, NoHook(), sy);
 }
 // warp-local mask: every pass but the first (when it reads global memory)

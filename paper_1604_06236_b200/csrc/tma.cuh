@@ -50,6 +50,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// 3-D tile store shared -> global (SASS UTMASTG): the box at element
+// coordinates (x, y, z) is read from dense shared memory by the TMA unit, no
+// LSU wavefronts and no registers; bulk-group completion.
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int x, int y, int z, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+// the committed stores have finished READING shared memory (the CTA may reuse it or exit)
+__device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -57,5 +70,11 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
 // Host: tensor map over a row-major [rows][Bp] complex128 array viewed as
 // doubles [rows][2 Bp], box = box_rows rows x box_sig signals.
 int tma_map_rows(CUtensorMap* map, const void* base, int64_t rows, int64_t Bp, int box_rows, int box_sig);
+// Host: tensor map over the same array viewed as [outer][inner][2 Bp] doubles
+// (row = outer * inner_n + inner), box = box_outer outer indices x 1 inner x
+// box_sig signals: the rows k * inner_n + r (k = k0 ... k0 + box_outer - 1) a
+// four-step tile owns.
+int tma_map_strided(CUtensorMap* map, const void* base, int64_t outer_n, int64_t inner_n, int64_t Bp, int box_outer,
+                    int box_sig);
 
 }  // namespace nfft45

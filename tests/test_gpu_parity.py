@@ -593,7 +593,10 @@ def test_kernel_variants_bitwise(tmp_path):
                 {"NFFT45_HYB": "0"}, {"NFFT45_FUSE": "0"}, {"NFFT45_GATHER_TMA": "0"}, {"NFFT45_PAD_PERSIST": "1"},
                 # natural-order fine grid (column pass in place) instead of the row-permuted one, and a
                 # blocked permutation
-                {"NFFT45_COL_PERM": "0"}, {"NFFT45_COL_BLK": "8"})
+                {"NFFT45_COL_PERM": "0"}, {"NFFT45_COL_BLK": "8"},
+                # outputs of the fused pad / mid kernels by per-thread global stores instead of bulk
+                # tensor stores (TMA), and the band kernel's output through the TMA unit as well
+                {"NFFT45_TMAST": "0"}, {"NFFT45_TMAST": "2"})
     outs = []
     for i, extra in enumerate(variants):
         f = tmp_path / f"v{i}.npz"
