@@ -771,20 +771,34 @@ constexpr int kGPSpanS = 96;  // short TMA box (rows)
 // SIG signals per group (16 or 32).  With SIG = 16 the two half-warps take
 // 4 nodes each of the warp's 8 (same cells, broadcast reads), which halves
 // the staging tile so 4 CTAs fit per SM.
-template <bool OUT_BM, int SUBM, int SIG>  // SUBM: 0 none, 1 batch-minor, 2 signal-major
-__global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 ? 4 : 5)) k_gather_p(
+// WARPS = 8 (with SIG = 32): 4 nodes per warp, lane = signal -- per staged
+// cell row a warp issues 3 LDS.128 (one 512-byte row of cells, two broadcast
+// weight pairs) for 8 DFMA pairs, against 3 LDS.128 per 4 DFMA pairs per
+// half-warp in the 16-signal layout, and the dense weight table of 4 nodes
+// has 83 % non-zero entries instead of 67 % for 8 nodes: the kernel is bound
+// by the L1's LSU data pipe, so both count.  8 warps per CTA keep 16-24 warps
+// per SM although the 32-signal cell tile is twice as large.
+template <int SIG, int WARPS>
+__host__ __device__ constexpr int gp_min_ctas(int subm, bool out_bm) {
+  if (WARPS == 8) return (subm == 2 || !out_bm) ? 2 : 3;
+  return SIG == 32 ? 2 : (SIG == 16 ? 4 : 5);
+}
+template <bool OUT_BM, int SUBM, int SIG, int WARPS = kGatherWarps>  // SUBM: 0 none, 1 batch-minor, 2 signal-major
+__global__ void __launch_bounds__(WARPS * 32, gp_min_ctas<SIG, WARPS>(SUBM, OUT_BM)) k_gather_p(
     const double* __restrict__ ts, const int* __restrict__ perm, int64_t Q, int64_t n, double alpha, GaussTab G,
     const double2* __restrict__ H, int64_t H_ld, int64_t batch, NodeFactor nf, const double2* __restrict__ sub,
     int64_t sub_ld, int mode, double2* __restrict__ out, int64_t out_ld, int ngroups, int* __restrict__ overflow, int sw,
     const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmHs, int tma) {
   pdl_enter();  // programmatic dependent launch: wait for the producer grid
-  constexpr int HALVES = 32 / SIG, NPL = kNPW / HALVES;
+  constexpr int NPW = kGatherNodes / WARPS;  // nodes per warp
+  constexpr int HALVES = 32 / SIG, NPL = NPW / HALVES;
   static_assert(kGatherNodes == 32, "one node per lane in the signal-major staging");
+  static_assert(NPL >= 2 && NPL % 2 == 0 && SIG % WARPS == 0, "weight pairs per lane; signals per warp in the transposes");
   extern __shared__ __align__(128) unsigned char smraw_gp[];  // own symbol: 128-byte aligned for the TMA box
   __shared__ __align__(8) uint64_t s_bar;  // TMA completion (transaction count) of the staged cell tile
   double2* Y = reinterpret_cast<double2*>(smraw_gp);                     // [kGPSpan][SIG]
   double* WT = reinterpret_cast<double*>(Y + kGPSpan * SIG);           // [warps][kWTSpan][8]
-  double2* Sb = reinterpret_cast<double2*>(WT + kGatherWarps * kWTSpan * kNPW);  // [nodes][SIG] (SUBM == 2)
+  double2* Sb = reinterpret_cast<double2*>(WT + WARPS * kWTSpan * NPW);  // [nodes][SIG] (SUBM == 2)
   double2* O = Sb + (SUBM == 2 ? kGatherNodes * SIG : 0);              // [nodes][SIG] (!OUT_BM)
   __shared__ int s_c0[kGatherNodes];
   __shared__ double s_f[kGatherNodes];
@@ -816,27 +830,27 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
   __syncthreads();
   const int cs = s_c0[0] - kM, ce = s_c0[kGatherNodes - 1] + kM;
   const int len = ce - cs + 1;
-  const int w_lo = s_c0[warp * kNPW] - kM, w_hi = s_c0[warp * kNPW + kNPW - 1] + kM;
+  const int w_lo = s_c0[warp * NPW] - kM, w_hi = s_c0[warp * NPW + NPW - 1] + kM;
   if (len > kGPSpan || w_hi - w_lo + 1 > kWTSpan || n < (int64_t)kGPSpan + 2 * kM + 2) {
     if (tid == 0 && by == 0) overflow[bx] = 1;  // handled by the fallback kernel
     return;
   }
   // per-warp dense weight table over the warp's cells, built once
-  double* wt = WT + warp * kWTSpan * kNPW;
+  double* wt = WT + warp * kWTSpan * NPW;
   const int wl = w_hi - w_lo + 1;
-  for (int i = lane; i < wl * kNPW; i += 32) wt[i] = 0.0;
+  for (int i = lane; i < wl * NPW; i += 32) wt[i] = 0.0;
   __syncwarp();
-  if (lane < kNPW && warp * kNPW + lane < nq) {
+  if (lane < NPW && warp * NPW + lane < nq) {
     double w[2 * kM + 1];
-    taps29(s_f[warp * kNPW + lane], alpha, G, w);
-    const int c0 = s_c0[warp * kNPW + lane] - kM - w_lo;
+    taps29(s_f[warp * NPW + lane], alpha, G, w);
+    const int c0 = s_c0[warp * NPW + lane] - kM - w_lo;
 #pragma unroll
-    for (int k = 0; k < 2 * kM + 1; k++) wt[(c0 + k) * kNPW + lane] = w[k];
+    for (int k = 0; k < 2 * kM + 1; k++) wt[(c0 + k) * NPW + lane] = w[k];
   }
   __syncwarp();
   const int ni = (int)n;
   // signal-major operands: this thread's node (lane) and first signal (warp)
-  const int64_t my_off = (int64_t)warp * Q + (lane < nq ? s_pq[lane] : 0);
+  const int64_t my_off = (int64_t)warp * Q + (lane < nq ? s_pq[lane] : 0);  // signals warp + WARPS k
   const double2* sb_src = sub + my_off;
   // Cell tile of a signal group: ONE bulk tensor copy (TMA, SASS UTMALDG)
   // issued by thread 0 when the block's cell span does not wrap around the
@@ -859,7 +873,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
     } else {
       const bool ok = b0 + sl < batch;
       const double2* col = H + b0 + (ok ? sl : 0);
-      for (int c = warp * HALVES + hf; c < len; c += kGatherWarps * HALVES) {
+      for (int c = warp * HALVES + hf; c < len; c += WARPS * HALVES) {
         int cell = cs + c;
         cell = cell < 0 ? cell + ni : (cell >= ni ? cell - ni : cell);
         cp_async16(&Y[c * SIG + sl], col + (int64_t)cell * H_ld, ok);
@@ -867,10 +881,10 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
     }
     if (SUBM == 2 && mode != 0) {  // node = lane, signals warp + 4k: one base pointer, stride 4Q
 #pragma unroll
-      for (int k = 0; k < SIG / kGatherWarps; k++) {
-        const int sig = warp + kGatherWarps * k;
+      for (int k = 0; k < SIG / WARPS; k++) {
+        const int sig = warp + WARPS * k;
         const bool okb = b0 + sig < batch && lane < nq;
-        cp_async16(&Sb[swz_nb<SIG>(sig, lane)], sb_src + (okb ? (b0 + kGatherWarps * k) * Q : 0), okb);
+        cp_async16(&Sb[swz_nb<SIG>(sig, lane)], sb_src + (okb ? (b0 + WARPS * k) * Q : 0), okb);
       }
     }
     cp_async_commit();
@@ -879,7 +893,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
   if (g < ngroups) stage(g);
   const double2* __restrict__ yw = Y + (w_lo - cs) * SIG + sl;
   const double2* __restrict__ wr0 = reinterpret_cast<const double2*>(wt) + hf * (NPL / 2);
-  const int e0 = warp * kNPW + hf * NPL;  // node of acc[0]
+  const int e0 = warp * NPW + hf * NPL;  // node of acc[0]
   unsigned phase = 0;
   for (; g < ngroups; g += gy) {
     const int64_t b0 = g * SIG;
@@ -906,7 +920,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
 #pragma unroll 4
     for (int i = 0; i < wl; i++) {
       const double2 y = yw[i * SIG];
-      const double2* wr = wr0 + i * (kNPW / 2);
+      const double2* wr = wr0 + i * (NPW / 2);
 #pragma unroll
       for (int i2 = 0; i2 < NPL / 2; i2++) {
         const double2 w = wr[i2];
@@ -951,9 +965,9 @@ __global__ void __launch_bounds__(kGatherWarps * 32, SIG == 32 ? 2 : (SIG == 16 
       __syncthreads();
       double2* dst = out + my_off + b0 * Q;
 #pragma unroll
-      for (int k = 0; k < SIG / kGatherWarps; k++) {
-        const int sig = warp + kGatherWarps * k;
-        if (b0 + sig < batch && lane < nq) dst[(int64_t)kGatherWarps * k * Q] = O[lane * SIG + swz(sig, lane)];
+      for (int k = 0; k < SIG / WARPS; k++) {
+        const int sig = warp + WARPS * k;
+        if (b0 + sig < batch && lane < nq) dst[(int64_t)WARPS * k * Q] = O[lane * SIG + swz(sig, lane)];
       }
     }
   }
@@ -990,6 +1004,12 @@ __global__ void k_overflow_clear(int* f, int64_t n) {
   if (i < n) f[i] = 0;
 }
 
+// 32-signal groups waste lanes on the last group of small batches: and their cell tiles leave fewer groups per walker: measured faster from 512 signals up (slower at 128 / 256)
+static bool gather_w8_default(int64_t nsig) {
+  static const int64_t min_sig = getenv("NFFT45_GATHER_W8_MIN") ? atoll(getenv("NFFT45_GATHER_W8_MIN")) : 512;
+  return nsig >= min_sig;
+}
+
 int gather_persistent(const GridDev& g, int64_t n, const Window& win, const double2* H, int64_t H_ld, int64_t batch,
                       NodeFactor f, const double2* sub, int64_t sub_ld, int mode, double2* out, int64_t out_ld,
                       cudaStream_t st) {
@@ -999,8 +1019,14 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
     const int v = e ? atoi(e) : 16;
     return v == 8 || v == 32 ? v : 16;
   }();
+  // 8 warps x 4 nodes with 32-signal groups (default); NFFT45_GATHER_WARPS=4: the 4-warp layouts
+  static const int env_w = getenv("NFFT45_GATHER_WARPS") ? atoi(getenv("NFFT45_GATHER_WARPS")) : 0;
+  static const bool sig_env = getenv("NFFT45_GATHER_SIG") != nullptr;
+  const bool w8 = env_w == 8 || (env_w == 0 && !sig_env && gather_w8_default(out_ld ? out_ld : batch));
+  const int SIGu = w8 ? 32 : SIG;
+  const int WARPSu = w8 ? 8 : kGatherWarps;
   const int64_t nblk = ceil_div(g.Q, kGatherNodes);
-  const int ngroups = (int)ceil_div(out_ld ? out_ld : batch, SIG);
+  const int ngroups = (int)ceil_div(out_ld ? out_ld : batch, SIGu);
   // at least 4 signal-group walkers per node block, walkers fastest in the
   // grid (concurrent CTAs then read 4 groups of each cell row: -4 % on C4)
   int slices = (int)std::min<int64_t>(ngroups, std::max<int64_t>(4, ceil_div(4 * 148, nblk)));
@@ -1017,8 +1043,8 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
     LAUNCH(k_overflow_clear, (unsigned)ceil_div(nblk, 256), 256, 0, st, overflow, nblk);
   }
   const int subm = mode == 0 ? 0 : (sub_ld ? 1 : 2);
-  size_t smem = (size_t)kGPSpan * SIG * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8 +
-                (subm == 2 ? (size_t)kGatherNodes * SIG * 16 : 0) + (out_ld ? 0 : (size_t)kGatherNodes * SIG * 16);
+  size_t smem = (size_t)kGPSpan * SIGu * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8 +
+                (subm == 2 ? (size_t)kGatherNodes * SIGu * 16 : 0) + (out_ld ? 0 : (size_t)kGatherNodes * SIGu * 16);
   const dim3 grid = sw ? dim3((unsigned)slices, (unsigned)nblk) : dim3((unsigned)nblk, (unsigned)slices);
   GaussTab G = gauss_tab(win);
   // TMA-staged cell tiles (NFFT45_GATHER_TMA=0: per-thread cp.async copies, for A/B runs)
@@ -1028,18 +1054,21 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
   int tma = use_tma && (reinterpret_cast<uintptr_t>(H) % 16 == 0) && n >= kGPSpan;
   CUtensorMap tmHs;
   memset(&tmHs, 0, sizeof(tmHs));
-  if (tma) NFFT_CHECK(tma_map_rows(&tmH, H, n, H_ld, kGPSpan, SIG));
-  if (tma) NFFT_CHECK(tma_map_rows(&tmHs, H, n, H_ld, kGPSpanS, SIG));
-#define NFFT_GP_LAUNCH(OBM, SM_, S_)                                                                           \
+  if (tma) NFFT_CHECK(tma_map_rows(&tmH, H, n, H_ld, kGPSpan, SIGu));
+  if (tma) NFFT_CHECK(tma_map_rows(&tmHs, H, n, H_ld, kGPSpanS, SIGu));
+#define NFFT_GP_LAUNCH(OBM, SM_, S_, W_)                                                                       \
   {                                                                                                          \
-    auto gather_p = k_gather_p<OBM, SM_, S_>;                                                                \
+    auto gather_p = k_gather_p<OBM, SM_, S_, W_>;                                                            \
     NFFT_CUDA(cudaFuncSetAttribute(gather_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
-    LAUNCH_PDL(gather_p, grid, kGatherWarps * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, H_ld, batch, f,  \
+    LAUNCH_PDL(gather_p, grid, W_ * 32, smem, st, g.ts, g.perm, g.Q, n, win.alpha, G, H, H_ld, batch, f,     \
            sub, sub_ld, mode, out, out_ld, ngroups, overflow, sw, tmH, tmHs, tma);                           \
   }
-#define NFFT_GP_SUB(OBM, S_) \
-  if (subm == 0) NFFT_GP_LAUNCH(OBM, 0, S_) else if (subm == 1) NFFT_GP_LAUNCH(OBM, 1, S_) else NFFT_GP_LAUNCH(OBM, 2, S_)
-  if (SIG == 16) {
+#define NFFT_GP_SUBW(OBM, S_, W_) \
+  if (subm == 0) NFFT_GP_LAUNCH(OBM, 0, S_, W_) else if (subm == 1) NFFT_GP_LAUNCH(OBM, 1, S_, W_) else NFFT_GP_LAUNCH(OBM, 2, S_, W_)
+#define NFFT_GP_SUB(OBM, S_) NFFT_GP_SUBW(OBM, S_, kGatherWarps)
+  if (WARPSu == 8) {
+    if (out_ld) NFFT_GP_SUBW(true, 32, 8) else NFFT_GP_SUBW(false, 32, 8)
+  } else if (SIG == 16) {
     if (out_ld) NFFT_GP_SUB(true, 16) else NFFT_GP_SUB(false, 16)
   } else if (SIG == 8) {
     if (out_ld) NFFT_GP_SUB(true, 8) else NFFT_GP_SUB(false, 8)
@@ -1047,6 +1076,7 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
     if (out_ld) NFFT_GP_SUB(true, 32) else NFFT_GP_SUB(false, 32)
   }
 #undef NFFT_GP_SUB
+#undef NFFT_GP_SUBW
 #undef NFFT_GP_LAUNCH
   // blocks that overflowed the staging buffers: recompute them with the chunked kernel
   if (cached_any) NFFT_CHECK(gather_fallback(g, n, win, H, batch, f, sub, mode, out, st, H_ld, sub_ld, out_ld, overflow));
