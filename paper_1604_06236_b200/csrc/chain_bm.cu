@@ -868,8 +868,10 @@ __global__ void __launch_bounds__(2 * fast_threads<2 * C, kSig>(), 1) kbm_pad_hp
 
 // XOUT: the tile also stores x (coalesced rows), so the last pass of the
 // C-point FFT keeps the column-fast mapping and is followed by a CTA barrier.
-template <int R, int C, bool XOUT>
-__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_pad_h(
+// TST: the padded grid Y leaves through the TMA unit (dense rows written in
+// place by the last pass, bulk tensor stores of <= 256 rows; see kbm_pad_hs).
+template <int R, int C, bool XOUT, bool TST>
+__device__ __forceinline__ void pad_h_body(double2* sm, const CUtensorMap* tmY,
     const double2* __restrict__ Z, double2* __restrict__ Y, int64_t Bp, const double2* __restrict__ twR,
     const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
     const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
@@ -880,7 +882,7 @@ __global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_thre
   using TrA = HalfTr<C>;
   using TrB = FastTraits<NC>;
   constexpr bool kLead2 = TrB::radix(0) == 2;
-  extern __shared__ double2 sm[];
+  static_assert(!TST || kLead2, "TMA-store form: power-of-two tiles");
   double* s_t0 = reinterpret_cast<double*>(sm + NC * SG);
   double* s_t1 = s_t0 + C;
   double2* s_xs = reinterpret_cast<double2*>(s_t1 + C);
@@ -936,12 +938,46 @@ __global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_thre
   else __syncwarp();
   auto st2 = [&](int k, int c, double2 v) { Yt[(unsigned)(k * R) * ub + c] = v; };
   const FourStepTw<+1> pt{loN, hiN, sN, twQ, Q, r, 0};
-  if constexpr (kLead2) {
+  if constexpr (TST) {
+    auto st3 = [&](int k, int c, double2 v) { sm[(k << 3) + c] = v; };
+    hyb_tile_fft_from<NC, +1, TrB, hyb_mask<TrB>(false, true), 1, 2, decltype(st3), FourStepTw<+1>, CtaSync, true>(
+        sm, st3, twC, pt);
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      constexpr int BOX = NC < 256 ? NC : 256;
+#pragma unroll
+      for (int k0 = 0; k0 < NC; k0 += BOX) tma_store_3d(tmY, (int)(2 * b0), r, k0, sm + k0 * kSig);
+      tma_store_commit();
+      tma_store_wait_read();
+    }
+  } else if constexpr (kLead2) {
     hyb_tile_fft_from<NC, +1, TrB, hyb_mask<TrB>(false, true), 1, 2>(sm, st2, twC, pt);
   } else {
     auto ld2 = [&](int i, int c) -> double2 { return sm[hidx(i, c)]; };
     hyb_tile_fft<NC, +1, TrB, hyb_mask<TrB>(false, true), true, false>(sm, ld2, st2, twC, pt);
   }
+}
+
+template <int R, int C, bool XOUT>
+__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_pad_h(
+    const double2* __restrict__ Z, double2* __restrict__ Y, int64_t Bp, const double2* __restrict__ twR,
+    const double2* __restrict__ twC, const double2* __restrict__ loN, const double2* __restrict__ hiN, int sN,
+    const double2* __restrict__ twQ, int Q, const double* __restrict__ coef, const double* __restrict__ deconv,
+    const double* __restrict__ cd, const double2* __restrict__ xsub, double2* __restrict__ xout) {
+  extern __shared__ double2 sm[];
+  pad_h_body<R, C, XOUT, false>(sm, nullptr, Z, Y, Bp, twR, twC, loN, hiN, sN, twQ, Q, coef, deconv, cd, xsub, xout);
+}
+template <int R, int C, bool XOUT>
+__global__ void __launch_bounds__(fast_threads<2 * C, kSig>(), bm_minb(fast_threads<2 * C, kSig>())) kbm_pad_hst(
+    const __grid_constant__ CUtensorMap tmY, const double2* __restrict__ Z, double2* __restrict__ Y, int64_t Bp,
+    const double2* __restrict__ twR, const double2* __restrict__ twC, const double2* __restrict__ loN,
+    const double2* __restrict__ hiN, int sN, const double2* __restrict__ twQ, int Q, const double* __restrict__ coef,
+    const double* __restrict__ deconv, const double* __restrict__ cd, const double2* __restrict__ xsub,
+    double2* __restrict__ xout) {
+  extern __shared__ __align__(128) double2 sm_hs[];
+  if constexpr (FastTraits<2 * C>::radix(0) == 2)
+    pad_h_body<R, C, XOUT, true>(sm_hs, &tmY, Z, Y, Bp, twR, twC, loN, hiN, sN, twQ, Q, coef, deconv, cd, xsub, xout);
 }
 
 // First-pass hook of the TMA-staged kernels: wait for the cp.async table
@@ -1557,6 +1593,17 @@ struct ChainBM {
       const int64_t Q = n / last_stride<2 * C>();
       const double2* twQ = nullptr;
       NFFT_CHECK(qtab(Q, &twQ));
+      if constexpr (FastTraits<2 * C>::radix(0) == 2) {
+        if (tma_st()) {  // the padded grid through bulk tensor stores
+          auto bm_pad = kbm_pad_hst<R, C, XOUT>;
+          NFFT_CHECK(bm_attr(bm_pad, smem));
+          CUtensorMap tm;
+          NFFT_CHECK(tma_map_strided(&tm, Y, 2 * C, R, Bp, 2 * C < 256 ? 2 * C : 256, kSig));
+          LAUNCH_PDL(bm_pad, dim3(groups, (unsigned)R), T, smem, st, tm, Z, Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi,
+                     t.tN->s, twQ, (int)Q, pv.tcoef, pv.tdeconv, pv.tcd, xsub, xout);
+          return NFFT45_OK;
+        }
+      }
       LAUNCH_PDL(bm_pad, dim3(groups, (unsigned)R), T, smem, st, Z, Y, Bp, t.twC, t.tw2C, t.tN->lo, t.tN->hi, t.tN->s,
                  twQ, (int)Q, pv.tcoef, pv.tdeconv, pv.tcd, xsub, xout);
     }
