@@ -127,12 +127,13 @@ def main(lpath, fpath, tag, steps, config="c4"):
                "kc_pad": "chain_pad", "kc_row": "chain_row", "k_spread_s": "spread_s1",
                "k_gather_s": "gather_s1"}
         base = k.split("<")[0]
-        for suf in ("_hf", "_hp", "_h"):  # hybrid / fused / persistent variants report under the stage's name
+        for suf in ("_hst", "_hs", "_hf", "_hp", "_h"):  # hybrid / fused / persistent / TMA-store variants report under the stage's name
             if base.startswith("kbm_") and base.endswith(suf):
                 base = base[: -len(suf)]
                 break
         key = key.get(base, base)
-        short[key] = sum(v) / len(v)
+        short.setdefault(key, []).extend(v)
+    short = {k: sum(v) / len(v) for k, v in short.items()}  # mean over all launches of the stage
     json.dump(short, open(os.path.join(REPO, "profiles", f"traffic_{config}.json"), "w"), indent=1)
     print(json.dumps(short, indent=1))
 
