@@ -261,8 +261,15 @@ __global__ void __launch_bounds__(256, 2) k_spread_b(const double* __restrict__ 
 // per group (weights recomputed), same arithmetic order.
 constexpr int kPipeCap = 64;
 
+// SPL = 2 (64-signal groups, two signals per lane): the weight rows, node
+// factors and active-node entries a warp loads per node feed twice the FMAs
+// (the kernel is bound by the L1's LSU data pipe and by issue slots, not by
+// the fp64 pipe).  To keep two CTAs per SM the amplitudes are SINGLE-buffered
+// (64 KB per group) — the next group's cp.async copies are issued once every
+// warp has finished the FMAs and fly during the stores — and the FMA loop
+// takes one node at a time (128 registers).
 template <int SPL, bool NB>  // NB: signal-major amplitudes, node-blocked staging layout (swz_nb)
-__global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double* __restrict__ ts, const int* __restrict__ perm,
+__global__ void __launch_bounds__(256, 2) k_spread_p(const double* __restrict__ ts, const int* __restrict__ perm,
                                                     int64_t Q, int64_t n, double alpha, GaussTab G,
                                                     const double2* __restrict__ amp, int64_t batch, NodeFactor nf,
                                                     double2* __restrict__ H, const int2* __restrict__ ranges, int NS,
@@ -272,7 +279,8 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
   constexpr int SIG = 32 * SPL;
   extern __shared__ __align__(16) unsigned char smraw[];
   double2* A0 = reinterpret_cast<double2*>(smraw);                        // [cap][SIG]
-  double2* A1 = A0 + kPipeCap * SIG;                                      // [cap][SIG]
+  constexpr bool DB = SPL == 1;                                           // double-buffered amplitudes
+  double2* A1 = DB ? A0 + kPipeCap * SIG : A0;                            // [cap][SIG]
   double* W = reinterpret_cast<double*>(A1 + kPipeCap * SIG);             // [cap][kWRow]
   double2* F = reinterpret_cast<double2*>(W + kPipeCap * kWRow);          // [cap]
   int* Cc2 = reinterpret_cast<int*>(F + kPipeCap);                        // [cap]
@@ -392,7 +400,7 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
 #pragma unroll
     for (int s2 = 0; s2 < SPL; s2++) sw[s2] = lane + 32 * s2;
     int k = 0;
-    for (; k + 1 < na; k += 2) {
+    for (; SPL == 1 && k + 1 < na; k += 2) {
       const int2 n0 = act[k], n1 = act[k + 1];
       const double2* w0 = reinterpret_cast<const double2*>(W + n0.y);
       const double2* w1 = reinterpret_cast<const double2*>(W + n1.y);
@@ -417,7 +425,7 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
         }
       }
     }
-    if (k < na) {
+    for (; k < na; k++) {
       const int2 n0 = act[k];
       const double2* w0 = reinterpret_cast<const double2*>(W + n0.y);
       const double2 a01 = w0[0], a23 = w0[1], a45 = w0[2], a67 = w0[3];
@@ -462,6 +470,22 @@ __global__ void __launch_bounds__(256, SPL == 1 ? 2 : 1) k_spread_p(const double
     compact(total);
     int64_t g = by;
     if (g < ngroups) stage(A0, g, total);
+    if constexpr (!DB) {
+      for (; g < ngroups; g += gy) {
+        cp_async_wait_group<0>();
+        __syncthreads();
+        double2 acc[kCPW][SPL];
+#pragma unroll
+        for (int c = 0; c < kCPW; c++)
+#pragma unroll
+          for (int s2 = 0; s2 < SPL; s2++) acc[c][s2] = make_double2(0.0, 0.0);
+        accumulate(A0, total, acc);
+        __syncthreads();  // every warp has consumed A0: refill it while the results are stored
+        if (g + gy < ngroups) stage(A0, g + gy, total);
+        store(g, acc);
+      }
+      return;
+    }
     for (int it = 0; g < ngroups; it++, g += gy) {
       double2* cur = (it & 1) ? A1 : A0;
       double2* nxt = (it & 1) ? A0 : A1;
@@ -512,15 +536,20 @@ int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const doubl
   const int2* ranges = nullptr;
   int2* own = nullptr;
   NFFT_CHECK(tile_ranges(g, n, win.m, kSpreadTile, NS, st, &ranges, &own));
-  constexpr int SIG = 32;
+  // 64-signal groups (two signals per lane, single-buffered amplitudes) from 256 signals up: measured
+  // -7.6 % at 1024 signals, -6 % at 512, equal at 128, slower below (half as many CTAs); NFFT45_SPREAD_SPL=1|2 forces
+  static const int spl_env = getenv("NFFT45_SPREAD_SPL") ? atoi(getenv("NFFT45_SPREAD_SPL")) : 0;
+  const int spl = spl_env == 1 || spl_env == 2 ? spl_env : (H_ld >= 256 ? 2 : 1);
+  const int SIG = 32 * spl;
   const int ngroups = (int)ceil_div(H_ld, SIG);
   // enough CTAs for ~2 waves of 148 SMs, each walking several signal groups
   int slices = (int)std::min<int64_t>(ngroups, std::max<int64_t>(1, ceil_div(4 * 148, ntiles)));
   static const int env_sl = getenv("NFFT45_SPREAD_SLICES") ? atoi(getenv("NFFT45_SPREAD_SLICES")) : 0;
   const int sw = env_sl > 0;
   if (env_sl > 0) slices = (int)std::min<int64_t>(ngroups, env_sl);
-  size_t smem = (size_t)2 * kPipeCap * SIG * 16 + (size_t)kPipeCap * kWRow * 8 + kPipeCap * 16 + kPipeCap * 16;
+  size_t smem = (size_t)(spl == 1 ? 2 : 1) * kPipeCap * SIG * 16 + (size_t)kPipeCap * kWRow * 8 + kPipeCap * 16 + kPipeCap * 16;
   auto spread_p = amp_ld == 0 ? k_spread_p<1, true> : k_spread_p<1, false>;
+  if (spl == 2) spread_p = amp_ld == 0 ? k_spread_p<2, true> : k_spread_p<2, false>;
   NFFT_CUDA(cudaFuncSetAttribute(spread_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const dim3 grid = sw ? dim3((unsigned)slices, (unsigned)ntiles) : dim3((unsigned)ntiles, (unsigned)slices);
   LAUNCH_PDL(spread_p, grid, 256, smem, st, g.ts, g.perm, g.Q, n, win.alpha, gauss_tab(win), amp, batch, f, H, ranges,

@@ -599,7 +599,10 @@ def test_kernel_variants_bitwise(tmp_path):
                 {"NFFT45_TMAST": "0"}, {"NFFT45_TMAST": "2"},
                 # persistent gather with 8 warps x 4 nodes on 32-signal groups (the default from 512
                 # signals up) forced on for these small, ragged batches
-                {"NFFT45_GATHER_WARPS": "8"})
+                {"NFFT45_GATHER_WARPS": "8"},
+                # pipelined spreading on 64-signal groups (two signals per lane, single-buffered
+                # amplitudes; the default from 256 signals up) forced on for these small batches
+                {"NFFT45_SPREAD_SPL": "2"})
     outs = []
     for i, extra in enumerate(variants):
         f = tmp_path / f"v{i}.npz"
