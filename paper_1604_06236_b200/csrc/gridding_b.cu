@@ -822,7 +822,7 @@ constexpr int kGPSpanS = 96;  // short TMA box (rows)
 // per SM although the 32-signal cell tile is twice as large.
 template <int SIG, int WARPS>
 __host__ __device__ constexpr int gp_min_ctas(int subm, bool out_bm) {
-  if (WARPS == 8) return (subm == 2 || !out_bm) ? 2 : 3;
+  if (WARPS == 8) return subm == 2 ? 2 : 3;  // (signal-major outputs transpose through the consumed cell tile)
   return SIG == 32 ? 2 : (SIG == 16 ? 4 : 5);
 }
 template <bool OUT_BM, int SUBM, int SIG, int WARPS = kGatherWarps>  // SUBM: 0 none, 1 batch-minor, 2 signal-major
@@ -841,7 +841,10 @@ __global__ void __launch_bounds__(WARPS * 32, gp_min_ctas<SIG, WARPS>(SUBM, OUT_
   double2* Y = reinterpret_cast<double2*>(smraw_gp);                     // [kGPSpan][SIG]
   double* WT = reinterpret_cast<double*>(Y + kGPSpan * SIG);           // [warps][kWTSpan][8]
   double2* Sb = reinterpret_cast<double2*>(WT + WARPS * kWTSpan * NPW);  // [nodes][SIG] (SUBM == 2)
-  double2* O = Sb + (SUBM == 2 ? kGatherNodes * SIG : 0);              // [nodes][SIG] (!OUT_BM)
+  // [nodes][SIG] transpose tile of signal-major outputs.  With 8 warps it is the (consumed) head of
+  // the cell tile and the next group's prefetch waits for the stores: 73 KB per CTA, 3 CTAs per SM.
+  constexpr bool O_IN_Y = !OUT_BM && WARPS == 8;
+  double2* O = O_IN_Y ? Y : Sb + (SUBM == 2 ? kGatherNodes * SIG : 0);
   __shared__ int s_c0[kGatherNodes];
   __shared__ double s_f[kGatherNodes];
   __shared__ double2 s_fac[kGatherNodes];
@@ -978,7 +981,7 @@ __global__ void __launch_bounds__(WARPS * 32, gp_min_ctas<SIG, WARPS>(SUBM, OUT_
       }
     }
     __syncthreads();  // Y (and Sb) consumed: prefetch the next group during the epilogue
-    if (g + gy < ngroups) stage(g + gy);
+    if (!O_IN_Y && g + gy < ngroups) stage(g + gy);
     if constexpr (OUT_BM) {
       const int64_t b = b0 + sl;
 #pragma unroll
@@ -1010,6 +1013,10 @@ __global__ void __launch_bounds__(WARPS * 32, gp_min_ctas<SIG, WARPS>(SUBM, OUT_
       for (int k = 0; k < SIG / WARPS; k++) {
         const int sig = warp + WARPS * k;
         if (b0 + sig < batch && lane < nq) dst[(int64_t)WARPS * k * Q] = O[lane * SIG + swz(sig, lane)];
+      }
+      if constexpr (O_IN_Y) {
+        __syncthreads();  // the transpose tile is drained: refill the cell tile
+        if (g + gy < ngroups) stage(g + gy);
       }
     }
   }
@@ -1086,7 +1093,8 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
   }
   const int subm = mode == 0 ? 0 : (sub_ld ? 1 : 2);
   size_t smem = (size_t)kGPSpan * SIGu * 16 + (size_t)kGatherWarps * kWTSpan * kNPW * 8 +
-                (subm == 2 ? (size_t)kGatherNodes * SIGu * 16 : 0) + (out_ld ? 0 : (size_t)kGatherNodes * SIGu * 16);
+                (subm == 2 ? (size_t)kGatherNodes * SIGu * 16 : 0) +
+                (out_ld || WARPSu == 8 ? 0 : (size_t)kGatherNodes * SIGu * 16);
   const dim3 grid = sw ? dim3((unsigned)slices, (unsigned)nblk) : dim3((unsigned)nblk, (unsigned)slices);
   GaussTab G = gauss_tab(win);
   // TMA-staged cell tiles (NFFT45_GATHER_TMA=0: per-thread cp.async copies, for A/B runs)
