@@ -883,16 +883,6 @@ __global__ void __launch_bounds__(WARPS * 32, gp_min_ctas<SIG, WARPS>(SUBM, OUT_
   // per-warp dense weight table over the warp's cells, built once
   double* wt = WT + warp * kWTSpan * NPW;
   const int wl = w_hi - w_lo + 1;
-  for (int i = lane; i < wl * NPW; i += 32) wt[i] = 0.0;
-  __syncwarp();
-  if (lane < NPW && warp * NPW + lane < nq) {
-    double w[2 * kM + 1];
-    taps29(s_f[warp * NPW + lane], alpha, G, w);
-    const int c0 = s_c0[warp * NPW + lane] - kM - w_lo;
-#pragma unroll
-    for (int k = 0; k < 2 * kM + 1; k++) wt[(c0 + k) * NPW + lane] = w[k];
-  }
-  __syncwarp();
   const int ni = (int)n;
   // signal-major operands: this thread's node (lane) and first signal (warp)
   const int64_t my_off = (int64_t)warp * Q + (lane < nq ? s_pq[lane] : 0);  // signals warp + WARPS k
@@ -936,6 +926,17 @@ __global__ void __launch_bounds__(WARPS * 32, gp_min_ctas<SIG, WARPS>(SUBM, OUT_
   };
   int64_t g = by;
   if (g < ngroups) stage(g);
+  // (built while the first group's cell tile is in flight)
+  for (int i = lane; i < wl * NPW; i += 32) wt[i] = 0.0;
+  __syncwarp();
+  if (lane < NPW && warp * NPW + lane < nq) {
+    double w[2 * kM + 1];
+    taps29(s_f[warp * NPW + lane], alpha, G, w);
+    const int c0 = s_c0[warp * NPW + lane] - kM - w_lo;
+#pragma unroll
+    for (int k = 0; k < 2 * kM + 1; k++) wt[(c0 + k) * NPW + lane] = w[k];
+  }
+  __syncwarp();
   const double2* __restrict__ yw = Y + (w_lo - cs) * SIG + sl;
   const double2* __restrict__ wr0 = reinterpret_cast<const double2*>(wt) + hf * (NPL / 2);
   const int e0 = warp * NPW + hf * NPL;  // node of acc[0]
