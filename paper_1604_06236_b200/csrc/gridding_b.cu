@@ -1054,9 +1054,10 @@ __global__ void k_overflow_clear(int* f, int64_t n) {
   if (i < n) f[i] = 0;
 }
 
-// 32-signal groups waste lanes on the last group of small batches: and their cell tiles leave fewer groups per walker: measured faster from 512 signals up (slower at 128 / 256)
+// 32-signal groups waste lanes on the last group of small batches; measured faster from 32 signals up
+// once a walker keeps 8 or more groups (see `slices`), equal at 48: the default from 64 signals
 static bool gather_w8_default(int64_t nsig) {
-  static const int64_t min_sig = getenv("NFFT45_GATHER_W8_MIN") ? atoll(getenv("NFFT45_GATHER_W8_MIN")) : 512;
+  static const int64_t min_sig = getenv("NFFT45_GATHER_W8_MIN") ? atoll(getenv("NFFT45_GATHER_W8_MIN")) : 64;
   return nsig >= min_sig;
 }
 
@@ -1079,8 +1080,9 @@ int gather_persistent(const GridDev& g, int64_t n, const Window& win, const doub
   const int ngroups = (int)ceil_div(out_ld ? out_ld : batch, SIGu);
   // at least 4 signal-group walkers per node block, walkers fastest in the
   // grid (concurrent CTAs then read 4 groups of each cell row: -4 % on C4)
-  // (the 8-warp layout amortises its per-block setup over more groups: 2 walkers, -1.3 %)
-  int slices = (int)std::min<int64_t>(ngroups, std::max<int64_t>(w8 ? 2 : 4, ceil_div(4 * 148, nblk)));
+  // (the 8-warp layout wants its per-block setup amortised over 8 or more groups: one or two walkers)
+  int slices = (int)std::min<int64_t>(
+      ngroups, std::max<int64_t>(w8 ? std::max(1, std::min(2, ngroups / 8)) : 4, ceil_div(4 * 148, nblk)));
   static const int env_sl = getenv("NFFT45_GATHER_SLICES") ? atoi(getenv("NFFT45_GATHER_SLICES")) : 0;
   const int sw = 1;
   if (env_sl > 0) slices = (int)std::min<int64_t>(ngroups, env_sl);

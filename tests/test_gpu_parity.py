@@ -597,7 +597,7 @@ def test_kernel_variants_bitwise(tmp_path):
                 # outputs of the fused pad / mid kernels by per-thread global stores instead of bulk
                 # tensor stores (TMA), and the band kernel's output through the TMA unit as well
                 {"NFFT45_TMAST": "0"}, {"NFFT45_TMAST": "2"},
-                # persistent gather with 8 warps x 4 nodes on 32-signal groups (the default from 512
+                # persistent gather with 8 warps x 4 nodes on 32-signal groups (the default from 64
                 # signals up) forced on for these small, ragged batches
                 {"NFFT45_GATHER_WARPS": "8"},
                 # pipelined spreading on 64-signal groups (two signals per lane, single-buffered
