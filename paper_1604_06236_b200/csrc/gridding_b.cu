@@ -549,10 +549,10 @@ int spread_pipelined(const GridDev& g, int64_t n, const Window& win, const doubl
   const int2* ranges = nullptr;
   int2* own = nullptr;
   NFFT_CHECK(tile_ranges(g, n, win.m, kSpreadTile, NS, st, &ranges, &own));
-  // 64-signal groups (two signals per lane, single-buffered amplitudes) from 256 signals up: measured
-  // -7.6 % at 1024 signals, -6 % at 512, equal at 128, slower below (half as many CTAs); NFFT45_SPREAD_SPL=1|2 forces
+  // 64-signal groups (two signals per lane, single-buffered amplitudes) from 128 signals up: measured
+  // -7.6 % at 1024 signals, -6 % at 512, -7 % at 128 / 192, +2 % at 64; NFFT45_SPREAD_SPL=1|2 forces
   static const int spl_env = getenv("NFFT45_SPREAD_SPL") ? atoi(getenv("NFFT45_SPREAD_SPL")) : 0;
-  const int spl = spl_env == 1 || spl_env == 2 ? spl_env : (H_ld >= 256 ? 2 : 1);
+  const int spl = spl_env == 1 || spl_env == 2 ? spl_env : (H_ld >= 128 ? 2 : 1);
   const int SIG = 32 * spl;
   const int ngroups = (int)ceil_div(H_ld, SIG);
   // enough CTAs for ~2 waves of 148 SMs, each walking several signal groups

@@ -601,7 +601,7 @@ def test_kernel_variants_bitwise(tmp_path):
                 # signals up) forced on for these small, ragged batches
                 {"NFFT45_GATHER_WARPS": "8"},
                 # pipelined spreading on 64-signal groups (two signals per lane, single-buffered
-                # amplitudes; the default from 256 signals up) forced on for these small batches
+                # amplitudes; the default from 128 signals up) forced on for these small batches
                 {"NFFT45_SPREAD_SPL": "2"})
     outs = []
     for i, extra in enumerate(variants):
