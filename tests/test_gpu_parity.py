@@ -186,6 +186,35 @@ def test_c4_full_size_1024x65536_properties():
     assert float(torch.linalg.norm(got - want) / torch.linalg.norm(want)) <= 1e-12
 
 
+def test_c4_shape_repeatable_and_row_independent():
+    """Race canary for the kernels that reuse live shared memory (compute-sanitizer is closed
+    on the pool): at the C4 kernel shape with enough signals for the 64-signal spreading groups,
+    the 8-warp gather (transpose tile aliased onto the consumed cell tile) and the bulk tensor
+    stores (dense rows written in place in the tile buffer), ten solves of the same operands
+    give bitwise the same outputs, a signal's result does not depend on which other signals
+    share its groups / tiles (rows of a 200-signal batch vs the same rows in a 131-signal
+    batch), and rows 0 / last agree with the oracle."""
+    P, B = 1 << 16, 200
+    t, data = O.make_inputs(P, 0.3, 8, 16044)
+    rng = np.random.default_rng(99)
+    data = (rng.standard_normal((B, P)) + 1j * rng.standard_normal((B, P))) / np.sqrt(2)
+    prm = nf.MethodParams.from_mu(1e-15, P, 2)
+    plan = nf.build_plan(nf.validate_grid(t), prm)
+    d = torch.from_numpy(data).cuda()
+    x5 = nf.refine_type5(plan, d, passes=1)
+    x4 = nf.refine_type4(plan, d, passes=1)
+    for _ in range(9):
+        assert torch.equal(x5, nf.refine_type5(plan, d, passes=1))
+        assert torch.equal(x4, nf.refine_type4(plan, d, passes=1))
+    sub = d[69:200].contiguous()  # 131 signals: other group / tile neighbours, ragged tail
+    assert torch.equal(x5[69:200], nf.refine_type5(plan, sub, passes=1))
+    assert torch.equal(x4[69:200], nf.refine_type4(plan, sub, passes=1))
+    oplan = O.Plan.build(t, prm.damping_a, 2)
+    for r in (0, B - 1):
+        assert rel(O.refine5(oplan, data[r], 1), x5[r].cpu().numpy()) <= G1
+        assert rel(O.refine4(oplan, data[r], 1), x4[r].cpu().numpy()) <= G1
+
+
 def test_c3_single_2_20():
     _check_config(1 << 20, 0.4, 1, 16043, passes=(1,))
 
