@@ -30,6 +30,13 @@
 #include "ops.cuh"
 #include "tma.cuh"
 
+// The file is compiled as TWO translation units (Makefile: -DNFFT45_BM_PART=1 / 2) so that the
+// per-size instantiations of the chains build in parallel: part 1 holds the R = C sizes, the host
+// helpers and the dispatch; part 2 the R = 2C and 3 * 2^k sizes.  Undefined: one unit with everything.
+#ifndef NFFT45_BM_PART
+#define NFFT45_BM_PART 0
+#endif
+
 namespace nfft45 {
 
 namespace {
@@ -1199,7 +1206,7 @@ __global__ void __launch_bounds__(fast_threads<C, 4 * RW>(), bm_minb(fast_thread
 // 2C (KK = 2: 32-byte runs on the signal-major side, 64-byte runs on the batch-minor side).
 //
 // deconvolution weights of the band p < P of the n = 2P grid (gridding.py:90), once per call
-__global__ void k_fwd_deconv(double* __restrict__ d, int64_t P, double wb) {
+static __global__ void k_fwd_deconv(double* __restrict__ d, int64_t P, double wb) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p < P) d[p] = deconv_weight(p, P / 2, 2 * P, wb);
 }
@@ -1306,6 +1313,7 @@ template __global__ void kbm_pad_h<NFFT45_EXP_RC, true>(const double2*, double2*
 #else
 // ------------------------------------------------------------ host side
 
+#if NFFT45_BM_PART != 2
 using TmaEncode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1356,6 +1364,8 @@ int tma_map_rows(CUtensorMap* map, const void* base, int64_t rows, int64_t Bp, i
   }
   return NFFT45_OK;
 }
+
+#endif  // NFFT45_BM_PART != 2
 
 template <typename K>
 static int bm_attr(K kernel, size_t bytes) {
@@ -1903,6 +1913,41 @@ static int forward_solve_bm(const GridDev& g, int kind, const double2* in, int64
   return status;
 }
 
+// ---- part 2: the R = 2C and 3 * 2^k sizes (their own translation unit when NFFT45_BM_PART is set)
+int forward_solve_bm_part2(const GridDev& g, int kind, const double2* in, int64_t batch, const double2* sub,
+                           double2* out, cudaStream_t st);
+int chain_solve_bm_part2(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes,
+                         double2* out, double* norms, cudaStream_t st);
+#if NFFT45_BM_PART != 1
+int forward_solve_bm_part2(const GridDev& g, int kind, const double2* in, int64_t batch, const double2* sub,
+                           double2* out, cudaStream_t st) {
+  switch (g.Q) {
+    case 2048: return forward_solve_bm<64, 32>(g, kind, in, batch, sub, out, st);
+    case 8192: return forward_solve_bm<128, 64>(g, kind, in, batch, sub, out, st);
+    case 32768: return forward_solve_bm<256, 128>(g, kind, in, batch, sub, out, st);
+    case 131072: return forward_solve_bm<512, 256>(g, kind, in, batch, sub, out, st);
+  }
+  return NFFT45_ERR_INVALID_ARGUMENT;
+}
+int chain_solve_bm_part2(const ChainPlanView& pv, int kind, const double2* data, int64_t batch, int passes,
+                         double2* out, double* norms, cudaStream_t st) {
+  switch (pv.P) {
+    case 2048: return chain_solve_bm<64, 32>(pv, kind, data, batch, passes, out, norms, st);
+    case 8192: return chain_solve_bm<128, 64>(pv, kind, data, batch, passes, out, norms, st);
+    case 32768: return chain_solve_bm<256, 128>(pv, kind, data, batch, passes, out, norms, st);
+    case 131072: return chain_solve_bm<512, 256>(pv, kind, data, batch, passes, out, norms, st);
+    case 524288: return chain_solve_bm<1024, 512>(pv, kind, data, batch, passes, out, norms, st);
+    case 3072: return chain_solve_bm<48, 64>(pv, kind, data, batch, passes, out, norms, st);
+    case 12288: return chain_solve_bm<96, 128>(pv, kind, data, batch, passes, out, norms, st);
+    case 49152: return chain_solve_bm<192, 256>(pv, kind, data, batch, passes, out, norms, st);
+    case 196608: return chain_solve_bm<384, 512>(pv, kind, data, batch, passes, out, norms, st);
+    case 786432: return chain_solve_bm<768, 1024>(pv, kind, data, batch, passes, out, norms, st);
+  }
+  return NFFT45_ERR_INVALID_ARGUMENT;
+}
+#endif  // NFFT45_BM_PART != 1
+
+#if NFFT45_BM_PART != 2
 bool forward_bm_usable(int64_t Q, int64_t P, int m, int64_t batch) {
   static const bool off = getenv("NFFT45_NO_FORWARD_BM") != nullptr;  // A/B switch: generic batched forward path
   int r = 0, c = 0;
@@ -1923,15 +1968,11 @@ int forward_run_bm(const GridDev& g, int kind, const double2* in, int64_t batch,
   }
   switch (g.Q) {
     case 1024: return forward_solve_bm<32, 32>(g, kind, in, batch, sub, out, st);
-    case 2048: return forward_solve_bm<64, 32>(g, kind, in, batch, sub, out, st);
     case 4096: return forward_solve_bm<64, 64>(g, kind, in, batch, sub, out, st);
-    case 8192: return forward_solve_bm<128, 64>(g, kind, in, batch, sub, out, st);
     case 16384: return forward_solve_bm<128, 128>(g, kind, in, batch, sub, out, st);
-    case 32768: return forward_solve_bm<256, 128>(g, kind, in, batch, sub, out, st);
     case 65536: return forward_solve_bm<256, 256>(g, kind, in, batch, sub, out, st);
-    case 131072: return forward_solve_bm<512, 256>(g, kind, in, batch, sub, out, st);
   }
-  return NFFT45_ERR_INVALID_ARGUMENT;
+  return forward_solve_bm_part2(g, kind, in, batch, sub, out, st);
 }
 
 bool chain_bm_hybrid_factors(int64_t P, int* R, int* C) {
@@ -1986,24 +2027,15 @@ int chain_run_bm(const ChainPlanView& pv, int kind, const double2* data, int64_t
   }
   switch (pv.P) {
     case 1024: return chain_solve_bm<32, 32>(pv, kind, data, batch, passes, out, norms, st);
-    case 2048: return chain_solve_bm<64, 32>(pv, kind, data, batch, passes, out, norms, st);
     case 4096: return chain_solve_bm<64, 64>(pv, kind, data, batch, passes, out, norms, st);
-    case 8192: return chain_solve_bm<128, 64>(pv, kind, data, batch, passes, out, norms, st);
     case 16384: return chain_solve_bm<128, 128>(pv, kind, data, batch, passes, out, norms, st);
-    case 32768: return chain_solve_bm<256, 128>(pv, kind, data, batch, passes, out, norms, st);
     case 65536: return chain_solve_bm<256, 256>(pv, kind, data, batch, passes, out, norms, st);
-    case 131072: return chain_solve_bm<512, 256>(pv, kind, data, batch, passes, out, norms, st);
     case 262144: return chain_solve_bm<512, 512>(pv, kind, data, batch, passes, out, norms, st);
-    case 524288: return chain_solve_bm<1024, 512>(pv, kind, data, batch, passes, out, norms, st);
     case 1048576: return chain_solve_bm<1024, 1024>(pv, kind, data, batch, passes, out, norms, st);
-    case 3072: return chain_solve_bm<48, 64>(pv, kind, data, batch, passes, out, norms, st);
-    case 12288: return chain_solve_bm<96, 128>(pv, kind, data, batch, passes, out, norms, st);
-    case 49152: return chain_solve_bm<192, 256>(pv, kind, data, batch, passes, out, norms, st);
-    case 196608: return chain_solve_bm<384, 512>(pv, kind, data, batch, passes, out, norms, st);
-    case 786432: return chain_solve_bm<768, 1024>(pv, kind, data, batch, passes, out, norms, st);
   }
-  return NFFT45_ERR_INVALID_ARGUMENT;
+  return chain_solve_bm_part2(pv, kind, data, batch, passes, out, norms, st);
 }
+#endif  // NFFT45_BM_PART != 2
 #endif  // NFFT45_EXP_ONLY
 
 }  // namespace nfft45
