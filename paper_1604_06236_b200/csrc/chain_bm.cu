@@ -125,6 +125,39 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<
   fast_tile_fft<L, kSig, S, true>(sm, ld, st, tw, pt);
 }
 
+// kbm_col on the unpadded swizzled tile of the hybrid kernels (all passes column-fast: same
+// butterflies and twiddles, bitwise identical) with the output leaving through the TMA unit: the
+// last pass writes dense rows in place (ROWST), one thread stores L <= 256 rows k1 L2 + n2.
+template <int L, int S>
+__global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<L, kSig>())) kbm_col_s(
+    const __grid_constant__ CUtensorMap tmO, const double2* __restrict__ in, int L2, int64_t Bp,
+    const double2* __restrict__ tw, const double2* __restrict__ lo, const double2* __restrict__ hi, int sh,
+    const double2* __restrict__ twQ, int Q, int perm) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
+  static_assert(L <= 256 && hyb_ok<L>(), "one TMA box, hybrid tile");
+  extern __shared__ __align__(128) double2 sm_hs[];
+  double2* sm = sm_hs;
+  const int n2 = blockIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * kSig;
+  const unsigned ub = (unsigned)Bp;
+  const double2* __restrict__ it =
+      in + (perm ? (int64_t)(n2 / perm) * L * perm + n2 % perm : (int64_t)n2) * Bp + b0;
+  const int istep = perm ? perm : L2;
+  auto ld = [&](int i, int c) -> double2 { return it[(unsigned)(i * istep) * ub + c]; };
+  auto st = [&](int k1, int c, double2 v) { sm[(k1 << 3) + c] = v; };
+  const FourStepTw<S> pt{lo, hi, sh, twQ, Q, n2, 0};
+  using Tr = FastTraits<L>;
+  hyb_passes<L, S, 0, 1, Tr, 0x0u, false, false, 0, decltype(ld), decltype(st), FourStepTw<S>, NoHook, Tr::np, CtaSync,
+             true>(sm, ld, st, tw, pt, NoHook());
+  fence_proxy_async();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_3d(&tmO, (int)(2 * b0), n2, 0, sm);
+    tma_store_commit();
+    tma_store_wait_read();
+  }
+}
+
 // row FFT_2P (row k1 < R, length 2C) -> band p = k1 + R m1 (m1 < C) with
 // deconv*decay (or (X deconv - sub) decay) -> column IFFT_P (length C) ->
 // W_P^{+k1 k1'} -> U[(k1' R + k1)][b].
@@ -1146,6 +1179,33 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<
   fast_tile_fft<L, kSig, S, true>(sm, ld, st, tw);
 }
 
+// kbm_row on the unpadded swizzled tile with the output through the TMA unit (see kbm_col_s).
+template <int L, int S>
+__global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<L, kSig>())) kbm_row_s(
+    const __grid_constant__ CUtensorMap tmO, const double2* __restrict__ in, int64_t Bp,
+    const double2* __restrict__ tw) {
+  pdl_enter();  // programmatic dependent launch: wait for the producer grid
+  static_assert(L <= 256 && hyb_ok<L>(), "one TMA box, hybrid tile");
+  extern __shared__ __align__(128) double2 sm_hs[];
+  double2* sm = sm_hs;
+  const int r = blockIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * kSig;
+  const unsigned ub = (unsigned)Bp;
+  const double2* __restrict__ it = in + (int64_t)r * L * Bp + b0;
+  auto ld = [&](int i, int c) -> double2 { return it[(unsigned)i * ub + c]; };
+  auto st = [&](int k, int c, double2 v) { sm[(k << 3) + c] = v; };
+  using Tr = FastTraits<L>;
+  hyb_passes<L, S, 0, 1, Tr, 0x0u, false, false, 0, decltype(ld), decltype(st), NoPostTw, NoHook, Tr::np, CtaSync, true>(
+      sm, ld, st, tw, NoPostTw(), NoHook());
+  fence_proxy_async();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_3d(&tmO, (int)(2 * b0), r, 0, sm);
+    tma_store_commit();
+    tma_store_wait_read();
+  }
+}
+
 // Boundary, type-4 input: signal-major A[b][P] -> column IFFT_P (length C,
 // columns k = RW blockIdx.x + (c % RW) of the p = k + R m layout, signals
 // b = 4 blockIdx.y + c / RW) * decay -> batch-minor U; optionally also a
@@ -1391,6 +1451,12 @@ struct ChainBM {
   int pf = 0;                // L2 prefetch distance in launch slots (0: off)
   bool hyb = false;          // hybrid two-FFT kernels (warp-local middle passes), when bm_hyb<R, C>()
   bool fuse = true;          // register handoff between the two transforms of band / mid (NFFT45_FUSE=0: off)
+  // FFT_2P / IFFT_2P passes on the hybrid tile with TMA-stored output: bit 0 column pass, bit 1 row
+  // pass (NFFT45_PASS_TMAST; A/B and the variant test)
+  static int pass_tma() {
+    static const int on = getenv("NFFT45_PASS_TMAST") ? atoi(getenv("NFFT45_PASS_TMAST")) : 1;
+    return on;
+  }
   // outputs of the fused hybrid kernels through bulk tensor stores: 1 (default) pad and mid, 2 also
   // band, 0 off (NFFT45_TMAST; A/B and the variant test)
   static int tma_st() {
@@ -1419,6 +1485,18 @@ struct ChainBM {
     const int64_t Q = n / last_stride<R>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
+    if constexpr (R <= 256 && hyb_ok<R>()) {
+      if ((pass_tma() & 1) && sw && pf == 0) {  // signal groups fastest (the default order), output through the TMA unit
+        auto bm_col = kbm_col_s<R, -1>;
+        constexpr size_t smem_s = sizeof(double2) * R * kSig;
+        NFFT_CHECK(bm_attr(bm_col, smem_s));
+        CUtensorMap tm;
+        NFFT_CHECK(tma_map_strided(&tm, out, R, 2 * C, Bp, R, kSig));
+        LAUNCH_PDL(bm_col, dim3(groups, (unsigned)(2 * C)), T, smem_s, st, tm, in, 2 * C, Bp, t.twR, t.tN->lo, t.tN->hi,
+                   t.tN->s, twQ, (int)Q, perm);
+        return NFFT45_OK;
+      }
+    }
     LAUNCH_PDL(bm_col, gdim(2 * C), T, smem, st, in, out, 2 * C, Bp, t.twR, t.tN->lo, t.tN->hi, t.tN->s, twQ, (int)Q,
            nullptr, (int)sw, pf, perm);
     return NFFT45_OK;
@@ -1635,6 +1713,17 @@ struct ChainBM {
     constexpr size_t smem = fast_smem<R, kSig>();
     NFFT_CHECK(bm_attr(bm_row, smem));
     constexpr int T = fast_threads<R, kSig>();
+    if constexpr (R <= 256 && hyb_ok<R>()) {
+      if ((pass_tma() & 2) && sw && pf == 0) {
+        auto bm_row = kbm_row_s<R, +1>;
+        constexpr size_t smem_s = sizeof(double2) * R * kSig;
+        NFFT_CHECK(bm_attr(bm_row, smem_s));
+        CUtensorMap tm;
+        NFFT_CHECK(tma_map_strided(&tm, H, R, 2 * C, Bp, R, kSig));
+        LAUNCH_PDL(bm_row, dim3(groups, (unsigned)(2 * C)), T, smem_s, st, tm, Y, Bp, t.twR);
+        return NFFT45_OK;
+      }
+    }
     LAUNCH_PDL(bm_row, gdim(2 * C), T, smem, st, Y, H, Bp, (int64_t)(2 * C), t.twR, (int)sw, pf);
     return NFFT45_OK;
   }

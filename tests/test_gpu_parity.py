@@ -631,7 +631,10 @@ def test_kernel_variants_bitwise(tmp_path):
                 {"NFFT45_GATHER_WARPS": "8"},
                 # pipelined spreading on 64-signal groups (two signals per lane, single-buffered
                 # amplitudes; the default from 128 signals up) forced on for these small batches
-                {"NFFT45_SPREAD_SPL": "2"})
+                {"NFFT45_SPREAD_SPL": "2"},
+                # FFT_2P column pass on the padded tile with per-thread stores (default: hybrid tile,
+                # output through the TMA unit), and the IFFT_2P row pass through the TMA unit as well
+                {"NFFT45_PASS_TMAST": "0"}, {"NFFT45_PASS_TMAST": "3"})
     outs = []
     for i, extra in enumerate(variants):
         f = tmp_path / f"v{i}.npz"
