@@ -127,7 +127,7 @@ def main(lpath, fpath, tag, steps, config="c4"):
                "kc_pad": "chain_pad", "kc_row": "chain_row", "k_spread_s": "spread_s1",
                "k_gather_s": "gather_s1"}
         base = k.split("<")[0]
-        for suf in ("_hst", "_hs", "_hf", "_hp", "_h"):  # hybrid / fused / persistent / TMA-store variants report under the stage's name
+        for suf in ("_hst", "_hs", "_hf", "_hp", "_h", "_s"):  # hybrid / fused / persistent / TMA-store variants report under the stage's name
             if base.startswith("kbm_") and base.endswith(suf):
                 base = base[: -len(suf)]
                 break
