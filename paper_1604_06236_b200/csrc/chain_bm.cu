@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<
     const double2* __restrict__ tw, const double2* __restrict__ lo, const double2* __restrict__ hi, int sh,
     const double2* __restrict__ twQ, int Q, int perm) {
   pdl_enter();  // programmatic dependent launch: wait for the producer grid
-  static_assert(L <= 256 && hyb_ok<L>(), "one TMA box, hybrid tile");
+  static_assert(L <= 512 && hyb_ok<L>(), "at most two TMA boxes, hybrid tile");
   extern __shared__ __align__(128) double2 sm_hs[];
   double2* sm = sm_hs;
   const int n2 = blockIdx.y;
@@ -152,7 +152,9 @@ __global__ void __launch_bounds__(fast_threads<L, kSig>(), bm_minb(fast_threads<
   fence_proxy_async();
   __syncthreads();
   if (threadIdx.x == 0) {
-    tma_store_3d(&tmO, (int)(2 * b0), n2, 0, sm);
+    constexpr int BOX = L < 256 ? L : 256;
+#pragma unroll
+    for (int k0 = 0; k0 < L; k0 += BOX) tma_store_3d(&tmO, (int)(2 * b0), n2, k0, sm + k0 * kSig);
     tma_store_commit();
     tma_store_wait_read();
   }
@@ -1485,13 +1487,13 @@ struct ChainBM {
     const int64_t Q = n / last_stride<R>();
     const double2* twQ = nullptr;
     NFFT_CHECK(qtab(Q, &twQ));
-    if constexpr (R <= 256 && hyb_ok<R>()) {
+    if constexpr (R <= 512 && hyb_ok<R>()) {
       if ((pass_tma() & 1) && sw && pf == 0) {  // signal groups fastest (the default order), output through the TMA unit
         auto bm_col = kbm_col_s<R, -1>;
         constexpr size_t smem_s = sizeof(double2) * R * kSig;
         NFFT_CHECK(bm_attr(bm_col, smem_s));
         CUtensorMap tm;
-        NFFT_CHECK(tma_map_strided(&tm, out, R, 2 * C, Bp, R, kSig));
+        NFFT_CHECK(tma_map_strided(&tm, out, R, 2 * C, Bp, R < 256 ? R : 256, kSig));
         LAUNCH_PDL(bm_col, dim3(groups, (unsigned)(2 * C)), T, smem_s, st, tm, in, 2 * C, Bp, t.twR, t.tN->lo, t.tN->hi,
                    t.tN->s, twQ, (int)Q, perm);
         return NFFT45_OK;
